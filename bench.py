@@ -1,0 +1,336 @@
+"""Benchmark: camera frames/s of the fused FFT -> window -> IFFT -> HG-coefficient
+hot path (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config dualpol]
+    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+A step is one pass of the hot path over one batch of synthetic frames already
+resident in HBM (``value``); ``e2e`` is the same metric through the public
+API with pinned HOST frames (host->device copy of the step's frames and the
+device->host read of its coefficients inside the timed region).  Each rank
+processes its own batch (weak scaling; frames are independent, no collective
+on the data path).  L2 is flushed (256 MB write) before every timed step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+LAM, PIX = 1565e-9, 20e-6
+WMAX = np.degrees(LAM / (2 * PIX))
+
+# BASELINE.json configs normalised as in BASELINE.md section 3
+WORKLOADS = {
+    "pr1": dict(frames=dict(width=256, height=256, pol_count=1, batch=16, group_count=9, waist=200e-6,
+                            tilt=(1.0, 1.0), noise="gauss", seed=1),
+                G=9, centres=[[0.0, 0.0], [0.0, 0.0]], nx=128),
+    "dualpol": dict(frames=dict(width=640, height=256, pol_count=2, batch=1000, group_count=14, waist=200e-6,
+                                tilt=(1.2, 0.9), noise="poisson", seed=2),
+                    G=14, centres=[[-160 * PIX, 160 * PIX], [0.0, 0.0]], nx=128),
+    "largeframe": dict(frames=dict(width=1024, height=1024, pol_count=1, batch=256, group_count=20, waist=1e-3,
+                                   tilt=(1.5, 1.5), noise="gauss", zernike_terms=10, seed=3),
+                       G=0, centres=[[0.0, 0.0], [0.0, 0.0]], nx=512),
+    "autoalign": dict(frames=dict(width=320, height=256, pol_count=1, batch=128, group_count=9, waist=200e-6,
+                                  tilt=(1.0, 1.0), noise="gauss", seed=4),
+                      G=9, centres=[[0.0, 0.0], [0.0, 0.0]], nx=128),
+    "largebasis": dict(frames=dict(width=320, height=256, pol_count=1, batch=8192, group_count=45, waist=200e-6,
+                                   tilt=(1.0, 1.0), noise="poisson", seed=5),
+                       G=45, centres=[[0.0, 0.0], [0.0, 0.0]], nx=128),
+}
+
+
+def config_for(name, batch=None):
+    w = WORKLOADS[name]
+    f = dict(w["frames"])
+    if batch:
+        f["batch"] = batch
+    tx, ty = f["tilt"]
+    cfg = dict(frameWidth=f["width"], frameHeight=f["height"], polCount=f["pol_count"], batchCount=f["batch"],
+               framePixelSize=PIX, wavelengthCentre=LAM, fourierWindowRadius=0.32 * WMAX,
+               fftWindowSizeX=w["nx"], fftWindowSizeY=w["nx"], tilt=[[tx, tx], [ty, ty]],
+               beamCentre=w["centres"], basisGroupCount=w["G"], basisWaist=[f["waist"], f["waist"]])
+    return f, cfg
+
+
+def algorithmic_bytes_per_frame(P, nx, ny, gh, gw, M):
+    # window read (f32) + int16 field pair + f32 scale + complex64 coefs
+    return P * (nx * ny * 4 + gh * gw * 4 + 4) + P * M * 8
+
+
+class ClockSampler:
+    """nvidia-smi samples during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i, v in enumerate(r[5:9]) if v.strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference(cfg_dict, frames, min_seconds=10.0, threads=None):
+    """Oracle (reference algorithm restated on numpy/scipy) on a bounded host sample."""
+    import scipy.fft
+    from oracle import holo_oracle as O
+    threads = threads or os.cpu_count() or 1
+    cfg = O.Cfg(**cfg_dict)
+    n = frames.shape[0]
+    with scipy.fft.set_workers(threads):
+        O.run_chain(cfg, frames[: min(n, 4)] if False else frames)  # warm-up (plans, caches)
+        reps, t0 = 0, time.perf_counter()
+        while True:
+            O.run_chain(cfg, frames)
+            reps += 1
+            el = time.perf_counter() - t0
+            if el >= min_seconds:
+                break
+    return reps * n / el, threads, reps, el
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2204_02348_b200.synth import FrameSpec, make_frames
+    sample = min(args.ref_sample, WORKLOADS[args.config]["frames"]["batch"])
+    fspec, cfg = config_for(args.config, batch=sample)
+    frames = make_frames(FrameSpec(**fspec))
+    import scipy.fft
+    from oracle import holo_oracle as O
+    threads = os.cpu_count() or 1
+    ocfg = O.Cfg(**cfg)
+    with scipy.fft.set_workers(threads):
+        for _ in range(max(args.warmup, 1)):
+            O.run_chain(ocfg, frames)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            O.run_chain(ocfg, frames)
+            times.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(times))
+    value = sample / (ms / 1e3)
+    desc = f"{sample} frames of the '{args.config}' workload per step (oracle port of holopipe on {threads} threads)"
+    print(json.dumps({
+        "impl": "reference", "metric": "camera frames/sec (FFT->IFFT->HG coefs)", "value": value,
+        "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": args.config, "frames_per_step": sample, "host_cores": threads},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="dualpol", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--batch", type=int, default=0, help="override frames per step (per GPU)")
+    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="dram read+write bytes per launch from an ncu --set full capture")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+
+    import torch
+    rank, world, local = dist_init(args.gpus)
+    from paper_2204_02348_b200 import api, native
+    from paper_2204_02348_b200.synth import FrameSpec, make_frames
+
+    fspec, cfg = config_for(args.config, batch=args.batch or None)
+    B = fspec["batch"]
+    fspec = dict(fspec, seed=fspec["seed"] * 1000 + rank)
+    frames_host = make_frames(FrameSpec(**fspec))
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    h = api.create_handle()
+    eng = api.engine(h)
+    for k, v in cfg.items():
+        setattr(eng.config, k, v)
+    frames_dev = torch.from_numpy(frames_host).to(dev)
+    api.set_batch(h, B, frames_dev)
+    eng.run_pipeline(0)
+    torch.cuda.synchronize()
+
+    # the timed unit: one fused kernel launch through the C ABI (hpg_run) on device frames
+    P, nx, ny = cfg["polCount"], cfg["fftWindowSizeX"], cfg["fftWindowSizeY"]
+    gh, gw = eng._field_r.shape[-2:]
+    M = eng._mode_count
+    bpf = algorithmic_bytes_per_frame(P, nx, ny, gh, gw, M)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    launch = eng.prepare_launch()   # one hpg_run on the resident frames, arguments pre-built
+    stream_h = native.stream_handle()
+
+    def step():
+        launch.launch(stream_h)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.zero_()
+            starts[i].record()
+            step()
+            ends[i].record()
+        torch.cuda.synchronize()
+    barrier(world)
+    per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms_local = float(np.mean(per_step))
+    ms = max_over_ranks(ms_local, world)
+    value = B * world / (ms / 1e3)
+    achieved = bpf * B / (ms_local / 1e3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+
+    # ---------------- e2e through the public API with pinned host frames
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(frames_host).pin_memory()
+        api.set_batch(h, B, pinned)
+        for _ in range(2):
+            api.process_batch(h)
+        torch.cuda.synchronize()
+        e_ms = []
+        barrier(world)
+        for i in range(max(3, min(args.steps, 10))):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            coefs, b, m, p = api.process_batch(h)       # H2D frames, kernel, D2H coefs
+            e.record()
+            e.synchronize()
+            e_ms.append(s.elapsed_time(e))
+        barrier(world)
+        em = max_over_ranks(float(np.mean(e_ms)), world)
+        e2e = {"value": B * world / (em / 1e3), "unit": "frames/s",
+               "h2d_bytes_per_step": int(frames_host.nbytes), "d2h_bytes_per_step": int(coefs.nbytes),
+               "ms_per_step": em, "path": "api.process_batch (pinned host frames)"}
+        api.set_batch(h, B, frames_dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = min(B, 256)
+        v, threads, reps, el = cpu_reference(cfg | {"batchCount": sample}, frames_host[:sample],
+                                             min_seconds=args.cpu_seconds)
+        cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
+               "sample": f"{sample} frames x {reps} reps ({el:.1f} s) of the same workload; "
+                         f"oracle/holo_oracle.py (numpy+scipy restatement of holopipe)"}
+
+    if rank == 0:
+        line = {
+            "metric": "camera frames/sec (FFT->IFFT->HG coefs)", "value": value, "unit": "frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded HG superposition holograms, BASELINE.md section 3)",
+            "config": {"workload": args.config, "frames_per_step_per_gpu": B, "frame": [fspec["height"], fspec["width"]],
+                       "pols": P, "fft_window": [ny, nx], "field": [int(gh), int(gw)], "modes_per_pol": int(M),
+                       "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": args.traffic_bytes,
+                         "kernel": "holo::fused_kernel", "bytes_per_frame": bpf,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+"""Plane summaries and transfer-matrix metrics (holopipe/analysis.py).
+
+The per-frame reductions run on the GPU (``hpg_run`` with HPG_FLAG_SUMMARY,
+``hpg_plane_summary``, ``hpg_metric_partials``).  What is left for the host is
+the O(rows + cols^2) finish of the nine metrics from the fp64 partial sums:
+logarithms, extrema, and the eigenvalues of the (small) Gram matrix for MDL,
+mirroring holopipe/analysis.py:143-188.  Partials from several GPUs are summed
+(NCCL all-reduce / all-gather) before this finish.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import constants as C
+
+SNR_CAP_DB = 200.0
+_NEG = float(np.finfo(np.float32).min)
+
+
+class AnalysisSummary:
+    """parameters (ANALYSIS_COUNT, polCount, totalCount) float32, summed intensity, axes."""
+
+    def __init__(self, parameters, total_intensity, x_axis, y_axis, plane):
+        self.parameters = parameters
+        self.total_intensity = total_intensity
+        self.x_axis = x_axis
+        self.y_axis = y_axis
+        self.plane = plane
+
+
+def analysis_value(summary, param, pol, idx):
+    v = summary.parameters[param, pol, idx]
+    if param == C.ANALYSIS_MAXABSIDX:
+        return int(np.float32(v).view(np.int32))
+    return float(v)
+
+
+class MetricsReport:
+    """values (METRIC_COUNT, wavelengthCount+1) float32; last slot = average."""
+
+    def __init__(self, wavelength_count=1):
+        self.wavelength_count = int(wavelength_count)
+        self.values = np.full((C.METRIC_COUNT, self.wavelength_count + 1), C.METRIC_UNSET,
+                              dtype=np.float32)
+
+    def get(self, idx):
+        if not (0 <= idx < C.METRIC_COUNT):
+            return 0.0
+        return float(self.values[idx, self.wavelength_count])
+
+    def get_all(self, idx):
+        if not (0 <= idx < C.METRIC_COUNT):
+            return None
+        return self.values[idx].copy()
+
+
+def _db(x):
+    return _NEG if x <= 0 else 10.0 * math.log10(x)
+
+
+def _snr(sig, noise):
+    if sig <= 0:
+        return _NEG
+    if noise <= 0:
+        return SNR_CAP_DB
+    return min(10.0 * math.log10(sig / noise), SNR_CAP_DB)
+
+
+def finish_metrics(row_power, diag_power, group_power, gram, rows, cols, have_labels=True):
+    """Nine metrics from fp64 partials of one transfer matrix (analysis.py:143-188).
+
+    row_power/diag_power/group_power are per virtual row (diag entries < 0 mark
+    rows without a diagonal element); gram is the Hermitian Gram matrix whose
+    top min(rows, cols) eigenvalues are the squared singular values.
+    """
+    v = np.full(C.METRIC_COUNT, C.METRIC_UNSET, dtype=np.float64)
+    if rows == 0 or cols == 0:
+        return v
+    row_power = np.asarray(row_power, np.float64)
+    nd = min(rows, cols)
+    has = np.asarray(diag_power) >= 0
+    d = np.asarray(diag_power, np.float64)[has][:nd]
+    grp = np.asarray(group_power, np.float64)[has][:nd]
+    rowd = row_power[has][:nd]
+    total = float(row_power.sum())
+    v[C.METRIC_IL] = _db(float(row_power.mean()))
+    if total > 0 and gram is not None:
+        ev = np.linalg.eigvalsh(np.asarray(gram, np.complex128))
+        top = ev[-nd:]
+        lo, hi = float(top.min()), float(top.max())
+        if lo > 0:
+            v[C.METRIC_MDL] = 10.0 * math.log10(hi / lo)
+    dt = float(d.sum())
+    v[C.METRIC_DIAG] = _db(dt / nd)
+    v[C.METRIC_SNRAVG] = _snr(dt, total - dt)
+    with np.errstate(divide="ignore"):
+        ddb = np.where(d > 0, 10.0 * np.log10(np.maximum(d, 1e-300)), _NEG)
+    v[C.METRIC_DIAGBEST] = float(ddb.max())
+    v[C.METRIC_DIAGWORST] = float(ddb.min())
+    snr = [_snr(float(d[i]), float(rowd[i] - d[i])) for i in range(nd)]
+    v[C.METRIC_SNRBEST] = max(snr)
+    v[C.METRIC_SNRWORST] = min(snr)
+    if have_labels:
+        sig = float(grp.sum())
+        v[C.METRIC_SNRMG] = _snr(sig, total - sig)
+    else:
+        v[C.METRIC_SNRMG] = v[C.METRIC_SNRAVG]
+    return v
+
+
+def metrics_of_matrix(A, labels=None):
+    """Host metrics of an explicit complex matrix (used for A A^H, analysis.py:124-125)."""
+    A = np.asarray(A, np.complex128)
+    pw = np.abs(A) ** 2
+    R, Cc = A.shape
+    nd = min(R, Cc)
+    rp = pw.sum(axis=1)
+    d = np.full(R, -1.0)
+    d[:nd] = pw[np.arange(nd), np.arange(nd)]
+    grp = d.copy()
+    if labels is not None:
+        lab = np.asarray(labels)
+        grp[:nd] = np.where(lab[:nd, None] == lab[None, :], pw[:nd], 0.0).sum(axis=1)
+    gram = A @ A.conj().T if R <= Cc else A.conj().T @ A
+    return finish_metrics(rp, d, grp, gram, R, Cc, labels is not None)
+
+
+def average_slot(per_wl):
+    """Across-wavelength mean of valid values (analysis.py:243-247)."""
+    per_wl = np.asarray(per_wl, np.float64)
+    L = per_wl.shape[1]
+    rep = MetricsReport(L)
+    rep.values[:, :L] = per_wl.astype(np.float32)
+    for m in range(C.METRIC_COUNT):
+        ok = per_wl[m][per_wl[m] > C.METRIC_UNSET / 2]
+        if ok.size:
+            rep.values[m, L] = np.float32(ok.mean())
+    return rep

@@ -1,0 +1,591 @@
+// C ABI (include/holo_b200.h): plan construction in fp64 on the host, device
+// table upload, workspace sizing and kernel launches.  No exceptions cross the
+// boundary; every entry point returns an hpg_status.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/holo_b200.h"
+#include "holo_internal.h"
+
+namespace holo {
+cudaError_t launch_fused(const RunParams& p, cudaStream_t s);
+cudaError_t launch_finalize(const RunParams& p, float* total, cudaStream_t s);
+cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s);
+cudaError_t launch_fourier_full(const RunParams& p, int64_t F, float2* plane, cudaStream_t s);
+cudaError_t set_smem_limits();
+cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
+                                 const double* ya, float* params, int slots, float* total, char* work,
+                                 int grid, cudaStream_t s);
+}  // namespace holo
+
+using namespace holo;
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+static int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return e == cudaErrorMemoryAllocation ? HPG_MEMORYALLOCATION : HPG_ERROR;
+}
+
+struct hpg_plan {
+  Geometry g;
+  DevTables t;
+  void* dev = nullptr;         // one allocation for every table
+  std::vector<float> xa, ya;   // host copies of the axes
+  std::vector<float> hx, hy;   // host copies of the dequantised basis
+  int device = 0;
+  int num_sms = 148;
+};
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+
+double radians(double deg) { return deg * (kPi / 180.0); }
+
+// round half to even, like Python's round() and numpy.rint
+long long rint_even(double v) { return (long long)std::nearbyint(v); }
+
+double sinc(double x) {
+  if (x == 0.0) return 1.0;
+  const double y = kPi * x;
+  return std::sin(y) / y;
+}
+
+int radix_plan(int n, int* radix) {
+  int e2 = 0, m = n;
+  while (m % 2 == 0) { m /= 2; ++e2; }
+  int e3 = 0;
+  while (m % 3 == 0) { m /= 3; ++e3; }
+  std::vector<int> r;
+  while (e2 >= 4) { r.push_back(16); e2 -= 4; }
+  if (e2 == 3) r.push_back(8);
+  else if (e2 == 2) r.push_back(4);
+  else if (e2 == 1) {
+    if (e3 > 0) { r.push_back(6); --e3; }
+    else r.push_back(2);
+  }
+  for (; e3 > 0; --e3) r.push_back(3);
+  for (int p : {5, 7}) while (m % p == 0) { r.push_back(p); m /= p; }
+  for (int p = 11; m > 1; p += 2)
+    while (m % p == 0) { r.push_back(p); m /= p; }
+  if (r.empty()) r.push_back(1);
+  if (r.size() > 8) return -1;
+  for (size_t i = 0; i < 8; ++i) radix[i] = i < r.size() ? r[i] : 1;
+  return n == 1 ? 0 : (int)r.size();
+}
+
+void twiddles(int n, std::vector<float2>& out) {
+  for (int i = 0; i < n; ++i) {
+    const double a = 2.0 * kPi * (double)i / (double)n;
+    out.push_back(make_float2((float)std::cos(a), (float)(-std::sin(a))));
+  }
+}
+
+// Normalised Hermite-Gaussian profiles (holopipe/hgbasis.py:42-70), fp64.
+std::vector<double> hg_profiles(int G, const std::vector<float>& axis, double waist) {
+  const size_t n = axis.size();
+  std::vector<double> h((size_t)G * n);
+  const double s2 = std::sqrt(2.0), c0 = std::pow(kPi, -0.25);
+  for (size_t i = 0; i < n; ++i) {
+    const double u = s2 * ((double)axis[i] - 0.0) / waist;
+    double hp = c0 * std::exp(-0.5 * u * u);
+    h[i] = hp;
+    if (G > 1) {
+      double hc = s2 * u * hp;
+      h[n + i] = hc;
+      for (int k = 2; k < G; ++k) {
+        const double hn = std::sqrt(2.0 / k) * u * hc - std::sqrt((k - 1.0) / k) * hp;
+        h[(size_t)k * n + i] = hn;
+        hp = hc;
+        hc = hn;
+      }
+    }
+  }
+  const double d = n > 1 ? std::fabs((double)axis[1] - (double)axis[0]) : 1.0;
+  for (int k = 0; k < G; ++k) {
+    double s = 0.0;
+    for (size_t i = 0; i < n; ++i) s += h[(size_t)k * n + i] * h[(size_t)k * n + i];
+    double nrm = std::sqrt(s * d);
+    if (nrm == 0.0) nrm = 1.0;
+    for (size_t i = 0; i < n; ++i) h[(size_t)k * n + i] /= nrm;
+  }
+  return h;
+}
+
+// int16 quantisation + float32 dequantisation of the profiles (hgbasis.py:84-93).
+void quantised_basis(int G, const std::vector<float>& axis, double waist, float* out) {
+  const std::vector<double> h = hg_profiles(G, axis, waist);
+  const size_t n = axis.size();
+  for (int k = 0; k < G; ++k) {
+    double mx = 0.0;
+    for (size_t i = 0; i < n; ++i) mx = std::fmax(mx, std::fabs(h[(size_t)k * n + i]));
+    const float scale = 32767.0f / (float)mx;
+    for (size_t i = 0; i < n; ++i) {
+      const double qv = std::nearbyint(h[(size_t)k * n + i] * (double)scale);
+      const int16_t q = (int16_t)qv;
+      out[(size_t)k * n + i] = (float)q / scale;
+    }
+  }
+}
+
+template <typename T>
+size_t push(std::vector<char>& blob, const std::vector<T>& v) {
+  size_t off = (blob.size() + 255) & ~size_t(255);
+  blob.resize(off + v.size() * sizeof(T));
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+
+int64_t align_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// Shared-memory / workspace placement of the fused kernel's buffers.
+Layout make_layout(const hpg_plan* P, int B, int A, unsigned flags, bool full_plane) {
+  const Geometry& g = P->g;
+  Layout L{};
+  const int64_t f2 = sizeof(float2);
+  const int cols = full_plane ? g.nx / 2 + 1 : g.ww;
+  int64_t nR = (int64_t)cols * g.ny;
+  int64_t nS = std::max<int64_t>((int64_t)g.gh * g.gw, (int64_t)g.gh * std::max(g.G, 1));
+  nS = std::max<int64_t>(nS, (int64_t)std::min(g.ny / 2, 16) * g.nx);
+  nS = std::max<int64_t>(nS, (int64_t)std::min(cols, 16) * g.ny);
+  if (full_plane) nS = std::max<int64_t>((int64_t)std::min(g.ny / 2, 16) * g.nx, (int64_t)std::min(cols, 16) * g.ny);
+  L.CH = (int)std::max<int64_t>(1, std::min<int64_t>(g.ny / 2, nS / g.nx));
+  L.CC = (int)std::max<int64_t>(1, std::min<int64_t>(cols, nS / g.ny));
+  const int64_t nW = full_plane ? 0 : (int64_t)g.wh * g.ww;
+  const int64_t nG = (!full_plane && (g.gh != g.wh || g.gw != g.ww)) ? (int64_t)g.gh * g.gw : 0;
+  const int64_t nAcc = (!full_plane && A > 1) ? 2 * (int64_t)g.wh * g.ww : 0;  // double2
+  struct Item { Region* r; int64_t bytes; };
+  Item items[] = {{&L.S0, nS * f2}, {&L.S1, nS * f2}, {&L.Wt, nW * f2}, {&L.R, nR * f2},
+                  {&L.Gd, nG * f2}, {&L.Acc, nAcc * f2}};
+  const int64_t budget = 200 * 1024;
+  int64_t total = 0;
+  for (auto& it : items) total += align_up(it.bytes, 256);
+  int64_t soff = 0, goff = 0;
+  for (auto& it : items) {
+    const int64_t b = align_up(it.bytes, 256);
+    if (total <= budget || soff + b <= budget) {
+      it.r->in_smem = 1;
+      it.r->off = soff;
+      soff += b;
+    } else {
+      it.r->in_smem = 0;
+      it.r->off = goff;
+      goff += b;
+    }
+  }
+  L.smem_bytes = (int)soff;
+  L.slab_bytes = goff;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hpg_version(void) { return 1; }
+
+const char* hpg_last_error(void) { return g_last_error.c_str(); }
+
+int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
+  if (!d || !out) return fail(HPG_NULLPOINTER, "null argument");
+  *out = nullptr;
+  if (d->pol_count < 1 || d->pol_count > 2) return fail(HPG_INVALIDPOLARISATION, "pol_count");
+  if (d->fft_nx < 2 || d->fft_ny < 2 || (d->fft_ny & 1) || d->frame_width < 1 || d->frame_height < 1)
+    return fail(HPG_INVALIDDIMENSION, "window dimensions");
+  if (d->wavelength_count < 1 || d->wavelength_count > kMaxWl || !d->wavelengths)
+    return fail(HPG_INVALIDARGUMENT, "wavelength_count");
+  if (d->pixel_size <= 0 || d->wavelength_centre <= 0) return fail(HPG_INVALIDARGUMENT, "pixel/wavelength");
+  if (d->group_count < 0) return fail(HPG_INVALIDARGUMENT, "group_count");
+  hpg_plan* P = new (std::nothrow) hpg_plan();
+  if (!P) return fail(HPG_MEMORYALLOCATION, "host allocation");
+  Geometry& g = P->g;
+  std::memset(&g, 0, sizeof(g));
+  g.W = d->frame_width;
+  g.H = d->frame_height;
+  g.P = d->pol_count;
+  g.nx = d->fft_nx;
+  g.ny = d->fft_ny;
+  g.mode = d->resolution_mode;
+  g.L = d->wavelength_count;
+  g.G = d->group_count;
+  g.M = g.G * (g.G + 1) / 2;
+  const double p = d->pixel_size;
+  // window box (holopipe/pipeline.py:62-69)
+  const double fr = std::sin(radians(d->window_radius_deg)) / d->wavelength_centre;
+  g.ww = (int)std::min<long long>(2 * ((long long)std::floor(fr * g.nx * p) + 1), g.nx);
+  g.wh = (int)std::min<long long>(2 * ((long long)std::floor(fr * g.ny * p) + 1), g.ny);
+  if (g.ww < 2 || g.wh < 2) { delete P; return fail(HPG_INVALIDDIMENSION, "window radius too small"); }
+  if (g.mode == 0) { g.gh = g.ny; g.gw = g.nx; }
+  else { g.gh = g.wh; g.gw = g.ww; }
+  if (g.gw & 1 || g.gh & 1) { delete P; return fail(HPG_INVALIDDIMENSION, "odd IFFT grid"); }
+  // window origins (pipeline.py:23-44) and fractional centres (engine.py:147-150)
+  double xi[2][2];
+  for (int q = 0; q < g.P; ++q) {
+    int x0 = 0, x1 = g.W;
+    if (g.P == 2) { x0 = q == 0 ? 0 : g.W / 2; x1 = q == 0 ? g.W / 2 : g.W; }
+    if (g.nx > x1 - x0 || g.ny > g.H) { delete P; return fail(HPG_INVALIDDIMENSION, "fft window does not fit the frame region"); }
+    const double xc = d->beam_centre[0][q] / p + g.W / 2.0;
+    const double yc = d->beam_centre[1][q] / p + g.H / 2.0;
+    long long c0 = rint_even(xc) - g.nx / 2, r0 = rint_even(yc) - g.ny / 2;
+    c0 = std::min<long long>(std::max<long long>(c0, x0), x1 - g.nx);
+    r0 = std::min<long long>(std::max<long long>(r0, 0), g.H - g.ny);
+    g.col0[q] = (int)c0;
+    g.row0[q] = (int)r0;
+    xi[q][0] = d->beam_centre[0][q] / p + g.W / 2.0 - c0;
+    xi[q][1] = d->beam_centre[1][q] / p + g.H / 2.0 - r0;
+  }
+  // carrier bins (engine.py:191-194)
+  for (int q = 0; q < g.P; ++q)
+    for (int w = 0; w < g.L; ++w) {
+      const double lam = d->wavelengths[w];
+      g.k0[q][w][0] = (int)rint_even(std::sin(radians(d->tilt_deg[0][q])) * g.nx * p / lam);
+      g.k0[q][w][1] = (int)rint_even(std::sin(radians(d->tilt_deg[1][q])) * g.ny * p / lam);
+    }
+  // field axes (pipeline.py:152-160)
+  P->xa.resize(g.gw);
+  P->ya.resize(g.gh);
+  for (int i = 0; i < g.gw; ++i)
+    P->xa[i] = g.mode == 0 ? (float)((double)(i - g.nx / 2) * p)
+                           : (float)((double)(i - g.ww / 2) * p * ((double)g.nx / g.ww));
+  for (int i = 0; i < g.gh; ++i)
+    P->ya[i] = g.mode == 0 ? (float)((double)(i - g.ny / 2) * p)
+                           : (float)((double)(i - g.wh / 2) * p * ((double)g.ny / g.wh));
+  g.dx = g.gw > 1 ? std::fabs((double)P->xa[1] - (double)P->xa[0]) : 1.0;
+  g.dy = g.gh > 1 ? std::fabs((double)P->ya[1] - (double)P->ya[0]) : 1.0;
+  for (int q = 0; q < g.P; ++q) g.dxdy[q] = (float)(g.dx * g.dy);
+  // FFT plans
+  g.nst_nx = radix_plan(g.nx, g.radix_nx);
+  g.nst_ny = radix_plan(g.ny, g.radix_ny);
+  g.nst_gw = radix_plan(g.gw, g.radix_gw);
+  g.nst_gh = radix_plan(g.gh, g.radix_gh);
+  if (g.nst_nx < 0 || g.nst_ny < 0 || g.nst_gw < 0 || g.nst_gh < 0) { delete P; return fail(HPG_INVALIDDIMENSION, "FFT size"); }
+
+  std::vector<float2> tw_nx, tw_ny, tw_gw, tw_gh;
+  twiddles(g.nx, tw_nx); twiddles(g.ny, tw_ny); twiddles(g.gw, tw_gw); twiddles(g.gh, tw_gh);
+  // window table: mask * recentring phase (/ sinc envelope)  (pipeline.py:72-127)
+  const int whw = g.wh * g.ww;
+  std::vector<float2> wtab((size_t)g.P * g.L * whw);
+  std::vector<float2> remx((size_t)g.P * g.L * g.gw), remy((size_t)g.P * g.L * g.gh);
+  for (int q = 0; q < g.P; ++q)
+    for (int w = 0; w < g.L; ++w) {
+      const int kx = g.k0[q][w][0], ky = g.k0[q][w][1];
+      const double lam = d->wavelengths[w];
+      float2* T = &wtab[((size_t)q * g.L + w) * whw];
+      for (int r = 0; r < g.wh; ++r) {
+        const double dfy = (double)(r - g.wh / 2) / (g.ny * p);
+        const double ty = (double)(ky + r - g.wh / 2);
+        const double ay = 2.0 * kPi * ty * (xi[q][1] - g.ny / 2.0) / g.ny;
+        for (int c = 0; c < g.ww; ++c) {
+          const double dfx = (double)(c - g.ww / 2) / (g.nx * p);
+          const bool in = dfy * dfy + dfx * dfx <= fr * fr + 1e-30;
+          const double tx = (double)(kx + c - g.ww / 2);
+          const double ax = 2.0 * kPi * tx * (xi[q][0] - g.nx / 2.0) / g.nx;
+          // product of the two separable phases in complex128 (pipeline.py:125-127)
+          const double pxr = std::cos(ax), pxi = std::sin(ax), pyr = std::cos(ay), pyi = std::sin(ay);
+          const double re = pyr * pxr - pyi * pxi;
+          const double im = pyr * pxi + pyi * pxr;
+          // complex64 cast, then the mask (bool * c64)
+          float fre = in ? (float)re : 0.f, fim = in ? (float)im : 0.f;
+          if (d->fill_factor) {
+            int txm = (kx + c - g.ww / 2) % g.nx; if (txm < 0) txm += g.nx;
+            int tym = (ky + r - g.wh / 2) % g.ny; if (tym < 0) tym += g.ny;
+            const int sx = txm <= g.nx / 2 ? txm : g.nx - txm;
+            const double fyw = (double)(tym > g.ny / 2 ? tym - g.ny : tym) / g.ny;
+            double env = sinc(fyw) * sinc((double)sx / g.nx);
+            if (std::fabs(env) < 1e-3) env = 1e-3;
+            const float fe = (float)env;
+            fre = fre / fe;
+            fim = fim / fe;
+          }
+          T[(size_t)r * g.ww + c] = make_float2(fre, fim);
+        }
+      }
+      // removal phase, separable (pipeline.py:163-185), with ifftshift sign
+      // (-1)^(x+y) and the 1/(nx*ny) inverse normalisation (pipeline.py:146-149)
+      const double fxl = std::sin(radians(d->removal_tilt_deg[0][q])) / lam;
+      const double fyl = std::sin(radians(d->removal_tilt_deg[1][q])) / lam;
+      const double rx = fxl - kx / (g.nx * p), ry = fyl - ky / (g.ny * p);
+      const double cst = 2.0 * kPi * (fxl * d->removal_beam_centre[0][q] + fyl * d->removal_beam_centre[1][q]) -
+                         kPi * (kx + ky);
+      const double quad = kPi * d->defocus[q] / lam;
+      const double norm = 1.0 / ((double)g.nx * g.ny);
+      for (int x = 0; x < g.gw; ++x) {
+        const double xv = (double)P->xa[x];
+        const double ph = 2.0 * kPi * rx * xv + quad * xv * xv;
+        const double sg = (x & 1) ? -1.0 : 1.0;
+        remx[((size_t)q * g.L + w) * g.gw + x] = make_float2((float)(sg * std::cos(ph)), (float)(-sg * std::sin(ph)));
+      }
+      for (int y = 0; y < g.gh; ++y) {
+        const double yv = (double)P->ya[y];
+        const double ph = cst + 2.0 * kPi * ry * yv + quad * yv * yv;
+        const double sg = ((y & 1) ? -1.0 : 1.0) * norm;
+        remy[((size_t)q * g.L + w) * g.gh + y] = make_float2((float)(sg * std::cos(ph)), (float)(-sg * std::sin(ph)));
+      }
+    }
+  // basis (hgbasis.py:76-93); centre 0, waist per pol
+  const int G = std::max(g.G, 0);
+  P->hx.assign((size_t)g.P * G * g.gw, 0.f);
+  P->hy.assign((size_t)g.P * G * g.gh, 0.f);
+  std::vector<int16_t> mm, mn;
+  if (G > 0) {
+    for (int q = 0; q < g.P; ++q) {
+      if (!(d->waist[q] > 0)) { delete P; return fail(HPG_INVALIDDIMENSION, "basis waist must be positive"); }
+      quantised_basis(G, P->xa, d->waist[q], &P->hx[(size_t)q * G * g.gw]);
+      quantised_basis(G, P->ya, d->waist[q], &P->hy[(size_t)q * G * g.gh]);
+    }
+    for (int gg = 0; gg < G; ++gg)
+      for (int m = gg; m >= 0; --m) { mm.push_back((int16_t)m); mn.push_back((int16_t)(gg - m)); }
+  } else {
+    mm.push_back(0); mn.push_back(0);
+  }
+  std::vector<char> blob;
+  const size_t o_nx = push(blob, tw_nx), o_ny = push(blob, tw_ny), o_gw = push(blob, tw_gw), o_gh = push(blob, tw_gh);
+  const size_t o_w = push(blob, wtab), o_rx = push(blob, remx), o_ry = push(blob, remy);
+  std::vector<float> hxv = P->hx, hyv = P->hy;
+  if (hxv.empty()) hxv.push_back(0.f);
+  if (hyv.empty()) hyv.push_back(0.f);
+  const size_t o_hx = push(blob, hxv), o_hy = push(blob, hyv);
+  const size_t o_xa = push(blob, P->xa), o_ya = push(blob, P->ya);
+  std::vector<double> xad(P->xa.begin(), P->xa.end()), yad(P->ya.begin(), P->ya.end());
+  const size_t o_xad = push(blob, xad), o_yad = push(blob, yad);
+  const size_t o_mm = push(blob, mm), o_mn = push(blob, mn);
+  cudaGetDevice(&P->device);
+  cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
+  cudaError_t e = cudaMalloc(&P->dev, blob.size());
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaMalloc(plan tables)"); }
+  e = cudaMemcpy(P->dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaMemcpy(plan tables)"); }
+  char* base = static_cast<char*>(P->dev);
+  P->t.tw_nx = reinterpret_cast<const float2*>(base + o_nx);
+  P->t.tw_ny = reinterpret_cast<const float2*>(base + o_ny);
+  P->t.tw_gw = reinterpret_cast<const float2*>(base + o_gw);
+  P->t.tw_gh = reinterpret_cast<const float2*>(base + o_gh);
+  P->t.win_tab = reinterpret_cast<const float2*>(base + o_w);
+  P->t.rem_x = reinterpret_cast<const float2*>(base + o_rx);
+  P->t.rem_y = reinterpret_cast<const float2*>(base + o_ry);
+  P->t.hx = reinterpret_cast<const float*>(base + o_hx);
+  P->t.hy = reinterpret_cast<const float*>(base + o_hy);
+  P->t.xa = reinterpret_cast<const float*>(base + o_xa);
+  P->t.ya = reinterpret_cast<const float*>(base + o_ya);
+  P->t.xad = reinterpret_cast<const double*>(base + o_xad);
+  P->t.yad = reinterpret_cast<const double*>(base + o_yad);
+  P->t.mode_m = reinterpret_cast<const int16_t*>(base + o_mm);
+  P->t.mode_n = reinterpret_cast<const int16_t*>(base + o_mn);
+  e = set_smem_limits();
+  if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
+  *out = P;
+  return HPG_SUCCESS;
+}
+
+int hpg_plan_destroy(hpg_plan* P) {
+  if (!P) return fail(HPG_NULLPOINTER, "null plan");
+  if (P->dev) cudaFree(P->dev);
+  delete P;
+  return HPG_SUCCESS;
+}
+
+int hpg_plan_get_info(const hpg_plan* P, hpg_plan_info* info) {
+  if (!P || !info) return fail(HPG_NULLPOINTER, "null argument");
+  std::memset(info, 0, sizeof(*info));
+  const Geometry& g = P->g;
+  info->wh = g.wh; info->ww = g.ww; info->gh = g.gh; info->gw = g.gw;
+  info->mode_count = g.M;
+  for (int q = 0; q < 2; ++q) {
+    info->col0[q] = g.col0[q];
+    info->row0[q] = g.row0[q];
+    for (int w = 0; w < kMaxWl; ++w) {
+      info->k0[q][w][0] = g.k0[q][w][0];
+      info->k0[q][w][1] = g.k0[q][w][1];
+    }
+  }
+  return HPG_SUCCESS;
+}
+
+int hpg_plan_get_axes(const hpg_plan* P, float* x, float* y) {
+  if (!P || !x || !y) return fail(HPG_NULLPOINTER, "null argument");
+  std::memcpy(x, P->xa.data(), P->xa.size() * sizeof(float));
+  std::memcpy(y, P->ya.data(), P->ya.size() * sizeof(float));
+  return HPG_SUCCESS;
+}
+
+int hpg_plan_get_basis(const hpg_plan* P, float* hx, float* hy) {
+  if (!P || !hx || !hy) return fail(HPG_NULLPOINTER, "null argument");
+  std::memcpy(hx, P->hx.data(), P->hx.size() * sizeof(float));
+  std::memcpy(hy, P->hy.data(), P->hy.size() * sizeof(float));
+  return HPG_SUCCESS;
+}
+
+static int grid_for(const hpg_plan* P, const Layout& L, int64_t items, const void* kernel_tag) {
+  (void)kernel_tag;
+  int per_sm = L.smem_bytes <= 100 * 1024 ? 2 : 1;
+  int64_t grid = (int64_t)P->num_sms * per_sm;
+  if (items < grid) grid = items;
+  return (int)std::max<int64_t>(grid, 1);
+}
+
+static void finish_layout(const hpg_plan* P, Layout& L, int64_t items, unsigned flags) {
+  L.grid = grid_for(P, L, items, nullptr);
+  L.agg_off = align_up(L.slab_bytes * L.grid, 256);
+  L.agg_per_cta = (flags & HPG_FLAG_SUMMARY) ? align_up((int64_t)P->g.P * P->g.gh * P->g.gw * 8, 256) : 0;
+}
+
+int hpg_workspace_size(const hpg_plan* P, int32_t B, uint32_t flags, size_t* bytes) {
+  if (!P || !bytes) return fail(HPG_NULLPOINTER, "null argument");
+  Layout L = make_layout(P, B, 2, flags, false);  // worst case: averaging enabled
+  finish_layout(P, L, (int64_t)B * P->g.P, flags);
+  const int64_t fused = L.agg_off + L.agg_per_cta * L.grid;
+  Layout F = make_layout(P, B, 1, 0, true);
+  finish_layout(P, F, (int64_t)P->num_sms * 2, 0);
+  *bytes = (size_t)std::max<int64_t>(std::max<int64_t>(fused, F.slab_bytes * F.grid), 256);
+  return HPG_SUCCESS;
+}
+
+static int fill_params(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, unsigned flags,
+                       RunParams& rp) {
+  std::memset(&rp, 0, sizeof(rp));
+  rp.g = P->g;
+  rp.t = P->t;
+  rp.frames = b->frames;
+  rp.fmt = b->frame_format;
+  rp.transpose = b->transpose;
+  rp.B = b->batch_count;
+  rp.A = std::max(1, b->avg_count);
+  rp.members = b->members;
+  rp.wl = b->wl_of_row;
+  rp.bcal = static_cast<const float2*>(b->batch_cal);
+  rp.cal_pols = b->cal_pols;
+  rp.cal_batch = b->cal_batch;
+  rp.rcal = static_cast<const float2*>(b->ref_cal);
+  rp.rcal_count = std::max(1, b->ref_cal_count);
+  rp.flags = flags;
+  if (b->layout_width > 0) {
+    rp.g.W = b->layout_width;
+    rp.g.H = b->layout_height;
+    for (int q = 0; q < P->g.P; ++q) {
+      rp.g.col0[q] = b->layout_col0[q];
+      rp.g.row0[q] = b->layout_row0[q];
+    }
+  }
+  if (o) {
+    rp.fr = o->field_r;
+    rp.fi = o->field_i;
+    rp.scale = o->field_scale;
+    rp.coefs = static_cast<float2*>(o->coefs);
+    rp.raw = static_cast<float2*>(o->raw_fields);
+    rp.windows = static_cast<float2*>(o->windows);
+    rp.params = o->field_params;
+    rp.param_slots = o->param_slots;
+    rp.work = static_cast<char*>(o->workspace);
+  }
+  return HPG_SUCCESS;
+}
+
+int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_t flags, void* stream) {
+  if (!P || !b || !o) return fail(HPG_NULLPOINTER, "null argument");
+  if (!b->frames || !o->field_r || !o->field_i || !o->field_scale) return fail(HPG_NULLPOINTER, "null buffer");
+  if (b->batch_count < 1) return fail(HPG_INVALIDDIMENSION, "batch_count");
+  const int A = std::max(1, b->avg_count);
+  if (!b->members && (int64_t)b->batch_count * A > b->frame_count)
+    return fail(HPG_INVALIDDIMENSION, "frame buffer holds fewer frames than batch*avg");
+  if (b->frame_format != 0 && b->frame_format != 1) return fail(HPG_INVALIDARGUMENT, "frame_format");
+  if (b->layout_width > 0) {
+    for (int q = 0; q < P->g.P; ++q)
+      if (b->layout_col0[q] < 0 || b->layout_row0[q] < 0 || b->layout_col0[q] + P->g.nx > b->layout_width ||
+          b->layout_row0[q] + P->g.ny > b->layout_height)
+        return fail(HPG_INVALIDDIMENSION, "layout override does not contain the FFT window");
+  }
+  if (b->batch_cal && (b->cal_pols < 1 || b->cal_batch < 1)) return fail(HPG_INVALIDARGUMENT, "batch calibration dims");
+  if ((flags & HPG_FLAG_SUMMARY) && o->field_params && o->param_slots < b->batch_count + 1)
+    return fail(HPG_INVALIDDIMENSION, "param_slots");
+  RunParams rp;
+  fill_params(P, b, o, flags, rp);
+  rp.lay = make_layout(P, b->batch_count, A, flags, false);
+  finish_layout(P, rp.lay, (int64_t)b->batch_count * P->g.P, flags);
+  const int64_t need = rp.lay.agg_off + rp.lay.agg_per_cta * rp.lay.grid;
+  if ((rp.lay.slab_bytes > 0 || (flags & HPG_FLAG_SUMMARY)) && (!o->workspace || (int64_t)o->workspace_bytes < need))
+    return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
+  cudaError_t e = launch_fused(rp, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
+  return HPG_SUCCESS;
+}
+
+int hpg_finalize_summary(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, float* total,
+                         void* stream) {
+  if (!P || !b || !o || !o->workspace) return fail(HPG_NULLPOINTER, "null argument");
+  RunParams rp;
+  fill_params(P, b, o, HPG_FLAG_SUMMARY, rp);
+  rp.lay = make_layout(P, b->batch_count, std::max(1, b->avg_count), HPG_FLAG_SUMMARY, false);
+  finish_layout(P, rp.lay, (int64_t)b->batch_count * P->g.P, HPG_FLAG_SUMMARY);
+  cudaError_t e = launch_finalize(rp, total, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "finalize kernel launch");
+  return HPG_SUCCESS;
+}
+
+int hpg_fourier_full(const hpg_plan* P, const void* frames, int32_t fmt, int32_t transpose,
+                        int64_t F, void* plane, void* workspace, size_t ws_bytes, void* stream) {
+  if (!P || !frames || !plane) return fail(HPG_NULLPOINTER, "null argument");
+  RunParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.g = P->g;
+  rp.t = P->t;
+  rp.frames = frames;
+  rp.fmt = fmt;
+  rp.transpose = transpose;
+  rp.work = static_cast<char*>(workspace);
+  rp.lay = make_layout(P, 1, 1, 0, true);
+  finish_layout(P, rp.lay, F * P->g.P, 0);
+  if (rp.lay.slab_bytes > 0 && (!workspace || (int64_t)ws_bytes < rp.lay.slab_bytes * rp.lay.grid))
+    return fail(HPG_INVALIDARGUMENT, "workspace too small");
+  cudaError_t e = launch_fourier_full(rp, F, static_cast<float2*>(plane), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "fourier kernel launch");
+  return HPG_SUCCESS;
+}
+
+static int plane_grid(int64_t count, int P) { return (int)std::min<int64_t>(count * P, 148); }
+
+size_t hpg_plane_summary_workspace(int64_t count, int32_t P, int32_t h, int32_t w) {
+  return (size_t)plane_grid(count, P) * (size_t)align_up((int64_t)P * h * w * 8, 256);
+}
+
+int hpg_plane_summary(const void* data, int64_t count, int32_t P, int32_t h, int32_t w, const double* xa,
+                      const double* ya, float* params, int32_t slots, float* total, void* work,
+                      size_t work_bytes, void* stream) {
+  if (!data || !xa || !ya || !params || !work) return fail(HPG_NULLPOINTER, "null argument");
+  if (count < 1 || P < 1 || h < 1 || w < 1) return fail(HPG_INVALIDDIMENSION, "empty plane");
+  if (slots < count + 1) return fail(HPG_INVALIDDIMENSION, "slots");
+  if (work_bytes < hpg_plane_summary_workspace(count, P, h, w)) return fail(HPG_INVALIDARGUMENT, "workspace too small");
+  cudaError_t e = launch_plane_summary(static_cast<const float2*>(data), count, P, h, w, xa, ya, params, slots,
+                                       total, static_cast<char*>(work), plane_grid(count, P),
+                                       static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "plane summary launch");
+  return HPG_SUCCESS;
+}
+
+int hpg_extract_coefs(const hpg_plan* P, const int16_t* fr, const int16_t* fi, const float* scale,
+                      int32_t B, void* coefs, void* stream) {
+  if (!P || !fr || !fi || !scale || !coefs) return fail(HPG_NULLPOINTER, "null argument");
+  if (P->g.G < 1) return HPG_SUCCESS;
+  RunParams rp;
+  std::memset(&rp, 0, sizeof(rp));
+  rp.g = P->g;
+  rp.t = P->t;
+  rp.B = B;
+  rp.fr = const_cast<int16_t*>(fr);
+  rp.fi = const_cast<int16_t*>(fi);
+  rp.scale = const_cast<float*>(scale);
+  rp.coefs = static_cast<float2*>(coefs);
+  const int grid = (int)std::min<int64_t>((int64_t)B * P->g.P, (int64_t)P->num_sms * 4);
+  cudaError_t e = launch_coefs(rp, grid, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "coefs kernel launch");
+  return HPG_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// Internal plan / kernel parameter structures shared by the CUDA kernels and
+// the C-ABI implementation.  Not part of the public boundary.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "holo_fft.cuh"
+
+namespace holo {
+
+constexpr int kMaxPol = 2;
+constexpr int kMaxWl = 16;
+constexpr int kThreads = 256;
+
+// Device-resident constant tables of one plan (all pointers into one cudaMalloc).
+struct DevTables {
+  const float2* tw_nx;    // [nx]   W_nx^i
+  const float2* tw_ny;    // [ny]
+  const float2* tw_gw;    // [gw]
+  const float2* tw_gh;    // [gh]
+  const float2* win_tab;  // [P][L][wh*ww] mask * recentring phase (/ sinc envelope)
+  const float2* rem_x;    // [P][L][gw] removal phase along x  (incl. ifftshift sign)
+  const float2* rem_y;    // [P][L][gh] removal phase along y  (incl. constant, sign, 1/(nx ny))
+  const float* hx;        // [P][G][gw] dequantised basis profiles (float32)
+  const float* hy;        // [P][G][gh]
+  const float* xa;        // [gw] field axis (float32)
+  const float* ya;        // [gh]
+  const double* xad;      // [gw] the same axes widened to fp64 (analysis.py:78-79)
+  const double* yad;      // [gh]
+  const int16_t* mode_m;  // [M]
+  const int16_t* mode_n;  // [M]
+};
+
+struct Geometry {
+  int W, H, P;
+  int nx, ny, wh, ww, gh, gw;
+  int mode;               // resolution mode
+  int L, G, M;
+  int col0[kMaxPol], row0[kMaxPol];
+  int k0[kMaxPol][kMaxWl][2];
+  float dxdy[kMaxPol];    // float32(complex64(dx*dy)) per pol
+  double dx, dy;          // field-axis pitch (fp64 from the float32 axes)
+  int radix_nx[8], nst_nx, radix_ny[8], nst_ny, radix_gw[8], nst_gw, radix_gh[8], nst_gh;
+};
+
+// Placement of the per-CTA working buffers: offset in shared memory (bytes) or,
+// when the region does not fit, offset inside the CTA's global workspace slab.
+struct Region {
+  int64_t off;
+  int in_smem;
+};
+
+struct Layout {
+  Region R, S0, S1, Wt, Gd, Acc;
+  int CH;                 // row pairs per row-pass chunk
+  int CC;                 // columns per column-pass chunk
+  int smem_bytes;         // dynamic shared memory per CTA
+  int64_t slab_bytes;     // global workspace per CTA (0 if all in smem)
+  int grid;               // persistent CTAs
+  int64_t agg_off;        // workspace offset of per-CTA fp64 aggregate images (summary)
+  int64_t agg_per_cta;    // bytes of one CTA's aggregate images
+};
+
+struct RunParams {
+  Geometry g;
+  DevTables t;
+  Layout lay;
+  const void* frames;
+  int fmt, transpose;
+  int B, A;
+  const int32_t* members;
+  const int32_t* wl;
+  const float2* bcal;
+  int cal_pols, cal_batch;
+  const float2* rcal;
+  int rcal_count;
+  int16_t* fr;
+  int16_t* fi;
+  float* scale;
+  float2* coefs;
+  float2* raw;
+  float2* windows;
+  float* params;
+  int param_slots;
+  char* work;
+  unsigned flags;
+};
+
+}  // namespace holo

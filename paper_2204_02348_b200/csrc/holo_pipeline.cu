@@ -1,0 +1,609 @@
+// Generic fused hot-path kernel: frame -> window -> R2C -> Fourier-window crop
+// -> reduced IFFT -> tilt/defocus removal -> field summary -> int16 -> HG overlap.
+//
+// One persistent CTA processes one (batch row, polarisation) item at a time.
+// The reference does this as four numpy stages with full-size intermediates
+// (holopipe/engine.py:135-385); here every intermediate stays on chip (or in
+// an L2-resident per-CTA slab for windows too large for shared memory) and
+// only the frame window is read from HBM and only int16 fields, scales and
+// coefficients are written.
+//
+// FFT strategy (pruned 2-D R2C):
+//   row pass   : rows y and y+ny/2 packed as one complex sequence, Stockham
+//                FFT along x, Hermitian split, keep only the ww needed bins
+//                (holopipe/pipeline.py:79-104 fetches them from the r2c plane)
+//   column pass: FFT along y of the ww kept columns, keep the wh needed rows,
+//                multiply by mask * recentring phase (pipeline.py:72-76,114-127)
+//   IFFT       : wh x ww inverse (pipeline.py:130-149), ifftshift folded into
+//                the separable removal phase (pipeline.py:163-185)
+#include "holo_internal.h"
+
+namespace holo {
+
+__device__ __forceinline__ float2* region_ptr(const Region& r, char* smem, char* slab) {
+  return reinterpret_cast<float2*>(r.in_smem ? smem + r.off : slab + r.off);
+}
+
+__device__ __forceinline__ int pmod(int v, int n) {
+  int r = v % n;
+  return r < 0 ? r + n : r;
+}
+
+__device__ __forceinline__ float load_px(const void* frames, int fmt, int transpose, int W, int H,
+                                         int64_t f, int y, int x) {
+  const int64_t base = f * (int64_t)W * H;
+  if (fmt == 0) return __ldg(reinterpret_cast<const float*>(frames) + base + (int64_t)y * W + x);
+  const unsigned short* u = reinterpret_cast<const unsigned short*>(frames);
+  if (transpose) return (float)__ldg(u + base + (int64_t)x * H + y);
+  return (float)__ldg(u + base + (int64_t)y * W + x);
+}
+
+template <typename T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum of NV doubles (same order every call).
+template <int NV>
+__device__ void block_sum(double* v, double (*red)[32]) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = warp_sum(v[i]);
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) red[i][w] = v[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double s = 0.0;
+    for (int j = 0; j < nw; ++j) s += red[i][j];
+    v[i] = s;
+  }
+}
+
+// Block max of v with the smallest index among ties (numpy argmax semantics).
+__device__ void block_argmax(float& v, int& idx, float* redf, int* redi) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, v, o);
+    int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+  }
+  __syncthreads();
+  if (l == 0) { redf[w] = v; redi[w] = idx; }
+  __syncthreads();
+  v = redf[0]; idx = redi[0];
+  for (int j = 1; j < nw; ++j)
+    if (redf[j] > v || (redf[j] == v && redi[j] < idx)) { v = redf[j]; idx = redi[j]; }
+}
+
+__device__ float block_max(float v, float* redf) {
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (l == 0) redf[w] = v;
+  __syncthreads();
+  v = redf[0];
+  for (int j = 1; j < nw; ++j) v = fmaxf(v, redf[j]);
+  return v;
+}
+
+__device__ __forceinline__ FFTPlan make_plan(int n, int nst, const int* radix, const float2* tw) {
+  FFTPlan p;
+  p.n = n;
+  p.nst = nst;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p.radix[i] = radix[i];
+  p.tw = tw;
+  return p;
+}
+
+// ---------------------------------------------------------------- row pass
+// Window rows (y, y+ny/2) -> complex sequence; FFT along x; Hermitian split;
+// keep bins kx_c = k0x + c - ww/2 (mod nx): R[c][y] (column-major, ny long).
+__device__ void row_pass(const RunParams& p, int64_t f, int q, int k0x, float2* R, float2* S0,
+                         float2* S1, const FFTPlan& pl) {
+  const Geometry& g = p.g;
+  const int nx = g.nx, ny = g.ny, ny2 = g.ny >> 1, ww = g.ww;
+  const int col0 = g.col0[q], row0 = g.row0[q];
+  for (int c0 = 0; c0 < ny2; c0 += p.lay.CH) {
+    const int ch = min(p.lay.CH, ny2 - c0);
+    for (int idx = threadIdx.x; idx < ch * nx; idx += blockDim.x) {
+      const int s = idx / nx, x = idx - s * nx, y = c0 + s;
+      const float a = load_px(p.frames, p.fmt, p.transpose, g.W, g.H, f, row0 + y, col0 + x);
+      const float b = load_px(p.frames, p.fmt, p.transpose, g.W, g.H, f, row0 + y + ny2, col0 + x);
+      S0[idx] = make_float2(a, b);
+    }
+    __syncthreads();
+    const float2* Z = stockham<false>(S0, S1, pl, ch, nx, 1);
+    for (int idx = threadIdx.x; idx < ch * ww; idx += blockDim.x) {
+      const int c = idx / ch, s = idx - c * ch;
+      const int kx = pmod(k0x + c - ww / 2, nx);
+      const int km = kx ? nx - kx : 0;
+      const float2 zk = Z[s * nx + kx], zm = Z[s * nx + km];
+      R[c * ny + c0 + s] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+      R[c * ny + c0 + s + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- column pass
+// FFT along y of each kept column; keep rows ky_r = k0y + r - wh/2 (mod ny);
+// multiply by the (mask * recentring phase [/ sinc]) table -> Wout[r][c].
+__device__ void col_pass(const RunParams& p, int k0y, const float2* wtab, float2* R, float2* S0,
+                         const FFTPlan& pl, float2* Wout) {
+  const Geometry& g = p.g;
+  const int ny = g.ny, ww = g.ww, wh = g.wh;
+  for (int c0 = 0; c0 < ww; c0 += p.lay.CC) {
+    const int cc = min(p.lay.CC, ww - c0);
+    const float2* res = stockham<false>(R + (size_t)c0 * ny, S0, pl, cc, ny, 1);
+    for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) {
+      const int j = idx / wh, r = idx - j * wh, c = c0 + j;
+      const int ky = pmod(k0y + r - wh / 2, ny);
+      Wout[r * ww + c] = cmul(res[j * ny + ky], __ldg(&wtab[r * ww + c]));
+    }
+    __syncthreads();
+  }
+}
+
+// -------------------------------------------------------------- epilogue
+struct Stats {
+  double v[6];  // tot, sx, sy, s2, cwrap, swrap
+};
+
+__device__ void write_params(float* params, int P, int slots, int q, int slot, const double* v,
+                             float maxabs, int argmax, double da, double ya0, double span) {
+  const double tot = v[0];
+  float out[7];
+  out[0] = (float)(tot * da);
+  if (tot > 0.0) {
+    out[1] = (float)(v[1] / tot);
+    out[2] = (float)(v[2] / tot);
+    out[5] = (float)((tot * da) * (tot * da) / (v[3] * da));
+    double th = atan2(v[5], v[4]);
+    th = fmod(th, 2.0 * M_PI);
+    if (th < 0) th += 2.0 * M_PI;
+    out[6] = (float)(ya0 + th * span / (2.0 * M_PI));
+  } else {
+    out[1] = out[2] = out[5] = 0.f;
+    out[6] = (float)ya0;
+  }
+  out[3] = maxabs;
+  out[4] = __int_as_float(argmax);
+#pragma unroll
+  for (int k = 0; k < 7; ++k) params[((size_t)k * P + q) * slots + slot] = out[k];
+}
+
+// Overlap of the dequantised field F (gh x gw, in `F`) with the separable basis:
+// U[y][m] = sum_x F[y][x] hx[m][x];  c(m,n) = dxdy * sum_y hy[n][y] U[y][m]
+// (holopipe/hgbasis.py:101-116).
+__device__ void overlap(const RunParams& p, int q, const float2* F, float2* U, float2* out) {
+  const Geometry& g = p.g;
+  const int G = g.G, gh = g.gh, gw = g.gw;
+  const float* hx = p.t.hx + (size_t)q * G * gw;
+  const float* hy = p.t.hy + (size_t)q * G * gh;
+  for (int idx = threadIdx.x; idx < gh * G; idx += blockDim.x) {
+    const int y = idx / G, m = idx - y * G;
+    const float2* row = F + (size_t)y * gw;
+    const float* h = hx + (size_t)m * gw;
+    float ax = 0.f, ay = 0.f;
+    for (int x = 0; x < gw; ++x) {
+      const float2 v = row[x];
+      const float hv = __ldg(&h[x]);
+      ax = fmaf(v.x, hv, ax);
+      ay = fmaf(v.y, hv, ay);
+    }
+    U[idx] = make_float2(ax, ay);
+  }
+  __syncthreads();
+  const float d = g.dxdy[q];
+  for (int i = threadIdx.x; i < g.M; i += blockDim.x) {
+    const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+    const float* h = hy + (size_t)n * gh;
+    float ax = 0.f, ay = 0.f;
+    for (int y = 0; y < gh; ++y) {
+      const float2 v = U[y * G + m];
+      const float hv = __ldg(&h[y]);
+      ax = fmaf(v.x, hv, ax);
+      ay = fmaf(v.y, hv, ay);
+    }
+    out[i] = make_float2(ax * d, ay * d);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) fused_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double red[8][32];
+  __shared__ float redf[32];
+  __shared__ int redi[32];
+  const Geometry& g = p.g;
+  char* slab = p.lay.slab_bytes ? p.work + (int64_t)blockIdx.x * p.lay.slab_bytes : nullptr;
+  float2* R = region_ptr(p.lay.R, smem, slab);
+  float2* S0 = region_ptr(p.lay.S0, smem, slab);
+  float2* S1 = region_ptr(p.lay.S1, smem, slab);
+  float2* Wt = region_ptr(p.lay.Wt, smem, slab);
+  float2* Gd = region_ptr(p.lay.Gd, smem, slab);
+  double2* Acc = reinterpret_cast<double2*>(region_ptr(p.lay.Acc, smem, slab));
+  const bool summary = (p.flags & 1u) != 0;
+  const int ghw = g.gh * g.gw, whw = g.wh * g.ww;
+  double* agg = summary ? reinterpret_cast<double*>(p.work + p.lay.agg_off +
+                                                    (int64_t)blockIdx.x * p.lay.agg_per_cta)
+                        : nullptr;
+  if (agg)
+    for (int i = threadIdx.x; i < g.P * ghw; i += blockDim.x) agg[i] = 0.0;
+
+  const FFTPlan pl_nx = make_plan(g.nx, g.nst_nx, g.radix_nx, p.t.tw_nx);
+  const FFTPlan pl_ny = make_plan(g.ny, g.nst_ny, g.radix_ny, p.t.tw_ny);
+  const FFTPlan pl_gw = make_plan(g.gw, g.nst_gw, g.radix_gw, p.t.tw_gw);
+  const FFTPlan pl_gh = make_plan(g.gh, g.nst_gh, g.radix_gh, p.t.tw_gh);
+  const double da = g.dx * g.dy;
+  const double span = g.dy * g.gh;
+
+  const int items = p.B * g.P;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = item / g.P, q = item - b * g.P;
+    const int w = p.wl ? p.wl[b] : 0;
+    const int k0x = g.k0[q][w][0], k0y = g.k0[q][w][1];
+    const float2* wtab = p.t.win_tab + (size_t)(q * g.L + w) * whw;
+
+    for (int a = 0; a < p.A; ++a) {
+      const int64_t f = p.members ? (int64_t)p.members[(int64_t)b * p.A + a] : (int64_t)b * p.A + a;
+      row_pass(p, f, q, k0x, R, S0, S1, pl_nx);
+      col_pass(p, k0y, wtab, R, S0, pl_ny, Wt);
+      if (p.A > 1) {
+        // constructive average (holopipe/engine.py:543-552), complex128 accumulator
+        if (a == 0) {
+          for (int i = threadIdx.x; i < whw; i += blockDim.x)
+            Acc[i] = make_double2(Wt[i].x, Wt[i].y);
+        } else {
+          double v[2] = {0.0, 0.0};
+          for (int i = threadIdx.x; i < whw; i += blockDim.x) {
+            const double2 ac = Acc[i];
+            const float2 m = Wt[i];
+            v[0] += ac.x * m.x + ac.y * m.y;
+            v[1] += ac.x * m.y - ac.y * m.x;
+          }
+          block_sum<2>(v, red);
+          const double mag = hypot(v[0], v[1]);
+          const double cr = mag > 0.0 ? v[0] / mag : 1.0, ci = mag > 0.0 ? -v[1] / mag : 0.0;
+          for (int i = threadIdx.x; i < whw; i += blockDim.x) {
+            const float2 m = Wt[i];
+            double2 ac = Acc[i];
+            ac.x += m.x * cr - m.y * ci;
+            ac.y += m.x * ci + m.y * cr;
+            Acc[i] = ac;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    if (p.A > 1) {
+      const double inv = 1.0 / p.A;
+      for (int i = threadIdx.x; i < whw; i += blockDim.x)
+        Wt[i] = make_float2((float)(Acc[i].x * inv), (float)(Acc[i].y * inv));
+      __syncthreads();
+    }
+    if (p.windows) {
+      float2* wo = p.windows + (size_t)item * whw;
+      for (int i = threadIdx.x; i < whw; i += blockDim.x) wo[i] = Wt[i];
+    }
+
+    // ---------------- inverse transform on the (gh x gw) grid
+    float2* grid = Wt;
+    if (g.gh != g.wh || g.gw != g.ww) {  // resolution mode 0: centred embedding
+      const int r0 = g.gh / 2 - g.wh / 2, c0 = g.gw / 2 - g.ww / 2;
+      for (int i = threadIdx.x; i < ghw; i += blockDim.x) {
+        const int y = i / g.gw, x = i - y * g.gw;
+        const int r = y - r0, c = x - c0;
+        Gd[i] = (r >= 0 && r < g.wh && c >= 0 && c < g.ww) ? Wt[r * g.ww + c] : make_float2(0.f, 0.f);
+      }
+      __syncthreads();
+      grid = Gd;
+    }
+    float2* r1 = stockham<true>(grid, S0, pl_gw, g.gh, g.gw, 1);
+    float2* F = stockham<true>(r1, r1 == grid ? S0 : grid, pl_gh, g.gw, 1, g.gw);
+
+    // ---------------- removal phase, calibrations, summary, peak
+    const float2* ex = p.t.rem_x + (size_t)(q * g.L + w) * g.gw;
+    const float2* ey = p.t.rem_y + (size_t)(q * g.L + w) * g.gh;
+    float2 bc = make_float2(1.f, 0.f);
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * ghw : nullptr;
+    float lmax = 0.f, amax = -1.f;
+    int aidx = 0x7fffffff;
+    double st[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = threadIdx.x; i < ghw; i += blockDim.x) {
+      const int y = i / g.gw, x = i - y * g.gw;
+      float2 v = cmul(cmul(F[i], __ldg(&ey[y])), __ldg(&ex[x]));
+      if (p.bcal) v = cmul(v, bc);
+      if (rc) v = cmul(v, rc[i]);
+      F[i] = v;
+      lmax = fmaxf(lmax, fmaxf(fabsf(v.x), fabsf(v.y)));
+      if (p.raw) p.raw[(size_t)item * ghw + i] = v;
+      if (summary) {
+        const float mag = hypotf(v.x, v.y);
+        const double I = (double)mag * (double)mag;
+        st[0] += I;
+        st[1] += I * __ldg(&p.t.xad[x]);
+        st[2] += I * __ldg(&p.t.yad[y]);
+        st[3] += I * I;
+        const double ang = 2.0 * M_PI * (__ldg(&p.t.yad[y]) - __ldg(&p.t.yad[0])) / span;
+        double sn, cs;
+        sincos(ang, &sn, &cs);
+        st[4] += I * cs;
+        st[5] += I * sn;
+        if (mag > amax) { amax = mag; aidx = i; }
+        agg[(size_t)q * ghw + i] += I;
+      }
+    }
+    const float peak = block_max(lmax, redf);
+    if (summary) {
+      block_sum<6>(st, red);
+      block_argmax(amax, aidx, redf, redi);
+      if (threadIdx.x == 0 && p.params)
+        write_params(p.params, g.P, p.param_slots, q, b, st, amax, aidx, da, p.t.yad[0], span);
+    }
+    const float scale = peak > 0.f ? (float)(32767.0 / (double)peak) : 1.0f;
+    // ---------------- int16 packing (holopipe/pipeline.py:188-199), dequantised copy
+    int16_t* fro = p.fr + (size_t)item * ghw;
+    int16_t* fio = p.fi + (size_t)item * ghw;
+    for (int i = threadIdx.x; i < ghw; i += blockDim.x) {
+      const float2 v = F[i];
+      const int qr = __float2int_rn(__fmul_rn(v.x, scale));
+      const int qi = __float2int_rn(__fmul_rn(v.y, scale));
+      fro[i] = (int16_t)qr;
+      fio[i] = (int16_t)qi;
+      F[i] = make_float2(__fdiv_rn((float)qr, scale), __fdiv_rn((float)qi, scale));
+    }
+    if (threadIdx.x == 0) p.scale[item] = scale;
+    __syncthreads();
+    if (p.coefs && g.G > 0) {
+      float2* U = (F == S0) ? S1 : S0;
+      if (F != S0 && F != S1) U = S1;
+      overlap(p, q, F, U, p.coefs + (size_t)item * g.M);
+    }
+    __syncthreads();
+  }
+}
+
+// Generic plane statistics (holopipe/analysis.py:39-94) of complex data
+// [count][P][h][w]: one CTA per (frame, pol) item writes its seven parameters
+// and accumulates |F|^2 into its own fp64 aggregate image (deterministic:
+// the finalize kernel sums the per-CTA images in a fixed order).
+struct PlaneArgs {
+  const float2* data;
+  int64_t count;
+  int P, h, w;
+  const double* xa;
+  const double* ya;
+  float* params;
+  int slots;
+  char* agg;           // per-CTA [P][h][w] doubles
+  int64_t agg_per_cta; // bytes
+  float* total;        // [h][w] or NULL
+  int agg_slot;        // slot index of the aggregate column
+  int nblocks;         // CTAs that produced partials (finalize)
+};
+
+__device__ void stats_loop(const PlaneArgs& a, int q, const float2* d, double* agg, double* st, float& amax,
+                           int& aidx) {
+  const int hw = a.h * a.w;
+  const double span = (a.h > 1 ? fabs(a.ya[1] - a.ya[0]) : 1.0) * a.h;
+  for (int i = threadIdx.x; i < hw; i += blockDim.x) {
+    const int y = i / a.w, x = i - y * a.w;
+    const float2 v = d[i];
+    const float mag = hypotf(v.x, v.y);
+    const double I = (double)mag * (double)mag;
+    st[0] += I;
+    st[1] += I * a.xa[x];
+    st[2] += I * a.ya[y];
+    st[3] += I * I;
+    double sn, cs;
+    sincos(2.0 * M_PI * (a.ya[y] - a.ya[0]) / span, &sn, &cs);
+    st[4] += I * cs;
+    st[5] += I * sn;
+    if (mag > amax) { amax = mag; aidx = i; }
+    agg[(size_t)q * hw + i] += I;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) plane_stats_kernel(const PlaneArgs a) {
+  __shared__ double red[8][32];
+  __shared__ float redf[32];
+  __shared__ int redi[32];
+  const int hw = a.h * a.w;
+  double* agg = reinterpret_cast<double*>(a.agg + (int64_t)blockIdx.x * a.agg_per_cta);
+  for (int i = threadIdx.x; i < a.P * hw; i += blockDim.x) agg[i] = 0.0;
+  __syncthreads();
+  const double dx = a.w > 1 ? fabs(a.xa[1] - a.xa[0]) : 1.0;
+  const double dy = a.h > 1 ? fabs(a.ya[1] - a.ya[0]) : 1.0;
+  for (int64_t item = blockIdx.x; item < a.count * a.P; item += gridDim.x) {
+    const int q = (int)(item % a.P);
+    const int64_t f = item / a.P;
+    double st[6] = {0, 0, 0, 0, 0, 0};
+    float amax = -1.f;
+    int aidx = 0x7fffffff;
+    stats_loop(a, q, a.data + (size_t)item * hw, agg, st, amax, aidx);
+    block_sum<6>(st, red);
+    block_argmax(amax, aidx, redf, redi);
+    if (threadIdx.x == 0)
+      write_params(a.params, a.P, a.slots, q, (int)f, st, amax, aidx, dx * dy, a.ya[0], dy * a.h);
+  }
+}
+
+// Aggregate slot: per-pixel sum of the per-CTA images in fixed CTA order, then
+// the seven parameters on the summed intensity with MAXABS = max sqrt(sum)
+// (analysis.py:88-91) and the total over pols (analysis.py:92).
+__global__ void __launch_bounds__(kThreads) plane_finalize_kernel(const PlaneArgs a) {
+  __shared__ double red[8][32];
+  __shared__ float redf[32];
+  __shared__ int redi[32];
+  const int q = blockIdx.x;
+  const int hw = a.h * a.w;
+  const int64_t stride = a.agg_per_cta / (int64_t)sizeof(double);
+  const double* base = reinterpret_cast<const double*>(a.agg);
+  const double dx = a.w > 1 ? fabs(a.xa[1] - a.xa[0]) : 1.0;
+  const double dy = a.h > 1 ? fabs(a.ya[1] - a.ya[0]) : 1.0;
+  const double span = dy * a.h;
+  double st[6] = {0, 0, 0, 0, 0, 0};
+  double amax = -1.0;
+  int aidx = 0x7fffffff;
+  for (int i = threadIdx.x; i < hw; i += blockDim.x) {
+    const int y = i / a.w, x = i - y * a.w;
+    double I = 0.0;
+    for (int c = 0; c < a.nblocks; ++c) I += base[c * stride + (size_t)q * hw + i];
+    st[0] += I;
+    st[1] += I * a.xa[x];
+    st[2] += I * a.ya[y];
+    st[3] += I * I;
+    double sn, cs;
+    sincos(2.0 * M_PI * (a.ya[y] - a.ya[0]) / span, &sn, &cs);
+    st[4] += I * cs;
+    st[5] += I * sn;
+    if (I > amax) { amax = I; aidx = i; }
+    if (a.total && q == 0) {
+      double tI = I;
+      for (int qq = 1; qq < a.P; ++qq)
+        for (int c = 0; c < a.nblocks; ++c) tI += base[c * stride + (size_t)qq * hw + i];
+      a.total[i] = (float)tI;
+    }
+  }
+  block_sum<6>(st, red);
+  float fm = (float)sqrt(fmax(amax, 0.0));
+  // argmax on the fp64 intensity (sqrt is monotonic), ties -> first index
+  {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, amax, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, aidx, o);
+      if (ov > amax || (ov == amax && oi < aidx)) { amax = ov; aidx = oi; }
+    }
+    __syncthreads();
+    if (l == 0) { red[6][w] = amax; redi[w] = aidx; }
+    __syncthreads();
+    amax = red[6][0];
+    aidx = redi[0];
+    for (int j = 1; j < nw; ++j)
+      if (red[6][j] > amax || (red[6][j] == amax && redi[j] < aidx)) { amax = red[6][j]; aidx = redi[j]; }
+    fm = (float)sqrt(fmax(amax, 0.0));
+  }
+  if (threadIdx.x == 0) write_params(a.params, a.P, a.slots, q, a.agg_slot, st, fm, aidx, dx * dy, a.ya[0], span);
+}
+
+// Overlap of already-quantised fields: one CTA per (row, pol).
+__global__ void __launch_bounds__(kThreads) coefs_kernel(const __grid_constant__ RunParams p) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int ghw = g.gh * g.gw;
+  float2* F = reinterpret_cast<float2*>(smem);
+  float2* U = F + ghw;
+  for (int item = blockIdx.x; item < p.B * g.P; item += gridDim.x) {
+    const float s = p.scale[item];
+    for (int i = threadIdx.x; i < ghw; i += blockDim.x)
+      F[i] = make_float2(__fdiv_rn((float)p.fr[(size_t)item * ghw + i], s),
+                         __fdiv_rn((float)p.fi[(size_t)item * ghw + i], s));
+    __syncthreads();
+    overlap(p, item % g.P, F, U, p.coefs + (size_t)item * g.M);
+  }
+}
+
+// ------------------------------------------------------- full R2C plane
+// plane[f][q][ky][kx], kx < nx/2+1 (holopipe/pipeline.py:47-59).
+__global__ void __launch_bounds__(kThreads) fourier_full_kernel(const __grid_constant__ RunParams p,
+                                                               int64_t F, float2* plane) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  char* slab = p.lay.slab_bytes ? p.work + (int64_t)blockIdx.x * p.lay.slab_bytes : nullptr;
+  float2* R = region_ptr(p.lay.R, smem, slab);   // (nx/2+1) columns x ny
+  float2* S0 = region_ptr(p.lay.S0, smem, slab);
+  float2* S1 = region_ptr(p.lay.S1, smem, slab);
+  const FFTPlan pl_nx = make_plan(g.nx, g.nst_nx, g.radix_nx, p.t.tw_nx);
+  const FFTPlan pl_ny = make_plan(g.ny, g.nst_ny, g.radix_ny, p.t.tw_ny);
+  const int nx = g.nx, ny = g.ny, ny2 = ny / 2, nh = nx / 2 + 1;
+  for (int64_t item = blockIdx.x; item < F * g.P; item += gridDim.x) {
+    const int64_t f = item / g.P;
+    const int q = (int)(item - f * g.P);
+    const int col0 = g.col0[q], row0 = g.row0[q];
+    for (int c0 = 0; c0 < ny2; c0 += p.lay.CH) {
+      const int ch = min(p.lay.CH, ny2 - c0);
+      for (int idx = threadIdx.x; idx < ch * nx; idx += blockDim.x) {
+        const int s = idx / nx, x = idx - s * nx, y = c0 + s;
+        S0[idx] = make_float2(load_px(p.frames, p.fmt, p.transpose, g.W, g.H, f, row0 + y, col0 + x),
+                              load_px(p.frames, p.fmt, p.transpose, g.W, g.H, f, row0 + y + ny2, col0 + x));
+      }
+      __syncthreads();
+      const float2* Z = stockham<false>(S0, S1, pl_nx, ch, nx, 1);
+      for (int idx = threadIdx.x; idx < ch * nh; idx += blockDim.x) {
+        const int c = idx / ch, s = idx - c * ch;
+        const int km = c ? nx - c : 0;
+        const float2 zk = Z[s * nx + c], zm = Z[s * nx + km];
+        R[c * ny + c0 + s] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+        R[c * ny + c0 + s + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+      }
+      __syncthreads();
+    }
+    float2* out = plane + (size_t)item * ny * nh;
+    for (int c0 = 0; c0 < nh; c0 += p.lay.CC) {
+      const int cc = min(p.lay.CC, nh - c0);
+      const float2* res = stockham<false>(R + (size_t)c0 * ny, S0, pl_ny, cc, ny, 1);
+      for (int idx = threadIdx.x; idx < ny * cc; idx += blockDim.x) {
+        const int ky = idx / cc, j = idx - ky * cc;
+        out[(size_t)ky * nh + c0 + j] = res[j * ny + ky];
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_fused(const RunParams& p, cudaStream_t s) {
+  fused_kernel<<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_finalize(const RunParams& p, float* total, cudaStream_t s) {
+  PlaneArgs a{};
+  a.P = p.g.P; a.h = p.g.gh; a.w = p.g.gw;
+  a.xa = p.t.xad; a.ya = p.t.yad;
+  a.params = p.params; a.slots = p.param_slots;
+  a.agg = p.work + p.lay.agg_off; a.agg_per_cta = p.lay.agg_per_cta;
+  a.total = total; a.agg_slot = p.B; a.nblocks = p.lay.grid;
+  plane_finalize_kernel<<<p.g.P, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
+                                 const double* ya, float* params, int slots, float* total, char* work,
+                                 int grid, cudaStream_t s) {
+  PlaneArgs a{};
+  a.data = data; a.count = count; a.P = P; a.h = h; a.w = w; a.xa = xa; a.ya = ya;
+  a.params = params; a.slots = slots; a.agg = work;
+  a.agg_per_cta = ((int64_t)P * h * w * 8 + 255) / 256 * 256;
+  a.total = total; a.agg_slot = (int)count; a.nblocks = grid;
+  plane_stats_kernel<<<grid, kThreads, 0, s>>>(a);
+  plane_finalize_kernel<<<P, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s) {
+  const int smem = (p.g.gh * p.g.gw + p.g.gh * p.g.G) * (int)sizeof(float2);
+  coefs_kernel<<<grid, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+cudaError_t launch_fourier_full(const RunParams& p, int64_t F, float2* plane, cudaStream_t s) {
+  fourier_full_kernel<<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p, F, plane);
+  return cudaGetLastError();
+}
+cudaError_t set_smem_limits() {
+  cudaError_t e = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(fourier_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(coefs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
+}  // namespace holo

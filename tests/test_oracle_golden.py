@@ -1,0 +1,54 @@
+"""Pin the CPU oracle against fixtures produced by the reference itself (CPU)."""
+
+import numpy as np
+import pytest
+
+from oracle import holo_oracle as O
+from tests.golden.cases import CASES
+from tests.golden_util import load, rel_l2_rows
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_oracle_matches_reference_fixture(name):
+    case, g, frames = load(name)
+    cfg = O.Cfg(**case["config"])
+    out = O.run_chain(cfg, frames, batch_cal=case.get("batch_cal"))
+    # int16 fields, scales and field-plane analysis are bit-exact
+    assert np.array_equal(out["fr"], g["fr"]) and np.array_equal(out["fi"], g["fi"])
+    assert np.array_equal(out["scale"], g["scale"])
+    assert np.array_equal(out["field_params"].view(np.int32), g["field_params"].view(np.int32))
+    assert np.array_equal(out["field_inten"], g["field_inten"])
+    assert np.array_equal(out["k0"], g["k0"])
+    if "coefs" in g:
+        assert rel_l2_rows(out["coefs_out"], g["coefs"]) <= 1e-6
+        m = O.chain_metrics(cfg, out["coefs"], out["mode_count"])
+        assert np.allclose(m, g["metrics"], atol=1e-4, rtol=0)
+    if "fourier_params" in g:
+        fp, fi = O.plane_stats(out["plane"], *_fourier_axes(cfg))
+        assert np.allclose(fp, g["fourier_params"], rtol=1e-6, atol=0)
+        assert np.allclose(fi, g["fourier_inten"], rtol=1e-6)
+        assert np.array_equal(out["window"], g["window"])
+
+
+def _fourier_axes(cfg):
+    # holopipe/engine.py:157-161 + geometry.py:86-89
+    nx, ny, p, lam = cfg.fftWindowSizeX, cfg.fftWindowSizeY, cfg.framePixelSize, cfg.wavelengthCentre
+    fx = np.degrees(np.arcsin(np.clip(np.arange(nx // 2 + 1) * lam / (nx * p), -1, 1)))
+    fy = np.degrees(np.arcsin(np.clip(np.fft.fftfreq(ny) * ny * lam / (ny * p), -1, 1)))
+    return fx, fy
+
+
+def test_quantise_matches_reference_rounding(rng):
+    # pipeline.py:188-199: float32 product, half-to-even, float32(32767/peak)
+    f = (rng.standard_normal((3, 2, 8, 8)) + 1j * rng.standard_normal((3, 2, 8, 8))).astype(np.complex64)
+    f[0, 0] = 0
+    fr, fi, s = O.pack_int16(f)
+    assert s[0, 0] == np.float32(1.0)
+    peak = max(float(np.abs(f[1, 1].real).max()), float(np.abs(f[1, 1].imag).max()))
+    assert s[1, 1] == np.float32(32767.0 / peak)
+    assert np.array_equal(fr[1, 1], np.rint(f[1, 1].real * s[1, 1]).astype(np.int16))
+
+
+def test_mode_order_group_major():
+    assert O.mode_list(3) == [(0, 0), (1, 0), (0, 1), (2, 0), (1, 1), (0, 2)]
+    assert [O.group_of_mode(i) for i in range(6)] == [0, 1, 1, 2, 2, 2]
