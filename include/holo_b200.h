@@ -123,6 +123,7 @@ typedef struct hpg_outputs {
 
 /* hpg_run flags */
 #define HPG_FLAG_SUMMARY 1u      /* per-row field summary + aggregate partials */
+#define HPG_FLAG_GENERIC 2u      /* diagnostic: force the generic (any-size) kernel */
 
 int hpg_version(void);
 int hpg_plan_create(const hpg_plan_desc* desc, hpg_plan** out);

@@ -1,0 +1,320 @@
+// Register-resident fused kernel for the hot geometry class: 128 x 128 FFT
+// window, a WH x WW (42 x 42 for BASELINE) Fourier window, IFFT resolution
+// mode 1, no averaging, no fill-factor correction.  Same algorithm and
+// numerical conventions as the generic kernel (holo_pipeline.cu), with every
+// size a compile-time constant:
+//
+//   row pass    8 threads per (row y, row y+64) pair, 16 points per thread:
+//               DFT-16 in registers -> twiddle W128^(t k1) -> 8x16 transpose
+//               through a padded shared tile -> DFT-8 -> keep only the bins
+//               the window needs (both +k and -k for the Hermitian split)
+//   column pass 8 threads per kept column: Hermitian split on load, same
+//               128-point FFT, keep the WH needed rows, mask * recentring
+//               phase (separable tables, circle as per-row column ranges)
+//   IFFT        compile-time Stockham (42 = 6 x 7) along rows then columns
+//   epilogue    removal phase, block peak, int16 packing, separable overlap
+//
+// Frames are read straight from HBM into registers (each warp load touches
+// four full 32-byte sectors), so the only HBM traffic is the window read and
+// the int16 / scale / coefficient writes.
+#include <algorithm>
+
+#include "holo_internal.h"
+
+namespace holo {
+
+// ----------------------------------------------------- fast-path tables
+// (device pointers appended to DevTables by the C ABI)
+struct FastTables {
+  const int16_t* slot;     // [P][L][128] slot of bin k in the zs row, -1 if unused
+  const int16_t* cslot;    // [P][L][WW][2] (slot of +kx_c, slot of -kx_c)
+  const float2* px;        // [P][L][WW] recentring phase along x
+  const float2* py;        // [P][L][WH] recentring phase along y
+  const int16_t* mrange;   // [WH][2] first/last column inside the circular mask
+  int nslots;              // max slots used (<= 2*WW)
+};
+
+template <int N, int P>
+HOLO_DEV void ct_stage_read(const float2* src, float2* v, int base, int stride) {
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] = src[base + j * stride];
+}
+
+// Compile-time Stockham stage over COUNT sequences of length N (see holo_fft.cuh
+// for the index algebra); element e of sequence q at q*SS + e*ES.
+template <int P, int N, int L, int COUNT, int SS, int ES, bool INV>
+HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw) {
+  constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
+  for (int task = threadIdx.x; task < total; task += blockDim.x) {
+    int q, r;
+    if (SS == 1) { q = task % COUNT; r = task / COUNT; }
+    else { q = task / per; r = task - q * per; }
+    const int k = r / mp, qp = r - k * mp;
+    float2 v[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = src[q * SS + (k * m_in + qp + mp * j) * ES];
+    if (L > 1) {
+#pragma unroll
+      for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<INV>(tw[(j * k * mp) % N]));
+    }
+    dft_fixed<P, INV>(v);
+#pragma unroll
+    for (int t = 0; t < P; ++t) dst[q * SS + ((k + L * t) * mp + qp) * ES] = v[t];
+  }
+}
+
+template <int N> struct Radix2 { static constexpr int a = 6, b = 7; };
+
+template <int WH, int WW>
+struct FastLayout {
+  static constexpr int ZS = 2 * WW + 2;            // padded zs row (float2)
+  static constexpr int XG = 152;                   // exchange tile per 8-thread group (float2)
+  static constexpr size_t xbuf = 0;                                        // [32][XG]
+  static constexpr size_t zs = xbuf + 32 * XG * sizeof(float2);            // [64][ZS]
+  static constexpr size_t W = zs + 64 * ZS * sizeof(float2);               // [WH*WW]
+  static constexpr size_t tw128 = W + WH * WW * sizeof(float2);            // [128]
+  static constexpr size_t twh = tw128 + 128 * sizeof(float2);              // [WH]
+  static constexpr size_t tww = twh + WH * sizeof(float2);                 // [WW]
+  static constexpr size_t slot = tww + WW * sizeof(float2);                // int16 [128]
+  static constexpr size_t bytes = slot + 128 * sizeof(int16_t) + 64;
+  static_assert(WH * WW <= 32 * XG, "IFFT ping-pong must fit the exchange tile");
+};
+
+template <int WH, int WW>
+__global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__ RunParams p,
+                                                        const __grid_constant__ FastTables ft) {
+  using LY = FastLayout<WH, WW>;
+  extern __shared__ __align__(16) char smem[];
+  __shared__ float redf[32];
+  float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
+  float2* zs = reinterpret_cast<float2*>(smem + LY::zs);
+  float2* Wb = reinterpret_cast<float2*>(smem + LY::W);
+  float2* tw128 = reinterpret_cast<float2*>(smem + LY::tw128);
+  float2* twh = reinterpret_cast<float2*>(smem + LY::twh);
+  float2* tww = reinterpret_cast<float2*>(smem + LY::tww);
+  int16_t* slot = reinterpret_cast<int16_t*>(smem + LY::slot);
+  const Geometry& g = p.g;
+  const int tid = threadIdx.x, t = tid & 7, grp = tid >> 3;
+  float2* xg = xbuf + grp * LY::XG;
+
+  for (int i = tid; i < 128; i += blockDim.x) tw128[i] = p.t.tw_nx[i];
+  for (int i = tid; i < WH; i += blockDim.x) twh[i] = p.t.tw_gh[i];
+  for (int i = tid; i < WW; i += blockDim.x) tww[i] = p.t.tw_gw[i];
+
+  const int items = p.B * g.P;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = item / g.P, q = item - b * g.P;
+    const int w = p.wl ? p.wl[b] : 0;
+    const int pl = q * g.L + w;
+    const int k0y = g.k0[q][w][1];
+    __syncthreads();  // previous item done with every buffer
+    for (int i = tid; i < 128; i += blockDim.x) slot[i] = ft.slot[pl * 128 + i];
+    __syncthreads();
+
+    // ------------------------------------------------------------ row pass
+    const int64_t f = (int64_t)b;  // A == 1 on this path
+    const int W = g.W, H = g.H;
+    const int col0 = g.col0[q], row0 = g.row0[q];
+#pragma unroll 1
+    for (int rnd = 0; rnd < 2; ++rnd) {
+      const int pr = rnd * 32 + grp;
+      float2 z[16];
+      if (p.fmt == 0) {
+        const float* fa = reinterpret_cast<const float*>(p.frames) + f * (int64_t)W * H +
+                          (int64_t)(row0 + pr) * W + col0 + t;
+        const float* fb = fa + (int64_t)64 * W;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = make_float2(__ldg(fa + 8 * j), __ldg(fb + 8 * j));
+      } else {
+        const unsigned short* fa = reinterpret_cast<const unsigned short*>(p.frames) + f * (int64_t)W * H +
+                                   (int64_t)(row0 + pr) * W + col0 + t;
+        const unsigned short* fb = fa + (int64_t)64 * W;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = make_float2((float)__ldg(fa + 8 * j), (float)__ldg(fb + 8 * j));
+      }
+      dft16<false>(z);
+#pragma unroll
+      for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], tw128[(t * k1) & 127]);
+#pragma unroll
+      for (int k1 = 0; k1 < 16; ++k1) xg[k1 * 9 + t] = z[k1];
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k1 = t + 8 * h;
+        float2 v[8];
+#pragma unroll
+        for (int tp = 0; tp < 8; ++tp) v[tp] = xg[k1 * 9 + tp];
+        dft8<false>(v);
+#pragma unroll
+        for (int k2 = 0; k2 < 8; ++k2) {
+          const int s = slot[k1 + 16 * k2];
+          if (s >= 0) zs[pr * LY::ZS + s] = v[k2];
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // --------------------------------------------------------- column pass
+    const int kys = ((k0y - WH / 2) % 128 + 128) % 128;
+#pragma unroll 1
+    for (int rnd = 0; rnd < (WW + 31) / 32; ++rnd) {
+      const int c = rnd * 32 + grp;
+      const bool active = c < WW;
+      float2 z[16];
+      if (active) {
+        const int sp = ft.cslot[(pl * WW + c) * 2], sm = ft.cslot[(pl * WW + c) * 2 + 1];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const float2 zk = zs[(t + 8 * jj) * LY::ZS + sp], zm = zs[(t + 8 * jj) * LY::ZS + sm];
+          z[jj] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+          z[jj + 8] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+        }
+        dft16<false>(z);
+#pragma unroll
+        for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], tw128[(t * k1) & 127]);
+#pragma unroll
+        for (int k1 = 0; k1 < 16; ++k1) xg[k1 * 9 + t] = z[k1];
+      }
+      __syncwarp();
+      if (active) {
+        const float2 pxc = ft.px[pl * WW + c];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k1 = t + 8 * h;
+          float2 v[8];
+#pragma unroll
+          for (int tp = 0; tp < 8; ++tp) v[tp] = xg[k1 * 9 + tp];
+          dft8<false>(v);
+#pragma unroll
+          for (int k2 = 0; k2 < 8; ++k2) {
+            const int r = (k1 + 16 * k2 - kys) & 127;
+            if (r < WH) {
+              const int lo = ft.mrange[2 * r], hi = ft.mrange[2 * r + 1];
+              float2 val = make_float2(0.f, 0.f);
+              if (c >= lo && c <= hi) val = cmul(v[k2], cmul(ft.py[pl * WH + r], pxc));
+              Wb[r * WW + c] = val;
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ IFFT (rows, then columns)
+    float2* T = xbuf;
+    ct_stage<6, WW, 1, WH, WW, 1, true>(Wb, T, tww);
+    __syncthreads();
+    ct_stage<7, WW, 6, WH, WW, 1, true>(T, Wb, tww);
+    __syncthreads();
+    ct_stage<6, WH, 1, WW, 1, WW, true>(Wb, T, twh);
+    __syncthreads();
+    ct_stage<7, WH, 6, WW, 1, WW, true>(T, Wb, twh);
+    __syncthreads();
+
+    // ------------------------------------------- removal phase, peak, int16
+    const float2* ex = p.t.rem_x + (size_t)pl * WW;
+    const float2* ey = p.t.rem_y + (size_t)pl * WH;
+    float2 bc = make_float2(1.f, 0.f);
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    float lmax = 0.f;
+    for (int i = tid; i < WH * WW; i += blockDim.x) {
+      const int y = i / WW, x = i - y * WW;
+      float2 v = cmul(cmul(Wb[i], __ldg(&ey[y])), __ldg(&ex[x]));
+      if (p.bcal) v = cmul(v, bc);
+      Wb[i] = v;
+      lmax = fmaxf(lmax, fmaxf(fabsf(v.x), fabsf(v.y)));
+      if (p.raw) p.raw[(size_t)item * WH * WW + i] = v;
+    }
+    // block max
+    {
+      float v = lmax;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if ((tid & 31) == 0) redf[tid >> 5] = v;
+      __syncthreads();
+      v = redf[0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) v = fmaxf(v, redf[j]);
+      lmax = v;
+    }
+    const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
+    int16_t* fro = p.fr + (size_t)item * WH * WW;
+    int16_t* fio = p.fi + (size_t)item * WH * WW;
+    for (int i = tid; i < WH * WW / 2; i += blockDim.x) {
+      const float2 v0 = Wb[2 * i], v1 = Wb[2 * i + 1];
+      const int r0 = __float2int_rn(__fmul_rn(v0.x, scale)), i0 = __float2int_rn(__fmul_rn(v0.y, scale));
+      const int r1 = __float2int_rn(__fmul_rn(v1.x, scale)), i1 = __float2int_rn(__fmul_rn(v1.y, scale));
+      reinterpret_cast<int*>(fro)[i] = (r0 & 0xffff) | (r1 << 16);
+      reinterpret_cast<int*>(fio)[i] = (i0 & 0xffff) | (i1 << 16);
+      Wb[2 * i] = make_float2(__fdiv_rn((float)r0, scale), __fdiv_rn((float)i0, scale));
+      Wb[2 * i + 1] = make_float2(__fdiv_rn((float)r1, scale), __fdiv_rn((float)i1, scale));
+    }
+    if (tid == 0) p.scale[item] = scale;
+    __syncthreads();
+
+    // ---------------------------------------------------------- HG overlap
+    if (p.coefs && g.G > 0) {
+      const int G = g.G;
+      float2* U = xbuf;
+      const float* hx = p.t.hx + (size_t)q * G * WW;
+      const float* hy = p.t.hy + (size_t)q * G * WH;
+      for (int idx = tid; idx < WH * G; idx += blockDim.x) {
+        const int y = idx / G, m = idx - y * G;
+        const float2* row = Wb + y * WW;
+        const float* h = hx + m * WW;
+        float ax = 0.f, ay = 0.f;
+#pragma unroll 6
+        for (int x = 0; x < WW; ++x) {
+          const float2 v = row[x];
+          const float hv = __ldg(&h[x]);
+          ax = fmaf(v.x, hv, ax);
+          ay = fmaf(v.y, hv, ay);
+        }
+        U[idx] = make_float2(ax, ay);
+      }
+      __syncthreads();
+      const float d = g.dxdy[q];
+      float2* out = p.coefs + (size_t)item * g.M;
+      for (int i = tid; i < g.M; i += blockDim.x) {
+        const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+        const float* h = hy + n * WH;
+        float ax = 0.f, ay = 0.f;
+#pragma unroll 6
+        for (int y = 0; y < WH; ++y) {
+          const float2 v = U[y * G + m];
+          const float hv = __ldg(&h[y]);
+          ax = fmaf(v.x, hv, ax);
+          ay = fmaf(v.y, hv, ay);
+        }
+        out[i] = make_float2(ax * d, ay * d);
+      }
+    }
+  }
+}
+
+bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
+                    unsigned flags, const void* windows) {
+  return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
+         !(fmt == 1 && transpose) && !fill && rcal == nullptr && (flags & 1u) == 0 && windows == nullptr;
+}
+
+cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
+  using LY = FastLayout<42, 42>;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(fast128_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)LY::bytes);
+    if (e != cudaSuccess) return e;
+    init = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast128_kernel<42, 42>, 256, LY::bytes);
+  const int items = p.B * p.g.P;
+  const int grid = std::max(1, std::min(items, num_sms * std::max(per_sm, 1)));
+  fast128_kernel<42, 42><<<grid, 256, LY::bytes, s>>>(p, ft);
+  return cudaGetLastError();
+}
+
+}  // namespace holo

@@ -598,12 +598,24 @@ cudaError_t launch_fourier_full(const RunParams& p, int64_t F, float2* plane, cu
   fourier_full_kernel<<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p, F, plane);
   return cudaGetLastError();
 }
+template <typename K>
+static cudaError_t raise_smem(K kernel) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  e = cudaFuncGetAttributes(&fa, kernel);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              optin - (int)fa.sharedSizeBytes);
+}
 cudaError_t set_smem_limits() {
-  cudaError_t e = cudaFuncSetAttribute(fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  cudaError_t e = raise_smem(fused_kernel);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(fourier_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  e = raise_smem(fourier_full_kernel);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(coefs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  return raise_smem(coefs_kernel);
 }
 
 }  // namespace holo

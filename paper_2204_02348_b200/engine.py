@@ -91,6 +91,7 @@ class Engine:
         self.window_title = ""
         self.tweak_cycles = 0
         self._device = device
+        self.force_generic = False      # diagnostic: bypass the specialised kernels
         self._plans = collections.OrderedDict()
         self._bufs = {}
         self._clear_products()
@@ -185,6 +186,10 @@ class Engine:
     # ------------------------------------------------------ native plans
     def _plan_key(self, group_count=None, waist=None):
         st0, st1, st2 = self._st0, self._st1, self._st2
+        if st1 is None:   # stage-0 products only (full Fourier plane): window params are inert
+            cfg = self.config
+            st1 = {"tilt": [[0.0, 0.0], [0.0, 0.0]], "radius": float(cfg.fourierWindowRadius),
+                   "lamc": float(cfg.wavelengthCentre), "fill": 0, "mode": 1}
         st2 = st2 or {"tilt": st1["tilt"], "centre": st0["centre"], "defocus": [0.0, 0.0]}
         if group_count is None:
             group_count = max(self.config.basisGroupCount, 0)
@@ -363,7 +368,7 @@ class Engine:
         L.fi = self._buf("fi", (B, P, gh, gw), torch.int16)
         L.sc = self._buf("scale", (B, P), torch.float32)
         L.coefs = self._buf("coefs", (B, P * plan.mode_count), torch.complex64) if (with_coefs and G > 0) else None
-        L.flags = native.HPG_FLAG_SUMMARY if summary else 0
+        L.flags = (native.HPG_FLAG_SUMMARY if summary else 0) | (native.HPG_FLAG_GENERIC if self.force_generic else 0)
         L.params = L.inten = None
         slots = B * A + 1
         if summary:

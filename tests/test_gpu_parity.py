@@ -118,3 +118,17 @@ def test_uint16_source_matches_float32():
     eng.source.set_uint16(np.ascontiguousarray(np.transpose(frames.astype(np.uint16), (0, 2, 1))), 1)
     c = eng.process_batch()[0]
     assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("name", ["pr1", "dualpol", "largebasis", "multiwl", "dualpol_cal"])
+def test_specialised_kernel_matches_generic(name):
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.run_pipeline(0)
+    fast = [t.cpu().numpy().copy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy().copy()]
+    eng.force_generic = True
+    eng.run_pipeline(0)
+    gen = [t.cpu().numpy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()]
+    assert np.abs(fast[0].astype(int) - gen[0]).max() <= 1 and np.abs(fast[1].astype(int) - gen[1]).max() <= 1
+    assert np.allclose(fast[2], gen[2], rtol=1e-5)
+    assert rel_l2_rows(fast[3], gen[3]) <= 2e-5
