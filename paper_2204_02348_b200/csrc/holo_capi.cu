@@ -17,12 +17,9 @@ cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s);
 cudaError_t launch_fourier_full(const RunParams& p, int64_t F, float2* plane, cudaStream_t s);
 cudaError_t set_smem_limits();
 struct FastTables {
-  const int16_t* slot;
-  const int16_t* cslot;
   const float2* px;
   const float2* py;
-  const int16_t* mrange;
-  int nslots;
+  const int16_t* crange;
 };
 bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
                     unsigned flags, const void* windows);
@@ -359,27 +356,15 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   } else {
     mm.push_back(0); mn.push_back(0);
   }
-  // fast-path tables: bin slots for the Hermitian split, separable recentring
-  // phases, circular-mask column ranges (used by holo_fast.cu)
-  std::vector<int16_t> slot((size_t)g.P * g.L * g.nx, -1), cslot((size_t)g.P * g.L * g.ww * 2, 0);
+  // fast-path tables (holo_fast.cu): separable recentring phases and the
+  // circular mask as a row range per column
   std::vector<float2> pxv((size_t)g.P * g.L * g.ww), pyv((size_t)g.P * g.L * g.wh);
-  std::vector<int16_t> mrange((size_t)g.wh * 2);
-  int nslots = 0;
+  std::vector<int16_t> crange((size_t)g.ww * 2);
   for (int q = 0; q < g.P; ++q)
     for (int w = 0; w < g.L; ++w) {
       const size_t pl = (size_t)q * g.L + w;
       const int kx = g.k0[q][w][0], ky = g.k0[q][w][1];
-      int used = 0;
-      auto slot_of = [&](int k) {
-        int16_t& sl = slot[pl * g.nx + k];
-        if (sl < 0) sl = (int16_t)used++;
-        return (int16_t)sl;
-      };
       for (int c = 0; c < g.ww; ++c) {
-        int kp = (kx + c - g.ww / 2) % g.nx; if (kp < 0) kp += g.nx;
-        const int km = kp ? g.nx - kp : 0;
-        cslot[(pl * g.ww + c) * 2] = slot_of(kp);
-        cslot[(pl * g.ww + c) * 2 + 1] = slot_of(km);
         const double ax = 2.0 * kPi * (double)(kx + c - g.ww / 2) * (xi[q][0] - g.nx / 2.0) / g.nx;
         pxv[pl * g.ww + c] = make_float2((float)std::cos(ax), (float)std::sin(ax));
       }
@@ -387,22 +372,20 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
         const double ay = 2.0 * kPi * (double)(ky + r - g.wh / 2) * (xi[q][1] - g.ny / 2.0) / g.ny;
         pyv[pl * g.wh + r] = make_float2((float)std::cos(ay), (float)std::sin(ay));
       }
-      nslots = std::max(nslots, used);
     }
-  for (int r = 0; r < g.wh; ++r) {
-    const double dfy = (double)(r - g.wh / 2) / (g.ny * p);
-    int lo = g.ww, hi = -1;
-    for (int c = 0; c < g.ww; ++c) {
-      const double dfx = (double)(c - g.ww / 2) / (g.nx * p);
-      if (dfy * dfy + dfx * dfx <= fr * fr + 1e-30) { lo = std::min(lo, c); hi = std::max(hi, c); }
+  for (int c = 0; c < g.ww; ++c) {
+    const double dfx = (double)(c - g.ww / 2) / (g.nx * p);
+    int lo = g.wh, hi = -1;
+    for (int r = 0; r < g.wh; ++r) {
+      const double dfy = (double)(r - g.wh / 2) / (g.ny * p);
+      if (dfy * dfy + dfx * dfx <= fr * fr + 1e-30) { lo = std::min(lo, r); hi = std::max(hi, r); }
     }
-    mrange[2 * r] = (int16_t)lo;
-    mrange[2 * r + 1] = (int16_t)hi;
+    crange[2 * c] = (int16_t)lo;
+    crange[2 * c + 1] = (int16_t)hi;
   }
   P->fill = d->fill_factor;
   std::vector<char> blob;
-  const size_t o_sl = push(blob, slot), o_cs = push(blob, cslot), o_px = push(blob, pxv), o_py = push(blob, pyv),
-               o_mr = push(blob, mrange);
+  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange);
   const size_t o_nx = push(blob, tw_nx), o_ny = push(blob, tw_ny), o_gw = push(blob, tw_gw), o_gh = push(blob, tw_gh);
   const size_t o_w = push(blob, wtab), o_rx = push(blob, remx), o_ry = push(blob, remy);
   std::vector<float> hxv = P->hx, hyv = P->hy;
@@ -435,12 +418,9 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->t.yad = reinterpret_cast<const double*>(base + o_yad);
   P->t.mode_m = reinterpret_cast<const int16_t*>(base + o_mm);
   P->t.mode_n = reinterpret_cast<const int16_t*>(base + o_mn);
-  P->ft.slot = reinterpret_cast<const int16_t*>(base + o_sl);
-  P->ft.cslot = reinterpret_cast<const int16_t*>(base + o_cs);
   P->ft.px = reinterpret_cast<const float2*>(base + o_px);
   P->ft.py = reinterpret_cast<const float2*>(base + o_py);
-  P->ft.mrange = reinterpret_cast<const int16_t*>(base + o_mr);
-  P->ft.nslots = nslots;
+  P->ft.crange = reinterpret_cast<const int16_t*>(base + o_cr);
   e = set_smem_limits();
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
   *out = P;
@@ -576,7 +556,7 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
     return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
   cudaError_t e;
   if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&
-      !b->members && P->ft.nslots <= 2 * 42)
+      !b->members)
     e = launch_fast(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
   else
     e = launch_fused(rp, static_cast<cudaStream_t>(stream));

@@ -7,12 +7,14 @@
 //   row pass    8 threads per (row y, row y+64) pair, 16 points per thread:
 //               DFT-16 in registers -> twiddle W128^(t k1) -> 8x16 transpose
 //               through a padded shared tile -> DFT-8 -> keep only the bins
-//               the window needs (both +k and -k for the Hermitian split)
+//               the window needs: zs[pair][c] = Z[kx_c], zs[pair][WW+c] = Z[-kx_c]
+//               (the two halves of the Hermitian split, holopipe/pipeline.py:89-98)
 //   column pass 8 threads per kept column: Hermitian split on load, same
-//               128-point FFT, keep the WH needed rows, mask * recentring
-//               phase (separable tables, circle as per-row column ranges)
+//               128-point FFT, keep the WH needed rows, circular mask (row
+//               range per column) * separable recentring phase (pipeline.py:72-127)
 //   IFFT        compile-time Stockham (42 = 6 x 7) along rows then columns
-//   epilogue    removal phase, block peak, int16 packing, separable overlap
+//   epilogue    removal phase, block peak, int16 packing (pipeline.py:163-199),
+//               separable HG overlap with the basis staged in shared memory
 //
 // Frames are read straight from HBM into registers (each warp load touches
 // four full 32-byte sectors), so the only HBM traffic is the window read and
@@ -23,25 +25,14 @@
 
 namespace holo {
 
-// ----------------------------------------------------- fast-path tables
-// (device pointers appended to DevTables by the C ABI)
 struct FastTables {
-  const int16_t* slot;     // [P][L][128] slot of bin k in the zs row, -1 if unused
-  const int16_t* cslot;    // [P][L][WW][2] (slot of +kx_c, slot of -kx_c)
   const float2* px;        // [P][L][WW] recentring phase along x
   const float2* py;        // [P][L][WH] recentring phase along y
-  const int16_t* mrange;   // [WH][2] first/last column inside the circular mask
-  int nslots;              // max slots used (<= 2*WW)
+  const int16_t* crange;   // [WW][2] first/last row inside the circular mask, per column
 };
 
-template <int N, int P>
-HOLO_DEV void ct_stage_read(const float2* src, float2* v, int base, int stride) {
-#pragma unroll
-  for (int j = 0; j < P; ++j) v[j] = src[base + j * stride];
-}
-
-// Compile-time Stockham stage over COUNT sequences of length N (see holo_fft.cuh
-// for the index algebra); element e of sequence q at q*SS + e*ES.
+// Compile-time Stockham stage over COUNT sequences of length N (index algebra
+// in holo_fft.cuh); element e of sequence q at q*SS + e*ES.
 template <int P, int N, int L, int COUNT, int SS, int ES, bool INV>
 HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw) {
   constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
@@ -63,21 +54,21 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
   }
 }
 
-template <int N> struct Radix2 { static constexpr int a = 6, b = 7; };
-
 template <int WH, int WW>
 struct FastLayout {
   static constexpr int ZS = 2 * WW + 2;            // padded zs row (float2)
   static constexpr int XG = 152;                   // exchange tile per 8-thread group (float2)
+  static constexpr int GP = 48;                    // max basis orders staged (multiple of 4)
   static constexpr size_t xbuf = 0;                                        // [32][XG]
   static constexpr size_t zs = xbuf + 32 * XG * sizeof(float2);            // [64][ZS]
   static constexpr size_t W = zs + 64 * ZS * sizeof(float2);               // [WH*WW]
   static constexpr size_t tw128 = W + WH * WW * sizeof(float2);            // [128]
   static constexpr size_t twh = tw128 + 128 * sizeof(float2);              // [WH]
   static constexpr size_t tww = twh + WH * sizeof(float2);                 // [WW]
-  static constexpr size_t slot = tww + WW * sizeof(float2);                // int16 [128]
-  static constexpr size_t bytes = slot + 128 * sizeof(int16_t) + 64;
+  static constexpr size_t ph = tww + WW * sizeof(float2);                  // px[WW] py[WH] ex[WW] ey[WH]
+  static constexpr size_t bytes = ph + 2 * (WH + WW) * sizeof(float2) + 64;
   static_assert(WH * WW <= 32 * XG, "IFFT ping-pong must fit the exchange tile");
+  static_assert((WH + WW) * GP * sizeof(float) <= 64 * ZS * sizeof(float2), "basis staging must fit zs");
 };
 
 template <int WH, int WW>
@@ -92,7 +83,10 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
   float2* tw128 = reinterpret_cast<float2*>(smem + LY::tw128);
   float2* twh = reinterpret_cast<float2*>(smem + LY::twh);
   float2* tww = reinterpret_cast<float2*>(smem + LY::tww);
-  int16_t* slot = reinterpret_cast<int16_t*>(smem + LY::slot);
+  float2* s_px = reinterpret_cast<float2*>(smem + LY::ph);
+  float2* s_py = s_px + WW;
+  float2* s_ex = s_py + WH;
+  float2* s_ey = s_ex + WW;
   const Geometry& g = p.g;
   const int tid = threadIdx.x, t = tid & 7, grp = tid >> 3;
   float2* xg = xbuf + grp * LY::XG;
@@ -106,10 +100,17 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     const int b = item / g.P, q = item - b * g.P;
     const int w = p.wl ? p.wl[b] : 0;
     const int pl = q * g.L + w;
-    const int k0y = g.k0[q][w][1];
+    const int k0x = g.k0[q][w][0], k0y = g.k0[q][w][1];
+    const int kxs = (k0x - WW / 2) & 127, kys = (k0y - WH / 2) & 127;
     __syncthreads();  // previous item done with every buffer
-    for (int i = tid; i < 128; i += blockDim.x) slot[i] = ft.slot[pl * 128 + i];
-    __syncthreads();
+    for (int i = tid; i < WW; i += blockDim.x) {
+      s_px[i] = ft.px[pl * WW + i];
+      s_ex[i] = p.t.rem_x[pl * WW + i];
+    }
+    for (int i = tid; i < WH; i += blockDim.x) {
+      s_py[i] = ft.py[pl * WH + i];
+      s_ey[i] = p.t.rem_y[pl * WH + i];
+    }
 
     // ------------------------------------------------------------ row pass
     const int64_t f = (int64_t)b;  // A == 1 on this path
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
 #pragma unroll
       for (int k1 = 0; k1 < 16; ++k1) xg[k1 * 9 + t] = z[k1];
       __syncwarp();
+      float2* zrow = zs + pr * LY::ZS;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int k1 = t + 8 * h;
@@ -147,8 +149,10 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
         dft8<false>(v);
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          const int s = slot[k1 + 16 * k2];
-          if (s >= 0) zs[pr * LY::ZS + s] = v[k2];
+          const int k = k1 + 16 * k2;
+          const int cp = (k - kxs) & 127, cm = (128 - k - kxs) & 127;
+          if (cp < WW) zrow[cp] = v[k2];
+          if (cm < WW) zrow[WW + cm] = v[k2];
         }
       }
       __syncwarp();
@@ -156,17 +160,15 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     __syncthreads();
 
     // --------------------------------------------------------- column pass
-    const int kys = ((k0y - WH / 2) % 128 + 128) % 128;
 #pragma unroll 1
     for (int rnd = 0; rnd < (WW + 31) / 32; ++rnd) {
       const int c = rnd * 32 + grp;
       const bool active = c < WW;
       float2 z[16];
       if (active) {
-        const int sp = ft.cslot[(pl * WW + c) * 2], sm = ft.cslot[(pl * WW + c) * 2 + 1];
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-          const float2 zk = zs[(t + 8 * jj) * LY::ZS + sp], zm = zs[(t + 8 * jj) * LY::ZS + sm];
+          const float2 zk = zs[(t + 8 * jj) * LY::ZS + c], zm = zs[(t + 8 * jj) * LY::ZS + WW + c];
           z[jj] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
           z[jj + 8] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
         }
@@ -178,7 +180,8 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
       }
       __syncwarp();
       if (active) {
-        const float2 pxc = ft.px[pl * WW + c];
+        const float2 pxc = s_px[c];
+        const int rlo = ft.crange[2 * c], rhi = ft.crange[2 * c + 1];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int k1 = t + 8 * h;
@@ -190,9 +193,8 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
           for (int k2 = 0; k2 < 8; ++k2) {
             const int r = (k1 + 16 * k2 - kys) & 127;
             if (r < WH) {
-              const int lo = ft.mrange[2 * r], hi = ft.mrange[2 * r + 1];
               float2 val = make_float2(0.f, 0.f);
-              if (c >= lo && c <= hi) val = cmul(v[k2], cmul(ft.py[pl * WH + r], pxc));
+              if (r >= rlo && r <= rhi) val = cmul(v[k2], cmul(s_py[r], pxc));
               Wb[r * WW + c] = val;
             }
           }
@@ -214,20 +216,17 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     __syncthreads();
 
     // ------------------------------------------- removal phase, peak, int16
-    const float2* ex = p.t.rem_x + (size_t)pl * WW;
-    const float2* ey = p.t.rem_y + (size_t)pl * WH;
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
     float lmax = 0.f;
     for (int i = tid; i < WH * WW; i += blockDim.x) {
       const int y = i / WW, x = i - y * WW;
-      float2 v = cmul(cmul(Wb[i], __ldg(&ey[y])), __ldg(&ex[x]));
+      float2 v = cmul(cmul(Wb[i], s_ey[y]), s_ex[x]);
       if (p.bcal) v = cmul(v, bc);
       Wb[i] = v;
       lmax = fmaxf(lmax, fmaxf(fabsf(v.x), fabsf(v.y)));
       if (p.raw) p.raw[(size_t)item * WH * WW + i] = v;
     }
-    // block max
     {
       float v = lmax;
 #pragma unroll
@@ -248,43 +247,60 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
       const int r1 = __float2int_rn(__fmul_rn(v1.x, scale)), i1 = __float2int_rn(__fmul_rn(v1.y, scale));
       reinterpret_cast<int*>(fro)[i] = (r0 & 0xffff) | (r1 << 16);
       reinterpret_cast<int*>(fio)[i] = (i0 & 0xffff) | (i1 << 16);
+      // dequantised copy for the overlap: exactly (float)q / scale (holopipe/engine.py:367-369)
       Wb[2 * i] = make_float2(__fdiv_rn((float)r0, scale), __fdiv_rn((float)i0, scale));
       Wb[2 * i + 1] = make_float2(__fdiv_rn((float)r1, scale), __fdiv_rn((float)i1, scale));
     }
     if (tid == 0) p.scale[item] = scale;
-    __syncthreads();
 
     // ---------------------------------------------------------- HG overlap
     if (p.coefs && g.G > 0) {
       const int G = g.G;
-      float2* U = xbuf;
+      constexpr int GP = LY::GP;
+      float* hxT = reinterpret_cast<float*>(zs);          // [WW][GP]  (zs is free now)
+      float* hyT = hxT + WW * GP;                          // [WH][GP]
+      float2* U = xbuf;                                    // [WH][GP]
       const float* hx = p.t.hx + (size_t)q * G * WW;
       const float* hy = p.t.hy + (size_t)q * G * WH;
-      for (int idx = tid; idx < WH * G; idx += blockDim.x) {
-        const int y = idx / G, m = idx - y * G;
+      for (int i = tid; i < WW * GP; i += blockDim.x) {
+        const int x = i / GP, m = i - x * GP;
+        hxT[i] = m < G ? __ldg(&hx[m * WW + x]) : 0.f;
+      }
+      for (int i = tid; i < WH * GP; i += blockDim.x) {
+        const int y = i / GP, n = i - y * GP;
+        hyT[i] = n < G ? __ldg(&hy[n * WH + y]) : 0.f;
+      }
+      __syncthreads();
+      const int GQ = (G + 3) >> 2;
+      for (int idx = tid; idx < WH * GQ; idx += blockDim.x) {
+        const int y = idx / GQ, mq = idx - y * GQ;
         const float2* row = Wb + y * WW;
-        const float* h = hx + m * WW;
-        float ax = 0.f, ay = 0.f;
+        float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
 #pragma unroll 6
         for (int x = 0; x < WW; ++x) {
           const float2 v = row[x];
-          const float hv = __ldg(&h[x]);
-          ax = fmaf(v.x, hv, ax);
-          ay = fmaf(v.y, hv, ay);
+          const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+          ar.x = fmaf(v.x, h.x, ar.x); ai.x = fmaf(v.y, h.x, ai.x);
+          ar.y = fmaf(v.x, h.y, ar.y); ai.y = fmaf(v.y, h.y, ai.y);
+          ar.z = fmaf(v.x, h.z, ar.z); ai.z = fmaf(v.y, h.z, ai.z);
+          ar.w = fmaf(v.x, h.w, ar.w); ai.w = fmaf(v.y, h.w, ai.w);
         }
-        U[idx] = make_float2(ax, ay);
+        float2* u = U + y * GP + 4 * mq;
+        u[0] = make_float2(ar.x, ai.x);
+        u[1] = make_float2(ar.y, ai.y);
+        u[2] = make_float2(ar.z, ai.z);
+        u[3] = make_float2(ar.w, ai.w);
       }
       __syncthreads();
       const float d = g.dxdy[q];
       float2* out = p.coefs + (size_t)item * g.M;
       for (int i = tid; i < g.M; i += blockDim.x) {
         const int m = p.t.mode_m[i], n = p.t.mode_n[i];
-        const float* h = hy + n * WH;
         float ax = 0.f, ay = 0.f;
 #pragma unroll 6
         for (int y = 0; y < WH; ++y) {
-          const float2 v = U[y * G + m];
-          const float hv = __ldg(&h[y]);
+          const float2 v = U[y * GP + m];
+          const float hv = hyT[y * GP + n];
           ax = fmaf(v.x, hv, ax);
           ay = fmaf(v.y, hv, ay);
         }
@@ -297,7 +313,8 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
 bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
                     unsigned flags, const void* windows) {
   return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
-         !(fmt == 1 && transpose) && !fill && rcal == nullptr && (flags & 1u) == 0 && windows == nullptr;
+         g.G <= FastLayout<42, 42>::GP && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
+         (flags & 1u) == 0 && windows == nullptr;
 }
 
 cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
