@@ -151,12 +151,19 @@ int hpg_fourier_full(const hpg_plan* plan, const void* frames, int32_t frame_for
 /* Seven analysis parameters (analysis.py:39-94) per (frame, pol) of complex
  * data [count][P][h][w] with fp64 device axes x[w], y[h], plus the aggregate
  * slot (index `count`) from the summed intensity.  params [7][P][slots]
- * (slots >= count+1); total_intensity [h][w] or NULL.  The workspace needs
+ * (slots >= count+1); total_intensity [h][w] or NULL; pol_intensity fp64
+ * [P][h][w] batch sums per pol or NULL (align.py:53-55).  The workspace needs
  * hpg_plane_summary_workspace() bytes.  Deterministic for a given input. */
 size_t hpg_plane_summary_workspace(int64_t count, int32_t P, int32_t h, int32_t w);
 int hpg_plane_summary(const void* data, int64_t count, int32_t P, int32_t h, int32_t w,
                       const double* x_axis, const double* y_axis, float* params, int32_t slots,
-                      float* total_intensity, void* workspace, size_t workspace_bytes, void* stream);
+                      float* total_intensity, double* pol_intensity, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* Batch-summed intensity per pol of dequantised int16 fields, fp64
+ * [P][h][w] = sum_b |(fr + i fi) / scale|^2 (holopipe/align.py:166-169). */
+int hpg_field_intensity(const int16_t* field_r, const int16_t* field_i, const float* field_scale,
+                        int32_t batch_count, int32_t P, int32_t h, int32_t w, double* out, void* stream);
 
 /* Coefficients of already-quantised fields (engine.py:353-370): fields int16
  * [B][P][gh][gw] + scale [B][P] -> coefs complex64 [B][P*M]. */

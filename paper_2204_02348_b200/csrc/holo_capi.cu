@@ -25,8 +25,10 @@ bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, 
                     unsigned flags, const void* windows);
 cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
 cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
-                                 const double* ya, float* params, int slots, float* total, char* work,
-                                 int grid, cudaStream_t s);
+                                 const double* ya, float* params, int slots, float* total, double* pol_total,
+                                 char* work, int grid, cudaStream_t s);
+cudaError_t launch_field_intensity(const int16_t* fr, const int16_t* fi, const float* scale, int B, int P, int hw,
+                                   double* out, cudaStream_t s);
 }  // namespace holo
 
 using namespace holo;
@@ -603,16 +605,25 @@ size_t hpg_plane_summary_workspace(int64_t count, int32_t P, int32_t h, int32_t 
 }
 
 int hpg_plane_summary(const void* data, int64_t count, int32_t P, int32_t h, int32_t w, const double* xa,
-                      const double* ya, float* params, int32_t slots, float* total, void* work,
+                      const double* ya, float* params, int32_t slots, float* total, double* pol_total, void* work,
                       size_t work_bytes, void* stream) {
   if (!data || !xa || !ya || !params || !work) return fail(HPG_NULLPOINTER, "null argument");
   if (count < 1 || P < 1 || h < 1 || w < 1) return fail(HPG_INVALIDDIMENSION, "empty plane");
   if (slots < count + 1) return fail(HPG_INVALIDDIMENSION, "slots");
   if (work_bytes < hpg_plane_summary_workspace(count, P, h, w)) return fail(HPG_INVALIDARGUMENT, "workspace too small");
   cudaError_t e = launch_plane_summary(static_cast<const float2*>(data), count, P, h, w, xa, ya, params, slots,
-                                       total, static_cast<char*>(work), plane_grid(count, P),
+                                       total, pol_total, static_cast<char*>(work), plane_grid(count, P),
                                        static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "plane summary launch");
+  return HPG_SUCCESS;
+}
+
+int hpg_field_intensity(const int16_t* fr, const int16_t* fi, const float* scale, int32_t B, int32_t P, int32_t h,
+                        int32_t w, double* out, void* stream) {
+  if (!fr || !fi || !scale || !out) return fail(HPG_NULLPOINTER, "null argument");
+  if (B < 1 || P < 1 || h < 1 || w < 1) return fail(HPG_INVALIDDIMENSION, "dimensions");
+  cudaError_t e = launch_field_intensity(fr, fi, scale, B, P, h * w, out, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "field intensity launch");
   return HPG_SUCCESS;
 }
 

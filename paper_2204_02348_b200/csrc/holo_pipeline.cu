@@ -388,6 +388,7 @@ struct PlaneArgs {
   char* agg;           // per-CTA [P][h][w] doubles
   int64_t agg_per_cta; // bytes
   float* total;        // [h][w] or NULL
+  double* pol_total;   // [P][h][w] or NULL
   int agg_slot;        // slot index of the aggregate column
   int nblocks;         // CTAs that produced partials (finalize)
 };
@@ -443,7 +444,6 @@ __global__ void __launch_bounds__(kThreads) plane_stats_kernel(const PlaneArgs a
 // (analysis.py:88-91) and the total over pols (analysis.py:92).
 __global__ void __launch_bounds__(kThreads) plane_finalize_kernel(const PlaneArgs a) {
   __shared__ double red[8][32];
-  __shared__ float redf[32];
   __shared__ int redi[32];
   const int q = blockIdx.x;
   const int hw = a.h * a.w;
@@ -468,6 +468,7 @@ __global__ void __launch_bounds__(kThreads) plane_finalize_kernel(const PlaneArg
     st[4] += I * cs;
     st[5] += I * sn;
     if (I > amax) { amax = I; aidx = i; }
+    if (a.pol_total) a.pol_total[(size_t)q * hw + i] = I;
     if (a.total && q == 0) {
       double tI = I;
       for (int qq = 1; qq < a.P; ++qq)
@@ -562,6 +563,29 @@ __global__ void __launch_bounds__(kThreads) fourier_full_kernel(const __grid_con
   }
 }
 
+// Sum over the batch of |dequantised int16 field|^2 per pol, fp64, fixed order.
+__global__ void field_intensity_kernel(const int16_t* fr, const int16_t* fi, const float* scale, int B, int P,
+                                       int hw, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)P * hw) return;
+  const int q = (int)(i / hw), pix = (int)(i - (int64_t)q * hw);
+  double acc = 0.0;
+  for (int b = 0; b < B; ++b) {
+    const size_t o = ((size_t)b * P + q) * hw + pix;
+    const double s = (double)scale[(size_t)b * P + q];
+    const double re = (double)fr[o] / s, im = (double)fi[o] / s;
+    acc += re * re + im * im;
+  }
+  out[i] = acc;
+}
+
+cudaError_t launch_field_intensity(const int16_t* fr, const int16_t* fi, const float* scale, int B, int P, int hw,
+                                   double* out, cudaStream_t s) {
+  const int64_t n = (int64_t)P * hw;
+  field_intensity_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(fr, fi, scale, B, P, hw, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_fused(const RunParams& p, cudaStream_t s) {
   fused_kernel<<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p);
@@ -578,9 +602,10 @@ cudaError_t launch_finalize(const RunParams& p, float* total, cudaStream_t s) {
   return cudaGetLastError();
 }
 cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
-                                 const double* ya, float* params, int slots, float* total, char* work,
-                                 int grid, cudaStream_t s) {
+                                 const double* ya, float* params, int slots, float* total, double* pol_total,
+                                 char* work, int grid, cudaStream_t s) {
   PlaneArgs a{};
+  a.pol_total = pol_total;
   a.data = data; a.count = count; a.P = P; a.h = h; a.w = w; a.xa = xa; a.ya = ya;
   a.params = params; a.slots = slots; a.agg = work;
   a.agg_per_cta = ((int64_t)P * h * w * 8 + 255) / 256 * 256;

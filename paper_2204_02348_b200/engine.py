@@ -556,7 +556,7 @@ class Engine:
         w = self._window.cpu().numpy()
         return w, self._plan["batch"], self._st0["P"], w.shape[-1], w.shape[-2]
 
-    def _plane_summary(self, data, xa, ya):
+    def _plane_summary(self, data, xa, ya, pol_sums=False):
         torch = _torch()
         count, P, h, w = data.shape
         slots = count + 1
@@ -567,11 +567,43 @@ class Engine:
         L = native.lib()
         wsb = L.hpg_plane_summary_workspace(count, P, h, w)
         ws = self._buf("ws_sum", (wsb,), torch.uint8)
+        pol_total = torch.empty((P, h, w), dtype=torch.float64, device=self.device) if pol_sums else None
         with torch.cuda.device(self.device):
             native.check(L.hpg_plane_summary(native.ptr(data), count, P, h, w, native.ptr(xa_d),
                                              native.ptr(ya_d), native.ptr(params), slots, native.ptr(inten),
-                                             native.ptr(ws), wsb, native.stream_handle()), "hpg_plane_summary")
+                                             native.ptr(pol_total), native.ptr(ws), wsb, native.stream_handle()),
+                         "hpg_plane_summary")
+        if pol_sums:
+            return params, inten, pol_total
         return params, inten
+
+    # ------------------------------------------------ AutoAlign reductions
+    def fourier_intensity_per_pol(self):
+        """sum_b |F|^2 over the full R2C plane per pol, fp64 (holopipe/align.py:53-55)."""
+        fx, fy = self._fourier_axes_f64
+        _, _, pt = self._plane_summary(self._fourier_plane_device(), fx, fy, pol_sums=True)
+        return pt.cpu().numpy()
+
+    def window_intensity_per_pol(self):
+        """sum_b |window|^2 per pol, fp64 (holopipe/align.py:177)."""
+        self.get_fourier_plane_window()
+        w = self._window
+        wh, ww = w.shape[-2:]
+        xa = np.arange(ww, dtype=np.float64)
+        ya = np.arange(wh, dtype=np.float64)
+        _, _, pt = self._plane_summary(w, xa, ya, pol_sums=True)
+        return pt.cpu().numpy()
+
+    def field_intensity_per_pol(self):
+        """sum_b |dequantised int16 field|^2 per pol, fp64 (holopipe/align.py:163-169)."""
+        torch = _torch()
+        B, P, h, w = self._field_r.shape
+        out = torch.empty((P, h, w), dtype=torch.float64, device=self.device)
+        with torch.cuda.device(self.device):
+            native.check(native.lib().hpg_field_intensity(
+                native.ptr(self._field_r), native.ptr(self._field_i), native.ptr(self._field_scale),
+                B, P, h, w, native.ptr(out), native.stream_handle()), "hpg_field_intensity")
+        return out.cpu().numpy()
 
     def batch_summary(self, plane_idx):
         if plane_idx not in (C.PLANE_FOURIER, C.PLANE_FIELD):

@@ -28,7 +28,7 @@ EXPORTS = [
     "hpg_version", "hpg_plan_create", "hpg_plan_destroy", "hpg_plan_get_info", "hpg_plan_get_axes",
     "hpg_plan_get_basis", "hpg_workspace_size", "hpg_run", "hpg_finalize_summary",
     "hpg_fourier_full", "hpg_extract_coefs", "hpg_metric_partials", "hpg_plane_summary",
-    "hpg_plane_summary_workspace", "hpg_last_error",
+    "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_last_error",
 ]
 
 
@@ -115,7 +115,9 @@ def lib():
                                     c_void_p]
     L.hpg_metric_partials.argtypes = [P(MetricArgs), c_void_p]
     L.hpg_plane_summary.argtypes = [c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
-                                    c_void_p, c_int32, c_void_p, c_void_p, c_size_t, c_void_p]
+                                    c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
+    L.hpg_field_intensity.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
+                                      c_void_p, c_void_p]
     L.hpg_plane_summary_workspace.argtypes = [c_int64, c_int32, c_int32, c_int32]
     for name in EXPORTS:
         getattr(L, name).restype = c_int32
