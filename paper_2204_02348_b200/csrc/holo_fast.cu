@@ -54,6 +54,36 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
   }
 }
 
+// Last column stage of the inverse transform with the epilogue fused in:
+// removal phase (separable ey[y] * ex[x], incl. ifftshift sign and 1/(nx ny)),
+// optional batch calibration, and the running max |Re|,|Im| for the int16 scale.
+template <int P, int N, int L, int COUNT>
+HOLO_DEV float ct_stage_final_cols(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw,
+                                   const float2* ey, const float2* ex, bool use_bc, float2 bc) {
+  constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
+  static_assert(mp == 1, "final stage");
+  float lmax = 0.f;
+  for (int task = threadIdx.x; task < total; task += blockDim.x) {
+    const int q = task % COUNT, k = task / COUNT;   // column x = q
+    float2 v[P];
+#pragma unroll
+    for (int j = 0; j < P; ++j) v[j] = src[q + (k * m_in + j) * COUNT];
+#pragma unroll
+    for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<true>(tw[(j * k) % N]));
+    dft_fixed<P, true>(v);
+    const float2 exq = ex[q];
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const int y = k + L * t;
+      float2 o = cmul(cmul(v[t], ey[y]), exq);
+      if (use_bc) o = cmul(o, bc);
+      lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
+      dst[q + y * COUNT] = o;
+    }
+  }
+  return lmax;
+}
+
 template <int WH, int WW>
 struct FastLayout {
   static constexpr int ZS = 2 * WW + 2;            // padded zs row (float2)
@@ -212,20 +242,13 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     __syncthreads();
     ct_stage<6, WH, 1, WW, 1, WW, true>(Wb, T, twh);
     __syncthreads();
-    ct_stage<7, WH, 6, WW, 1, WW, true>(T, Wb, twh);
-    __syncthreads();
-
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
-    float lmax = 0.f;
-    for (int i = tid; i < WH * WW; i += blockDim.x) {
-      const int y = i / WW, x = i - y * WW;
-      float2 v = cmul(cmul(Wb[i], s_ey[y]), s_ex[x]);
-      if (p.bcal) v = cmul(v, bc);
-      Wb[i] = v;
-      lmax = fmaxf(lmax, fmaxf(fabsf(v.x), fabsf(v.y)));
-      if (p.raw) p.raw[(size_t)item * WH * WW + i] = v;
+    float lmax = ct_stage_final_cols<7, WH, 6, WW>(T, Wb, twh, s_ey, s_ex, p.bcal != nullptr, bc);
+    if (p.raw) {
+      __syncthreads();
+      for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = Wb[i];
     }
     {
       float v = lmax;
@@ -242,33 +265,33 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     int16_t* fro = p.fr + (size_t)item * WH * WW;
     int16_t* fio = p.fi + (size_t)item * WH * WW;
     for (int i = tid; i < WH * WW / 2; i += blockDim.x) {
-      const float2 v0 = Wb[2 * i], v1 = Wb[2 * i + 1];
-      const int r0 = __float2int_rn(__fmul_rn(v0.x, scale)), i0 = __float2int_rn(__fmul_rn(v0.y, scale));
-      const int r1 = __float2int_rn(__fmul_rn(v1.x, scale)), i1 = __float2int_rn(__fmul_rn(v1.y, scale));
+      const float4 v = reinterpret_cast<const float4*>(Wb)[i];
+      const int r0 = __float2int_rn(__fmul_rn(v.x, scale)), i0 = __float2int_rn(__fmul_rn(v.y, scale));
+      const int r1 = __float2int_rn(__fmul_rn(v.z, scale)), i1 = __float2int_rn(__fmul_rn(v.w, scale));
       reinterpret_cast<int*>(fro)[i] = (r0 & 0xffff) | (r1 << 16);
       reinterpret_cast<int*>(fio)[i] = (i0 & 0xffff) | (i1 << 16);
-      // dequantised copy for the overlap: exactly (float)q / scale (holopipe/engine.py:367-369)
-      Wb[2 * i] = make_float2(__fdiv_rn((float)r0, scale), __fdiv_rn((float)i0, scale));
-      Wb[2 * i + 1] = make_float2(__fdiv_rn((float)r1, scale), __fdiv_rn((float)i1, scale));
+      // integer-valued copy for the overlap; the 1/scale of the dequantisation
+      // (holopipe/engine.py:367-369) is applied once to each coefficient
+      reinterpret_cast<float4*>(Wb)[i] = make_float4((float)r0, (float)i0, (float)r1, (float)i1);
     }
     if (tid == 0) p.scale[item] = scale;
 
     // ---------------------------------------------------------- HG overlap
     if (p.coefs && g.G > 0) {
       const int G = g.G;
-      constexpr int GP = LY::GP;
+      const int GP = (G + 3) & ~3;
       float* hxT = reinterpret_cast<float*>(zs);          // [WW][GP]  (zs is free now)
       float* hyT = hxT + WW * GP;                          // [WH][GP]
       float2* U = xbuf;                                    // [WH][GP]
       const float* hx = p.t.hx + (size_t)q * G * WW;
       const float* hy = p.t.hy + (size_t)q * G * WH;
-      for (int i = tid; i < WW * GP; i += blockDim.x) {
-        const int x = i / GP, m = i - x * GP;
-        hxT[i] = m < G ? __ldg(&hx[m * WW + x]) : 0.f;
+      for (int i = tid; i < GP * WW; i += blockDim.x) {   // i = m*WW + x: coalesced reads
+        const int m = i / WW, x = i - m * WW;
+        hxT[x * GP + m] = m < G ? __ldg(&hx[i]) : 0.f;
       }
-      for (int i = tid; i < WH * GP; i += blockDim.x) {
-        const int y = i / GP, n = i - y * GP;
-        hyT[i] = n < G ? __ldg(&hy[n * WH + y]) : 0.f;
+      for (int i = tid; i < GP * WH; i += blockDim.x) {
+        const int n = i / WH, y = i - n * WH;
+        hyT[y * GP + n] = n < G ? __ldg(&hy[i]) : 0.f;
       }
       __syncthreads();
       const int GQ = (G + 3) >> 2;
@@ -292,7 +315,7 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
         u[3] = make_float2(ar.w, ai.w);
       }
       __syncthreads();
-      const float d = g.dxdy[q];
+      const float d = __fdiv_rn(g.dxdy[q], scale);
       float2* out = p.coefs + (size_t)item * g.M;
       for (int i = tid; i < g.M; i += blockDim.x) {
         const int m = p.t.mode_m[i], n = p.t.mode_n[i];
