@@ -1,24 +1,30 @@
-// Register-resident fused kernel for the hot geometry class: 128 x 128 FFT
-// window, a WH x WW (42 x 42 for BASELINE) Fourier window, IFFT resolution
-// mode 1, no averaging, no fill-factor correction.  Same algorithm and
-// numerical conventions as the generic kernel (holo_pipeline.cu), with every
-// size a compile-time constant:
+// Fused kernel for the hot geometry class: 128 x 128 FFT window, a WH x WW
+// (42 x 42 for BASELINE) Fourier window, IFFT resolution mode 1, no
+// averaging, no fill-factor correction.  Same algorithm and numerical
+// conventions as the generic kernel (holo_pipeline.cu) with every size a
+// compile-time constant.  One (frame, pol) item per 256-thread CTA at a time,
+// three CTAs per SM (64 KB shared memory, <= 85 registers):
 //
 //   row pass    8 threads per (row y, row y+64) pair, 16 points per thread:
-//               DFT-16 in registers -> twiddle W128^(t k1) -> 8x16 transpose
-//               through a padded shared tile -> DFT-8 -> keep only the bins
-//               the window needs: zs[pair][c] = Z[kx_c], zs[pair][WW+c] = Z[-kx_c]
-//               (the two halves of the Hermitian split, holopipe/pipeline.py:89-98)
+//               DFT-16 in registers -> twiddle W128^(t k1) -> two 8x8
+//               transposes through a padded shared tile -> DFT-8 -> keep only
+//               the bins the window needs, Z[kx_c] and Z[-kx_c] (the two halves
+//               of the Hermitian split, holopipe/pipeline.py:89-98), in zs
 //   column pass 8 threads per kept column: Hermitian split on load, same
 //               128-point FFT, keep the WH needed rows, circular mask (row
-//               range per column) * separable recentring phase (pipeline.py:72-127)
+//               range per column) * separable recentring phase (pipeline.py:72-127).
+//               The window W is written into the zs slots the first column
+//               round has already consumed (zs row layout below).
 //   IFFT        compile-time Stockham (42 = 6 x 7) along rows then columns
-//   epilogue    removal phase, block peak, int16 packing (pipeline.py:163-199),
-//               separable HG overlap with the basis staged in shared memory
+//               (pipeline.py:130-149); removal phase (pipeline.py:163-185) and
+//               the peak search fused into the last stage
+//   epilogue    int16 packing (pipeline.py:188-199) and the separable HG
+//               overlap (hgbasis.py:101-116) on the integer-valued field with
+//               the 1/scale of the dequantisation folded into the coefficients
 //
 // Frames are read straight from HBM into registers (each warp load touches
-// four full 32-byte sectors), so the only HBM traffic is the window read and
-// the int16 / scale / coefficient writes.
+// four full 32-byte sectors): HBM traffic is the window read and the int16 /
+// scale / coefficient writes.
 #include <algorithm>
 
 #include "holo_internal.h"
@@ -31,9 +37,20 @@ struct FastTables {
   const int16_t* crange;   // [WW][2] first/last row inside the circular mask, per column
 };
 
+// zs row (one row pair) layout, 2*WW+2 float2:
+//   [0,32)        Z[-kx_c], c < 32        (read by column round 0)
+//   [32,64)       Z[+kx_c], c < 32        (read by column round 0)
+//   [64,64+R2)    Z[+kx_c], c >= 32       (read by column round 1, R2 = WW-32)
+//   [64+R2,64+2R2) Z[-kx_c], c >= 32
+// After round 0 the first 64 slots of every row are free and hold W.
+template <int WW> HOLO_DEV int zs_pos(int c) { return c < 32 ? 32 + c : 64 + (c - 32); }
+template <int WW> HOLO_DEV int zs_neg(int c) { return c < 32 ? c : 64 + (WW - 32) + (c - 32); }
+template <int ZS> HOLO_DEV int w_addr(int i) { return (i >> 6) * ZS + (i & 63); }
+
 // Compile-time Stockham stage over COUNT sequences of length N (index algebra
-// in holo_fft.cuh); element e of sequence q at q*SS + e*ES.
-template <int P, int N, int L, int COUNT, int SS, int ES, bool INV>
+// in holo_fft.cuh); element e of sequence q at q*SS + e*ES.  MAPPED: the source
+// is W inside zs (w_addr).
+template <int P, int N, int L, int COUNT, int SS, int ES, bool INV, int MAPPED_ZS = 0>
 HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw) {
   constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
   for (int task = threadIdx.x; task < total; task += blockDim.x) {
@@ -43,7 +60,10 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
     const int k = r / mp, qp = r - k * mp;
     float2 v[P];
 #pragma unroll
-    for (int j = 0; j < P; ++j) v[j] = src[q * SS + (k * m_in + qp + mp * j) * ES];
+    for (int j = 0; j < P; ++j) {
+      const int i = q * SS + (k * m_in + qp + mp * j) * ES;
+      v[j] = src[MAPPED_ZS ? w_addr<MAPPED_ZS>(i) : i];
+    }
     if (L > 1) {
 #pragma unroll
       for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<INV>(tw[(j * k * mp) % N]));
@@ -84,32 +104,55 @@ HOLO_DEV float ct_stage_final_cols(const float2* __restrict__ src, float2* __res
   return lmax;
 }
 
+// First half of a 128-point FFT with 16 points per thread (8 threads per
+// transform): on entry z holds x[t + 8 j]; on exit z[k1] = W128^(t k1) DFT16(z)[k1].
+HOLO_DEV void fft128_stage1(float2* z, int t, const float2* tw128) {
+  dft16<false>(z);
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], tw128[(t * k1) & 127]);
+}
+// Second half for k1 = t + 8h: 8x8 transpose through the group's tile, DFT-8;
+// v[k2] = X[t + 8h + 16 k2].
+HOLO_DEV void fft128_stage2(const float2* z, int h, float2* xg, int t, float2* v) {
+#pragma unroll
+  for (int kk = 0; kk < 8; ++kk) xg[kk * 9 + t] = z[8 * h + kk];
+  __syncwarp();
+#pragma unroll
+  for (int tp = 0; tp < 8; ++tp) v[tp] = xg[t * 9 + tp];
+  __syncwarp();
+  dft8<false>(v);
+}
+
 template <int WH, int WW>
 struct FastLayout {
-  static constexpr int ZS = 2 * WW + 2;            // padded zs row (float2)
-  static constexpr int XG = 152;                   // exchange tile per 8-thread group (float2)
-  static constexpr int GP = 48;                    // max basis orders staged (multiple of 4)
-  static constexpr size_t xbuf = 0;                                        // [32][XG]
-  static constexpr size_t zs = xbuf + 32 * XG * sizeof(float2);            // [64][ZS]
-  static constexpr size_t W = zs + 64 * ZS * sizeof(float2);               // [WH*WW]
-  static constexpr size_t tw128 = W + WH * WW * sizeof(float2);            // [128]
+  static constexpr int ZS = 2 * WW + 2;            // zs row pitch (float2)
+  static constexpr int XG = 72;                    // 8x8 exchange tile per 8-thread group (float2)
+  static constexpr int GMAX = 48;                  // max basis orders on this path
+  static constexpr size_t zs = 0;                                          // [64][ZS]
+  static constexpr size_t xbuf = zs + 64 * ZS * sizeof(float2);            // [32][XG]
+  static constexpr size_t tw128 = xbuf + 32 * XG * sizeof(float2);         // [128]
   static constexpr size_t twh = tw128 + 128 * sizeof(float2);              // [WH]
   static constexpr size_t tww = twh + WH * sizeof(float2);                 // [WW]
   static constexpr size_t ph = tww + WW * sizeof(float2);                  // px[WW] py[WH] ex[WW] ey[WH]
   static constexpr size_t bytes = ph + 2 * (WH + WW) * sizeof(float2) + 64;
-  static_assert(WH * WW <= 32 * XG, "IFFT ping-pong must fit the exchange tile");
-  static_assert((WH + WW) * GP * sizeof(float) <= 64 * ZS * sizeof(float2), "basis staging must fit zs");
+  // after the IFFT, zs holds F (linear, [WH][WW]) then the staged basis
+  static constexpr size_t basis_off = ((WH * WW * sizeof(float2)) + 255) & ~size_t(255);
+  static_assert(WW > 32 && WW <= 64 && WH <= 64, "zs row layout assumes two column rounds");
+  static_assert((WH * WW + 63) / 64 <= 64, "W must fit the freed zs slots");
+  static_assert(WH * WW * sizeof(float2) <= 32 * XG * sizeof(float2), "IFFT ping-pong must fit xbuf");
+  static_assert(WH * GMAX * sizeof(float2) <= 32 * XG * sizeof(float2), "overlap U must fit xbuf");
+  static_assert(basis_off + (WH + WW) * GMAX * sizeof(float) <= 64 * ZS * sizeof(float2), "basis must fit zs");
 };
 
 template <int WH, int WW>
-__global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__ RunParams p,
+__global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__ RunParams p,
                                                         const __grid_constant__ FastTables ft) {
   using LY = FastLayout<WH, WW>;
+  constexpr int ZS = LY::ZS;
   extern __shared__ __align__(16) char smem[];
-  __shared__ float redf[32];
-  float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
+  __shared__ float redf[8];
   float2* zs = reinterpret_cast<float2*>(smem + LY::zs);
-  float2* Wb = reinterpret_cast<float2*>(smem + LY::W);
+  float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
   float2* tw128 = reinterpret_cast<float2*>(smem + LY::tw128);
   float2* twh = reinterpret_cast<float2*>(smem + LY::twh);
   float2* tww = reinterpret_cast<float2*>(smem + LY::tww);
@@ -130,8 +173,7 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     const int b = item / g.P, q = item - b * g.P;
     const int w = p.wl ? p.wl[b] : 0;
     const int pl = q * g.L + w;
-    const int k0x = g.k0[q][w][0], k0y = g.k0[q][w][1];
-    const int kxs = (k0x - WW / 2) & 127, kys = (k0y - WH / 2) & 127;
+    const int kxs = (g.k0[q][w][0] - WW / 2) & 127, kys = (g.k0[q][w][1] - WH / 2) & 127;
     __syncthreads();  // previous item done with every buffer
     for (int i = tid; i < WW; i += blockDim.x) {
       s_px[i] = ft.px[pl * WW + i];
@@ -143,146 +185,125 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
     }
 
     // ------------------------------------------------------------ row pass
-    const int64_t f = (int64_t)b;  // A == 1 on this path
     const int W = g.W, H = g.H;
-    const int col0 = g.col0[q], row0 = g.row0[q];
 #pragma unroll 1
     for (int rnd = 0; rnd < 2; ++rnd) {
       const int pr = rnd * 32 + grp;
       float2 z[16];
       if (p.fmt == 0) {
-        const float* fa = reinterpret_cast<const float*>(p.frames) + f * (int64_t)W * H +
-                          (int64_t)(row0 + pr) * W + col0 + t;
-        const float* fb = fa + (int64_t)64 * W;
+        const float* fa = reinterpret_cast<const float*>(p.frames) + (int64_t)b * W * H +
+                          (int64_t)(g.row0[q] + pr) * W + g.col0[q] + t;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = make_float2(__ldg(fa + 8 * j), __ldg(fb + 8 * j));
+        for (int j = 0; j < 16; ++j) z[j] = make_float2(__ldg(fa + 8 * j), __ldg(fa + 64 * W + 8 * j));
       } else {
-        const unsigned short* fa = reinterpret_cast<const unsigned short*>(p.frames) + f * (int64_t)W * H +
-                                   (int64_t)(row0 + pr) * W + col0 + t;
-        const unsigned short* fb = fa + (int64_t)64 * W;
+        const unsigned short* fa = reinterpret_cast<const unsigned short*>(p.frames) + (int64_t)b * W * H +
+                                   (int64_t)(g.row0[q] + pr) * W + g.col0[q] + t;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) z[j] = make_float2((float)__ldg(fa + 8 * j), (float)__ldg(fb + 8 * j));
+        for (int j = 0; j < 16; ++j)
+          z[j] = make_float2((float)__ldg(fa + 8 * j), (float)__ldg(fa + 64 * W + 8 * j));
       }
-      dft16<false>(z);
-#pragma unroll
-      for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], tw128[(t * k1) & 127]);
-#pragma unroll
-      for (int k1 = 0; k1 < 16; ++k1) xg[k1 * 9 + t] = z[k1];
-      __syncwarp();
-      float2* zrow = zs + pr * LY::ZS;
+      fft128_stage1(z, t, tw128);
+      float2* zrow = zs + pr * ZS;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int k1 = t + 8 * h;
         float2 v[8];
-#pragma unroll
-        for (int tp = 0; tp < 8; ++tp) v[tp] = xg[k1 * 9 + tp];
-        dft8<false>(v);
+        fft128_stage2(z, h, xg, t, v);
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          const int k = k1 + 16 * k2;
-          const int cp = (k - kxs) & 127, cm = (128 - k - kxs) & 127;
-          if (cp < WW) zrow[cp] = v[k2];
-          if (cm < WW) zrow[WW + cm] = v[k2];
+          const int kk = t + 8 * h + 16 * k2;
+          const int cp = (kk - kxs) & 127, cm = (128 - kk - kxs) & 127;
+          if (cp < WW) zrow[zs_pos<WW>(cp)] = v[k2];
+          if (cm < WW) zrow[zs_neg<WW>(cm)] = v[k2];
         }
       }
-      __syncwarp();
     }
     __syncthreads();
 
     // --------------------------------------------------------- column pass
 #pragma unroll 1
-    for (int rnd = 0; rnd < (WW + 31) / 32; ++rnd) {
+    for (int rnd = 0; rnd < 2; ++rnd) {
       const int c = rnd * 32 + grp;
       const bool active = c < WW;
       float2 z[16];
       if (active) {
+        const int sp = zs_pos<WW>(c), sn = zs_neg<WW>(c);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-          const float2 zk = zs[(t + 8 * jj) * LY::ZS + c], zm = zs[(t + 8 * jj) * LY::ZS + WW + c];
+          const float2 zk = zs[(t + 8 * jj) * ZS + sp], zm = zs[(t + 8 * jj) * ZS + sn];
           z[jj] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
           z[jj + 8] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
         }
-        dft16<false>(z);
+        fft128_stage1(z, t, tw128);
+      } else {
 #pragma unroll
-        for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], tw128[(t * k1) & 127]);
-#pragma unroll
-        for (int k1 = 0; k1 < 16; ++k1) xg[k1 * 9 + t] = z[k1];
+        for (int jj = 0; jj < 16; ++jj) z[jj] = make_float2(0.f, 0.f);
       }
-      __syncwarp();
+      float2 o0[8], o1[8];
+      fft128_stage2(z, 0, xg, t, o0);   // all lanes take part in the warp exchange
+      fft128_stage2(z, 1, xg, t, o1);
+      if (rnd == 0) __syncthreads();    // round 0 consumed zs slots [0,64) of every row
       if (active) {
         const float2 pxc = s_px[c];
         const int rlo = ft.crange[2 * c], rhi = ft.crange[2 * c + 1];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k1 = t + 8 * h;
-          float2 v[8];
+        for (int k2 = 0; k2 < 8; ++k2) {
 #pragma unroll
-          for (int tp = 0; tp < 8; ++tp) v[tp] = xg[k1 * 9 + tp];
-          dft8<false>(v);
-#pragma unroll
-          for (int k2 = 0; k2 < 8; ++k2) {
-            const int r = (k1 + 16 * k2 - kys) & 127;
+          for (int h = 0; h < 2; ++h) {
+            const int r = (t + 8 * h + 16 * k2 - kys) & 127;
             if (r < WH) {
               float2 val = make_float2(0.f, 0.f);
-              if (r >= rlo && r <= rhi) val = cmul(v[k2], cmul(s_py[r], pxc));
-              Wb[r * WW + c] = val;
+              if (r >= rlo && r <= rhi) val = cmul(h ? o1[k2] : o0[k2], cmul(s_py[r], pxc));
+              zs[w_addr<ZS>(r * WW + c)] = val;
             }
           }
         }
       }
-      __syncwarp();
     }
     __syncthreads();
 
     // ------------------------------------------------ IFFT (rows, then columns)
     float2* T = xbuf;
-    ct_stage<6, WW, 1, WH, WW, 1, true>(Wb, T, tww);
+    float2* F = zs;   // linear [WH][WW] once the mapped W has been consumed
+    ct_stage<6, WW, 1, WH, WW, 1, true, ZS>(zs, T, tww);
     __syncthreads();
-    ct_stage<7, WW, 6, WH, WW, 1, true>(T, Wb, tww);
+    ct_stage<7, WW, 6, WH, WW, 1, true>(T, F, tww);
     __syncthreads();
-    ct_stage<6, WH, 1, WW, 1, WW, true>(Wb, T, twh);
+    ct_stage<6, WH, 1, WW, 1, WW, true>(F, T, twh);
     __syncthreads();
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
-    float lmax = ct_stage_final_cols<7, WH, 6, WW>(T, Wb, twh, s_ey, s_ex, p.bcal != nullptr, bc);
-    if (p.raw) {
-      __syncthreads();
-      for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = Wb[i];
-    }
-    {
-      float v = lmax;
+    float lmax = ct_stage_final_cols<7, WH, 6, WW>(T, F, twh, s_ey, s_ex, p.bcal != nullptr, bc);
 #pragma unroll
-      for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if ((tid & 31) == 0) redf[tid >> 5] = v;
-      __syncthreads();
-      v = redf[0];
+    for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if ((tid & 31) == 0) redf[tid >> 5] = lmax;
+    __syncthreads();
+    lmax = redf[0];
 #pragma unroll
-      for (int j = 1; j < 8; ++j) v = fmaxf(v, redf[j]);
-      lmax = v;
-    }
+    for (int j = 1; j < 8; ++j) lmax = fmaxf(lmax, redf[j]);
+    if (p.raw)
+      for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = F[i];
     const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
     int16_t* fro = p.fr + (size_t)item * WH * WW;
     int16_t* fio = p.fi + (size_t)item * WH * WW;
     for (int i = tid; i < WH * WW / 2; i += blockDim.x) {
-      const float4 v = reinterpret_cast<const float4*>(Wb)[i];
+      const float4 v = reinterpret_cast<const float4*>(F)[i];
       const int r0 = __float2int_rn(__fmul_rn(v.x, scale)), i0 = __float2int_rn(__fmul_rn(v.y, scale));
       const int r1 = __float2int_rn(__fmul_rn(v.z, scale)), i1 = __float2int_rn(__fmul_rn(v.w, scale));
       reinterpret_cast<int*>(fro)[i] = (r0 & 0xffff) | (r1 << 16);
       reinterpret_cast<int*>(fio)[i] = (i0 & 0xffff) | (i1 << 16);
       // integer-valued copy for the overlap; the 1/scale of the dequantisation
       // (holopipe/engine.py:367-369) is applied once to each coefficient
-      reinterpret_cast<float4*>(Wb)[i] = make_float4((float)r0, (float)i0, (float)r1, (float)i1);
+      reinterpret_cast<float4*>(F)[i] = make_float4((float)r0, (float)i0, (float)r1, (float)i1);
     }
     if (tid == 0) p.scale[item] = scale;
 
     // ---------------------------------------------------------- HG overlap
     if (p.coefs && g.G > 0) {
-      const int G = g.G;
-      const int GP = (G + 3) & ~3;
-      float* hxT = reinterpret_cast<float*>(zs);          // [WW][GP]  (zs is free now)
-      float* hyT = hxT + WW * GP;                          // [WH][GP]
-      float2* U = xbuf;                                    // [WH][GP]
+      const int G = g.G, GP = (G + 3) & ~3;
+      float* hxT = reinterpret_cast<float*>(smem + LY::zs + LY::basis_off);   // [WW][GP]
+      float* hyT = hxT + WW * GP;                                             // [WH][GP]
+      float2* U = xbuf;                                                       // [WH][GP]
       const float* hx = p.t.hx + (size_t)q * G * WW;
       const float* hy = p.t.hy + (size_t)q * G * WH;
       for (int i = tid; i < GP * WW; i += blockDim.x) {   // i = m*WW + x: coalesced reads
@@ -294,10 +315,10 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
         hyT[y * GP + n] = n < G ? __ldg(&hy[i]) : 0.f;
       }
       __syncthreads();
-      const int GQ = (G + 3) >> 2;
+      const int GQ = GP >> 2;
       for (int idx = tid; idx < WH * GQ; idx += blockDim.x) {
         const int y = idx / GQ, mq = idx - y * GQ;
-        const float2* row = Wb + y * WW;
+        const float2* row = F + y * WW;
         float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
 #pragma unroll 6
         for (int x = 0; x < WW; ++x) {
@@ -336,7 +357,7 @@ __global__ void __launch_bounds__(256, 2) fast128_kernel(const __grid_constant__
 bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
                     unsigned flags, const void* windows) {
   return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
-         g.G <= FastLayout<42, 42>::GP && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
+         g.G <= FastLayout<42, 42>::GMAX && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
          (flags & 1u) == 0 && windows == nullptr;
 }
 
