@@ -295,8 +295,10 @@ def main():
         barrier(world)
         em = max_over_ranks(float(np.mean(e_ms)), world)
         e2e = {"value": B * world / (em / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(frames_host.nbytes), "d2h_bytes_per_step": int(coefs.nbytes),
-               "ms_per_step": em, "path": "api.process_batch (pinned host frames)"}
+               "h2d_bytes_per_step": int(eng.last_h2d_bytes), "d2h_bytes_per_step": int(coefs.nbytes),
+               "ms_per_step": em,
+               "path": "api.process_batch on pinned host frames: window-only H2D (hpg_upload_windows), "
+                       "fused kernel, D2H of the coefficients"}
         api.set_batch(h, B, frames_dev)
 
     cpu = None
@@ -319,7 +321,7 @@ def main():
                        "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": args.traffic_bytes,
-                         "kernel": "holo::fused_kernel", "bytes_per_frame": bpf,
+                         "kernel": "holo::fast128_kernel<42,42>", "bytes_per_frame": bpf,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"},
             "cpu_baseline": cpu,
             "e2e": e2e,

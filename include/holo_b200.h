@@ -142,10 +142,10 @@ int hpg_run(const hpg_plan* plan, const hpg_batch* batch, const hpg_outputs* out
 int hpg_finalize_summary(const hpg_plan* plan, const hpg_batch* batch, const hpg_outputs* out,
                          float* total_intensity, void* stream);
 
-/* Full R2C plane complex64 [F][P][ny][nx/2+1] of frames f = 0..F-1 (pipeline.py:47-59).
+/* Full R2C plane complex64 [F][P][ny][nx/2+1] of frames f = 0..F-1 (pipeline.py:47-59);
+ * frames->frames/frame_format/transpose/frame_count (+ layout override) are used. 
  * workspace: hpg_workspace_size() bytes (used only for windows too large for shared memory). */
-int hpg_fourier_full(const hpg_plan* plan, const void* frames, int32_t frame_format,
-                     int32_t transpose, int64_t frame_count, void* plane, void* workspace,
+int hpg_fourier_full(const hpg_plan* plan, const hpg_batch* frames, void* plane, void* workspace,
                      size_t workspace_bytes, void* stream);
 
 /* Seven analysis parameters (analysis.py:39-94) per (frame, pol) of complex
@@ -196,6 +196,15 @@ typedef struct hpg_metric_args {
 } hpg_metric_args;
 
 int hpg_metric_partials(const hpg_metric_args* args, void* stream);
+
+/* Host -> device upload of only the FFT windows of F frames (the bytes the
+ * pipeline reads, holopipe/pipeline.py:47-54): one cudaMemcpy3DAsync per pol
+ * from the host frame buffer ([F][H][W], frame_format elements; pinned memory
+ * for asynchronous copies) into dst, packed as [F][ny][P*nx].  Process the
+ * packed buffer with hpg_batch.layout_width = P*nx, layout_height = ny,
+ * layout_col0[q] = q*nx, layout_row0[q] = 0. */
+int hpg_upload_windows(const hpg_plan* plan, const void* host_frames, int32_t frame_format,
+                       int64_t frame_count, void* dst, void* stream);
 
 const char* hpg_last_error(void);
 

@@ -33,7 +33,9 @@ def _evaluate(eng, from_stage):
     val = eng.metric(g) * _direction(g)
     rec = getattr(eng, "eval_log", None)
     if rec is not None:
-        rec.append((from_stage, val))
+        c = eng.config
+        rec.append((from_stage, val, [c.tilt[0][0], c.tilt[1][0], c.beamCentre[0][0], c.beamCentre[1][0],
+                                      c.defocus[0], c.basisWaist[0]]))
     return val
 
 
@@ -244,6 +246,7 @@ def auto_align(eng):
     eng.tweak_cycles = 0
     try:
         # frames cannot change during one auto_align call: stage them on the device once
+        # (full frames: the window origins move with the beam centre)
         plan = eng._batch_plan()
         frames = eng.source.staged(plan["frame_count"], cfg.frameWidth, cfg.frameHeight, eng.device)
         eng.source.freeze(frames[0].clone())

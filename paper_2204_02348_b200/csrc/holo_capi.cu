@@ -578,17 +578,13 @@ int hpg_finalize_summary(const hpg_plan* P, const hpg_batch* b, const hpg_output
   return HPG_SUCCESS;
 }
 
-int hpg_fourier_full(const hpg_plan* P, const void* frames, int32_t fmt, int32_t transpose,
-                        int64_t F, void* plane, void* workspace, size_t ws_bytes, void* stream) {
-  if (!P || !frames || !plane) return fail(HPG_NULLPOINTER, "null argument");
+int hpg_fourier_full(const hpg_plan* P, const hpg_batch* b, void* plane, void* workspace, size_t ws_bytes,
+                     void* stream) {
+  if (!P || !b || !b->frames || !plane) return fail(HPG_NULLPOINTER, "null argument");
   RunParams rp;
-  std::memset(&rp, 0, sizeof(rp));
-  rp.g = P->g;
-  rp.t = P->t;
-  rp.frames = frames;
-  rp.fmt = fmt;
-  rp.transpose = transpose;
+  fill_params(P, b, nullptr, 0, rp);
   rp.work = static_cast<char*>(workspace);
+  const int64_t F = b->frame_count;
   rp.lay = make_layout(P, 1, 1, 0, true);
   finish_layout(P, rp.lay, F * P->g.P, 0);
   if (rp.lay.slab_bytes > 0 && (!workspace || (int64_t)ws_bytes < rp.lay.slab_bytes * rp.lay.grid))
@@ -624,6 +620,25 @@ int hpg_field_intensity(const int16_t* fr, const int16_t* fi, const float* scale
   if (B < 1 || P < 1 || h < 1 || w < 1) return fail(HPG_INVALIDDIMENSION, "dimensions");
   cudaError_t e = launch_field_intensity(fr, fi, scale, B, P, h * w, out, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "field intensity launch");
+  return HPG_SUCCESS;
+}
+
+int hpg_upload_windows(const hpg_plan* P, const void* host, int32_t fmt, int64_t F, void* dst, void* stream) {
+  if (!P || !host || !dst) return fail(HPG_NULLPOINTER, "null argument");
+  if (F < 1) return fail(HPG_INVALIDDIMENSION, "frame_count");
+  const Geometry& g = P->g;
+  const size_t es = fmt == 1 ? 2 : 4;
+  for (int q = 0; q < g.P; ++q) {
+    cudaMemcpy3DParms m = {};
+    m.srcPtr = make_cudaPitchedPtr(const_cast<void*>(host), (size_t)g.W * es, (size_t)g.W, (size_t)g.H);
+    m.srcPos = make_cudaPos((size_t)g.col0[q] * es, (size_t)g.row0[q], 0);
+    m.dstPtr = make_cudaPitchedPtr(dst, (size_t)g.P * g.nx * es, (size_t)g.P * g.nx, (size_t)g.ny);
+    m.dstPos = make_cudaPos((size_t)q * g.nx * es, 0, 0);
+    m.extent = make_cudaExtent((size_t)g.nx * es, (size_t)g.ny, (size_t)F);
+    m.kind = cudaMemcpyHostToDevice;
+    cudaError_t e = cudaMemcpy3DAsync(&m, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy3DAsync");
+  }
   return HPG_SUCCESS;
 }
 

@@ -92,6 +92,7 @@ class Engine:
         self.tweak_cycles = 0
         self._device = device
         self.force_generic = False      # diagnostic: bypass the specialised kernels
+        self.last_h2d_bytes = 0
         self._plans = collections.OrderedDict()
         self._bufs = {}
         self._clear_products()
@@ -247,14 +248,12 @@ class Engine:
                 ((0, cfg.frameWidth // 2) if q == 0 else (cfg.frameWidth // 2, cfg.frameWidth))
             if nx > hi - lo or ny > cfg.frameHeight:
                 raise HoloError(ErrorCode.INVALIDDIMENSION, "fft window does not fit the frame region")
-        frames, fmt, tr = self.source.staged(plan["frame_count"], cfg.frameWidth, cfg.frameHeight,
-                                             self.device)
         self._clear_products()
         self._plan = plan
-        self._frames_dev = (frames, fmt, tr)
         self._st0 = {"W": cfg.frameWidth, "H": cfg.frameHeight, "P": cfg.polCount, "nx": nx, "ny": ny,
                      "pixel": float(cfg.framePixelSize), "lambdas": [float(v) for v in plan["lambdas"]],
                      "centre": [list(map(float, cfg.beamCentre[0][:2])), list(map(float, cfg.beamCentre[1][:2]))]}
+        self._frames_dev = self._stage_frames(plan["frame_count"])
         lam0, p = cfg.wavelengthCentre, cfg.framePixelSize
         from .geometry import fourier_angle_axis
         fx = fourier_angle_axis(np.arange(nx // 2 + 1), nx, p, lam0)
@@ -262,6 +261,52 @@ class Engine:
         self._fourier_axes_f64 = (fx, fy)
         self._fourier_axes = (fx.astype(np.float32), fy.astype(np.float32))
         return ErrorCode.SUCCESS
+
+    def _stage_frames(self, F):
+        """Device copy of the frames the pipeline reads: (tensor, fmt, transpose, layout).
+
+        Host sources (numpy / CPU tensors) are uploaded window-only
+        (hpg_upload_windows: one 3-D copy per pol, packed [F][ny][P*nx]);
+        device sources are used in place."""
+        cfg = self.config
+        src = self.source
+        host = src.host_array() if src._pinned is None else None
+        if host is not None and not (src.format() == 1 and src.transpose):
+            torch = _torch()
+            st0 = self._st0
+            fmt = src.format()
+            need = F * st0["W"] * st0["H"]
+            n = host.numel() if hasattr(host, "numel") else host.size
+            if n < need:
+                raise HoloError(ErrorCode.INVALIDDIMENSION, f"frame buffer holds {n} pixels, need {need}")
+            plan0 = self._native_plan(self._plan_key(0, (1.0, 1.0)))
+            P, nx, ny = st0["P"], st0["nx"], st0["ny"]
+            packed = self._buf("packed", (F, ny, P * nx), torch.float32 if fmt == 0 else torch.int16)
+            ptr = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
+            with torch.cuda.device(self.device):
+                native.check(native.lib().hpg_upload_windows(plan0.handle, ctypes.c_void_p(ptr), fmt, F,
+                                                             native.ptr(packed), native.stream_handle()),
+                             "hpg_upload_windows")
+            layout = (P * nx, ny, [q * nx for q in range(P)], [0, 0])
+            self.last_h2d_bytes = packed.numel() * packed.element_size()
+            return packed, fmt, 0, layout
+        frames, fmt, tr = src.staged(F, cfg.frameWidth, cfg.frameHeight, self.device)
+        self.last_h2d_bytes = 0 if host is None else frames.numel() * frames.element_size()
+        return frames, fmt, tr, None
+
+    def _batch_frames(self, b):
+        """Fill the frame fields (and layout override) of an hpg_batch."""
+        frames, fmt, tr, layout = self._frames_dev
+        b.frames = frames.data_ptr()
+        b.frame_format, b.transpose = fmt, tr
+        if layout is not None:
+            b.layout_width, b.layout_height = layout[0], layout[1]
+            for q in range(2):
+                b.layout_col0[q] = layout[2][q] if q < len(layout[2]) else 0
+                b.layout_row0[q] = layout[3][q]
+            b.frame_count = frames.numel() // (layout[0] * layout[1])
+        else:
+            b.frame_count = frames.numel() // (self._st0["W"] * self._st0["H"])
 
     def process_ifft(self):
         """Stage 1: carrier bins, window, IFFT grid (engine.py:170-220)."""
@@ -361,7 +406,6 @@ class Engine:
         plan = self._native_plan(key)
         B, A, P = self._plan["batch"], self._plan["avg"], st0["P"]
         gh, gw = plan.gh, plan.gw
-        frames, fmt, tr = self._frames_dev
         L = _Launch()
         L.plan, L.G, L.waist = plan, G, waist
         L.fr = self._buf("fr", (B, P, gh, gw), torch.int16)
@@ -378,11 +422,9 @@ class Engine:
         ws_bytes = plan.workspace_size(B, L.flags)
         ws = self._buf("ws", (ws_bytes,), torch.uint8)
         b = native.Batch()
-        b.frames = frames.data_ptr()
-        b.frame_format, b.transpose = fmt, tr
-        b.frame_count = frames.numel() // (st0["W"] * st0["H"])
+        self._batch_frames(b)
         b.batch_count, b.avg_count = B, A
-        L.keep = [frames, ws]
+        L.keep = [self._frames_dev[0], ws]
         if A > 1 or self._plan["mode"] != C.AVGMODE_SEQUENTIAL:
             members = torch.as_tensor(self._plan["members"].reshape(-1).astype(np.int32), device=self.device)
             b.members = members.data_ptr()
@@ -526,16 +568,18 @@ class Engine:
             torch = _torch()
             st0 = self._st0
             plan = self._native_plan(self._plan_key(0, (1.0, 1.0)))
-            frames, fmt, tr = self._frames_dev
             F = self._plan["frame_count"]
             P, ny, nh = st0["P"], st0["ny"], st0["nx"] // 2 + 1
             plane = torch.empty((F, P, ny, nh), dtype=torch.complex64, device=self.device)
             ws_bytes = plan.workspace_size(max(F, 1), 0)
             ws = self._buf("ws", (ws_bytes,), torch.uint8)
             with torch.cuda.device(self.device):
-                native.check(native.lib().hpg_fourier_full(plan.handle, native.ptr(frames), fmt, tr, F,
-                                                           native.ptr(plane), native.ptr(ws), ws_bytes,
-                                                           native.stream_handle()), "hpg_fourier_full")
+                fb = native.Batch()
+                self._batch_frames(fb)
+                fb.frame_count = F
+                native.check(native.lib().hpg_fourier_full(plan.handle, ctypes.byref(fb), native.ptr(plane),
+                                                           native.ptr(ws), ws_bytes, native.stream_handle()),
+                             "hpg_fourier_full")
             self._fourier_full = plane
         return self._fourier_full
 

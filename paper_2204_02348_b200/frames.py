@@ -100,6 +100,22 @@ class FrameSource:
         dev.copy_(host)
         return dev, fmt, tr
 
+    def host_array(self):
+        """The host-resident source buffer (numpy or CPU tensor), or None for device sources."""
+        src = self.f32 if self.kind == SOURCE_FLOAT32 else self.u16
+        if src is None:
+            return None
+        if _is_torch(src):
+            if src.device.type != "cpu":
+                return None
+            return src if src.is_contiguous() else None
+        arr = np.asarray(src)
+        if not arr.flags["C_CONTIGUOUS"]:
+            return None
+        if self.kind == SOURCE_FLOAT32 and arr.dtype != np.float32:
+            return None
+        return arr
+
     def freeze(self, tensor):
         """Keep a device copy for repeated evaluations (no external mutation expected)."""
         self._pinned = tensor

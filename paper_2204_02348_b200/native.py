@@ -28,7 +28,7 @@ EXPORTS = [
     "hpg_version", "hpg_plan_create", "hpg_plan_destroy", "hpg_plan_get_info", "hpg_plan_get_axes",
     "hpg_plan_get_basis", "hpg_workspace_size", "hpg_run", "hpg_finalize_summary",
     "hpg_fourier_full", "hpg_extract_coefs", "hpg_metric_partials", "hpg_plane_summary",
-    "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_last_error",
+    "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_upload_windows", "hpg_last_error",
 ]
 
 
@@ -109,8 +109,7 @@ def lib():
     L.hpg_workspace_size.argtypes = [c_void_p, c_int32, ctypes.c_uint32, P(c_size_t)]
     L.hpg_run.argtypes = [c_void_p, P(Batch), P(Outputs), ctypes.c_uint32, c_void_p]
     L.hpg_finalize_summary.argtypes = [c_void_p, P(Batch), P(Outputs), c_void_p, c_void_p]
-    L.hpg_fourier_full.argtypes = [c_void_p, c_void_p, c_int32, c_int32, c_int64, c_void_p,
-                                   c_void_p, c_size_t, c_void_p]
+    L.hpg_fourier_full.argtypes = [c_void_p, P(Batch), c_void_p, c_void_p, c_size_t, c_void_p]
     L.hpg_extract_coefs.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                     c_void_p]
     L.hpg_metric_partials.argtypes = [P(MetricArgs), c_void_p]
@@ -119,6 +118,7 @@ def lib():
     L.hpg_field_intensity.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
                                       c_void_p, c_void_p]
     L.hpg_plane_summary_workspace.argtypes = [c_int64, c_int32, c_int32, c_int32]
+    L.hpg_upload_windows.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]
     for name in EXPORTS:
         getattr(L, name).restype = c_int32
     L.hpg_last_error.restype = ctypes.c_char_p

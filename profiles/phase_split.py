@@ -15,10 +15,9 @@ src_path = rows[0][1]
 markers = {}
 for i, line in enumerate(open(src_path), 1):
     m = re.search(r"// -+ (row pass|column pass|IFFT|removal phase|HG overlap)", line)
-    if re.search(r"^template <int P, int N, int L, int COUNT", line):
-        markers[i] = "IFFT"
-    if re.search(r"^struct FastLayout", line):
+    if re.search(r"__global__ void", line) and "kernel_line" not in markers.values():
         markers[i] = "setup"
+        kernel_start = i
     if m:
         markers[i] = m.group(1)
 hdr = rows[2]
@@ -64,10 +63,11 @@ def phase_of(line):
     return name
 
 
+first = min(markers)   # lines before the kernel body are inlined helpers: they inherit the phase
 cur = "setup"
 tot, st = {}, {}
 for a, fname, line, n, s in ins:
-    if fname == main and line is not None:
+    if fname == main and line is not None and line >= first:
         cur = phase_of(line)
     tot[cur] = tot.get(cur, 0) + n
     st[cur] = st.get(cur, 0) + s
