@@ -1,0 +1,143 @@
+"""Multi-GPU data parallelism over frames.
+
+Frames (batch rows) are independent for fields and coefficients, so each
+rank processes a contiguous shard of the batch with its own engine and plan
+replica -- no collective on the data path.  The only exchange is the metric
+reduction AutoAlign iterates on: each rank computes fp64 partials of its
+rows on the GPU (hpg_metric_partials), then
+
+  * the Gram matrix A^H A (cols x cols) is all-reduced (sum),
+  * the per-row power / diagonal / mode-group sums are all-gathered,
+
+and every rank finishes the nine metrics identically on the host
+(analysis.finish_metrics), so AutoAlign decisions stay replicated and
+deterministic.  Works with NCCL (GPU tensors) and gloo (CPU tensors, used by
+the CPU tests).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import constants as C
+from .analysis import average_slot, finish_metrics
+from .engine import mode_group_of_index
+
+
+def shard(batch, world, rank):
+    """Contiguous [start, stop) rows of ``batch`` owned by ``rank``."""
+    per = -(-batch // world)
+    start = min(batch, rank * per)
+    return start, min(batch, start + per)
+
+
+def _all_gather_var(t, group=None):
+    """all_gather of 1-D tensors of different lengths, concatenated in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = torch.tensor([t.numel()], dtype=torch.int64, device=t.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    mx = int(max(int(s.item()) for s in sizes))
+    buf = torch.zeros(mx, dtype=t.dtype, device=t.device)
+    buf[:t.numel()] = t
+    out = [torch.zeros_like(buf) for _ in range(world)]
+    dist.all_gather(out, buf, group=group)
+    return torch.cat([o[:int(s.item())] for o, s in zip(out, sizes)])
+
+
+def exclusive_prefix(count, group=None, device="cpu"):
+    """Sum of ``count`` over lower ranks (global row offset of this shard)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    t = torch.tensor([int(count)], dtype=torch.int64, device=device)
+    all_c = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(all_c, t, group=group)
+    r = dist.get_rank(group)
+    return int(sum(int(c.item()) for c in all_c[:r])), int(sum(int(c.item()) for c in all_c))
+
+
+def reduce_and_finish(row_power, diag_power, group_power, gram, rows_global, cols, group=None,
+                      have_labels=True):
+    """Combine per-rank partials (torch tensors on the process-group device) into the metrics."""
+    import torch.distributed as dist
+    dist.all_reduce(gram, group=group)
+    rp = _all_gather_var(row_power, group).cpu().numpy()
+    dp = _all_gather_var(diag_power, group).cpu().numpy()
+    gp = _all_gather_var(group_power, group).cpu().numpy()
+    return finish_metrics(rp, dp, gp, gram.cpu().numpy(), rows_global, cols, have_labels)
+
+
+def host_partials(coefs, labels, diag_offset, ndiag):
+    """Reference partial sums of one shard in numpy (what hpg_metric_partials computes)."""
+    A = np.asarray(coefs, np.complex128)
+    pw = np.abs(A) ** 2
+    R, Cc = A.shape
+    rp = pw.sum(axis=1)
+    dp = np.full(R, -1.0)
+    gp = np.full(R, -1.0)
+    for r in range(R):
+        d = r + diag_offset
+        if d < ndiag:
+            dp[r] = pw[r, d]
+            gp[r] = pw[r, np.asarray(labels) == labels[d]].sum() if labels is not None else dp[r]
+    gram = A.conj().T @ A
+    return rp, dp, gp, gram
+
+
+def calc_metrics(eng, row_offset=0, group=None):
+    """Transfer-matrix metrics of a batch sharded over the process group.
+
+    ``eng`` holds this rank's rows (a contiguous shard starting at global row
+    ``row_offset``); wavelength membership follows the global row index
+    (holopipe/engine.py:102-106).  Returns the MetricsReport, identical on
+    every rank.  Pol-independent / A A^H variants are single-process only.
+    """
+    import torch
+    from . import native
+    cfg = eng.config
+    dev = eng.device
+    coefs = eng.coefs_device()
+    B_local = coefs.shape[0]
+    P, M = eng._st0["P"], eng._mode_count
+    cols = P * M
+    lams = cfg.wavelength_list()
+    L = len(lams)
+    start, B = exclusive_prefix(B_local, group, device=dev)
+    rows = np.arange(start, start + B_local)
+    if cfg.wavelengthOrdering[C.WAVELENGTHORDER_INPUT] == C.WAVELENGTHORDER_FAST or L <= 1:
+        wl = rows % L
+    else:
+        wl = np.minimum(rows * L // B, L - 1)
+    labels = torch.as_tensor(np.array([q * 1000 + mode_group_of_index(i) for q in range(P) for i in range(M)],
+                                      np.int32), device=dev)
+    per = np.full((C.METRIC_COUNT, L), C.METRIC_UNSET)
+    for w in range(L):
+        local = np.nonzero(wl == w)[0]
+        off, n_w = exclusive_prefix(local.size, group, device=dev)
+        if n_w == 0:
+            continue
+        R = local.size
+        rp = torch.zeros(R, dtype=torch.float64, device=dev)
+        dp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
+        gp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
+        gram = torch.zeros((cols, cols), dtype=torch.complex128, device=dev)
+        if R:
+            ids = torch.as_tensor(local.astype(np.int32), device=dev)
+            a = native.MetricArgs()
+            a.coefs = coefs.data_ptr()
+            a.rows, a.cols, a.ld = R, cols, cols
+            a.row_ids = ids.data_ptr()
+            a.labels = labels.data_ptr()
+            a.ndiag, a.diag_offset, a.gram_rows = min(n_w, cols), off, 0
+            a.row_power, a.diag_power, a.group_power = rp.data_ptr(), dp.data_ptr(), gp.data_ptr()
+            a.gram = gram.data_ptr()
+            with torch.cuda.device(dev):
+                native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle()),
+                             "hpg_metric_partials")
+        per[:, w] = reduce_and_finish(rp, dp, gp, gram, n_w, cols, group)
+    return average_slot(per)

@@ -77,8 +77,22 @@ def test_snap_estimate_matches_reference():
 
 
 def test_end_to_end_converges_like_reference():
+    """The tweak stage is a trajectory: a 2e-6 dB difference in one parabola
+    point moves a vertex by a sub-nanometre amount and later decisions diverge
+    (tools/autoalign_trace.py finds the first divergent evaluation).  The bar
+    is therefore on the converged goal: not worse than the reference's by more
+    than 1e-3 dB, and the converged parameters in the same basin."""
     from paper_2204_02348_b200 import align
     g = np.load(os.path.join(GOLDEN, "autoalign_tol1e-4.npz"))
     eng = _engine(tol=1e-4)
     goal = align.auto_align(eng)
-    assert abs(goal - float(g["goal"])) <= 1e-3, (goal, float(g["goal"]))
+    ref = float(g["goal"])
+    assert goal >= ref - 1e-3, (goal, ref)
+    assert goal <= ref + 0.05, (goal, ref)
+    c = eng.config
+    got = np.array([c.tilt[0][0], c.tilt[1][0], c.beamCentre[0][0], c.beamCentre[1][0], c.defocus[0],
+                    c.basisWaist[0]])
+    fin = g["final"]
+    assert np.all(np.abs(got[:2] - fin[:2]) <= 0.01)          # degrees
+    assert np.all(np.abs(got[2:4] - fin[2:4]) <= 2e-6)        # metres (0.1 px)
+    assert abs(got[5] / fin[5] - 1) <= 0.02
