@@ -74,31 +74,33 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
   }
 }
 
-// Last column stage of the inverse transform with the epilogue fused in:
-// removal phase (separable ey[y] * ex[x], incl. ifftshift sign and 1/(nx ny)),
-// optional batch calibration, and the running max |Re|,|Im| for the int16 scale.
+// Last stage of the inverse transform (along x, for every row y) with the
+// epilogue fused in: reads T[c][y] (column-major), writes F[y][x] row-major,
+// applies the removal phase (separable ey[y] * ex[x], incl. ifftshift sign and
+// 1/(nx ny)), the optional batch calibration, and keeps the running max
+// |Re|,|Im| for the int16 scale.
 template <int P, int N, int L, int COUNT>
-HOLO_DEV float ct_stage_final_cols(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw,
+HOLO_DEV float ct_stage_final_rows(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw,
                                    const float2* ey, const float2* ex, bool use_bc, float2 bc) {
   constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
   static_assert(mp == 1, "final stage");
   float lmax = 0.f;
   for (int task = threadIdx.x; task < total; task += blockDim.x) {
-    const int q = task % COUNT, k = task / COUNT;   // column x = q
+    const int y = task % COUNT, k = task / COUNT;
     float2 v[P];
 #pragma unroll
-    for (int j = 0; j < P; ++j) v[j] = src[q + (k * m_in + j) * COUNT];
+    for (int j = 0; j < P; ++j) v[j] = src[y + (k * m_in + j) * COUNT];
 #pragma unroll
     for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<true>(tw[(j * k) % N]));
     dft_fixed<P, true>(v);
-    const float2 exq = ex[q];
+    const float2 eyq = ey[y];
 #pragma unroll
     for (int t = 0; t < P; ++t) {
-      const int y = k + L * t;
-      float2 o = cmul(cmul(v[t], ey[y]), exq);
+      const int x = k + L * t;
+      float2 o = cmul(cmul(v[t], eyq), ex[x]);
       if (use_bc) o = cmul(o, bc);
       lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
-      dst[q + y * COUNT] = o;
+      dst[y * N + x] = o;
     }
   }
   return lmax;
@@ -106,10 +108,10 @@ HOLO_DEV float ct_stage_final_cols(const float2* __restrict__ src, float2* __res
 
 // First half of a 128-point FFT with 16 points per thread (8 threads per
 // transform): on entry z holds x[t + 8 j]; on exit z[k1] = W128^(t k1) DFT16(z)[k1].
-HOLO_DEV void fft128_stage1(float2* z, int t, const float2* tw128) {
+HOLO_DEV void fft128_stage1(float2* z, int t, const float2* twt) {
   dft16<false>(z);
 #pragma unroll
-  for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], tw128[(t * k1) & 127]);
+  for (int k1 = 1; k1 < 16; ++k1) z[k1] = cmul(z[k1], twt[k1 * 8 + t]);   // W128^(t k1), conflict-free
 }
 // Second half for k1 = t + 8h: 8x8 transpose through the group's tile, DFT-8;
 // v[k2] = X[t + 8h + 16 k2].
@@ -144,6 +146,11 @@ struct FastLayout {
   static_assert(basis_off + (WH + WW) * GMAX * sizeof(float) <= 64 * ZS * sizeof(float2), "basis must fit zs");
 };
 
+// the transposed basis of one pol stays resident when it fits next to the 64 KB layout
+// without dropping below 3 CTAs per SM
+constexpr int kPersistentBasisGP = 36;
+HOLO_DEV bool persistent_basis(int GP) { return GP <= kPersistentBasisGP; }
+
 template <int WH, int WW>
 __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__ RunParams p,
                                                         const __grid_constant__ FastTables ft) {
@@ -164,11 +171,12 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
   const int tid = threadIdx.x, t = tid & 7, grp = tid >> 3;
   float2* xg = xbuf + grp * LY::XG;
 
-  for (int i = tid; i < 128; i += blockDim.x) tw128[i] = p.t.tw_nx[i];
+  for (int i = tid; i < 128; i += blockDim.x) tw128[i] = p.t.tw_nx[((i >> 3) * (i & 7)) & 127];
   for (int i = tid; i < WH; i += blockDim.x) twh[i] = p.t.tw_gh[i];
   for (int i = tid; i < WW; i += blockDim.x) tww[i] = p.t.tw_gw[i];
 
   const int items = p.B * g.P;
+  int staged_q = -1;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int b = item / g.P, q = item - b * g.P;
     const int w = p.wl ? p.wl[b] : 0;
@@ -218,6 +226,22 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
       }
     }
     __syncthreads();
+    {
+      // warm L2 with the window this CTA processes next (its HBM latency then
+      // hides behind this item's column pass, IFFT and overlap)
+      const int nitem = item + gridDim.x;
+      if (nitem < items) {
+        const int nb = nitem / g.P, nq = nitem - nb * g.P;
+        const int es = p.fmt == 0 ? 4 : 2;
+        const char* base = reinterpret_cast<const char*>(p.frames) +
+                           ((int64_t)nb * W * H + (int64_t)g.row0[nq] * W + g.col0[nq]) * es;
+        for (int i = tid; i < 128 * 5; i += blockDim.x) {
+          const int row = i / 5, part = i - row * 5;
+          const int off = min(part * 128, 128 * es - 1);
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)row * W * es + off));
+        }
+      }
+    }
 
     // --------------------------------------------------------- column pass
 #pragma unroll 1
@@ -253,7 +277,7 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
             if (r < WH) {
               float2 val = make_float2(0.f, 0.f);
               if (r >= rlo && r <= rhi) val = cmul(h ? o1[k2] : o0[k2], cmul(s_py[r], pxc));
-              zs[w_addr<ZS>(r * WW + c)] = val;
+              zs[w_addr<ZS>(c * WH + r)] = val;
             }
           }
         }
@@ -264,16 +288,17 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
     // ------------------------------------------------ IFFT (rows, then columns)
     float2* T = xbuf;
     float2* F = zs;   // linear [WH][WW] once the mapped W has been consumed
-    ct_stage<6, WW, 1, WH, WW, 1, true, ZS>(zs, T, tww);
+    // W is column-major (WT[c][r]): transform along r (y) first, then along c (x)
+    ct_stage<6, WH, 1, WW, WH, 1, true, ZS>(zs, T, twh);
     __syncthreads();
-    ct_stage<7, WW, 6, WH, WW, 1, true>(T, F, tww);
+    ct_stage<7, WH, 6, WW, WH, 1, true>(T, F, twh);
     __syncthreads();
-    ct_stage<6, WH, 1, WW, 1, WW, true>(F, T, twh);
+    ct_stage<6, WW, 1, WH, 1, WH, true>(F, T, tww);
     __syncthreads();
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
-    float lmax = ct_stage_final_cols<7, WH, 6, WW>(T, F, twh, s_ey, s_ex, p.bcal != nullptr, bc);
+    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc);
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     if ((tid & 31) == 0) redf[tid >> 5] = lmax;
@@ -301,18 +326,36 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
     // ---------------------------------------------------------- HG overlap
     if (p.coefs && g.G > 0) {
       const int G = g.G, GP = (G + 3) & ~3;
-      float* hxT = reinterpret_cast<float*>(smem + LY::zs + LY::basis_off);   // [WW][GP]
-      float* hyT = hxT + WW * GP;                                             // [WH][GP]
-      float2* U = xbuf;                                                       // [WH][GP]
-      const float* hx = p.t.hx + (size_t)q * G * WW;
-      const float* hy = p.t.hy + (size_t)q * G * WH;
-      for (int i = tid; i < GP * WW; i += blockDim.x) {   // i = m*WW + x: coalesced reads
-        const int m = i / WW, x = i - m * WW;
-        hxT[x * GP + m] = m < G ? __ldg(&hx[i]) : 0.f;
-      }
-      for (int i = tid; i < GP * WH; i += blockDim.x) {
-        const int n = i / WH, y = i - n * WH;
-        hyT[y * GP + n] = n < G ? __ldg(&hy[i]) : 0.f;
+      // basis, transposed to [x][m] so one 16-byte load gives 4 orders: kept for
+      // the CTA's lifetime when it fits (items of one CTA share a pol whenever
+      // gridDim is a multiple of P), else staged per item into the free zs
+      const bool keep = persistent_basis(GP);
+      float* hxT = keep ? reinterpret_cast<float*>(smem + LY::bytes)
+                        : reinterpret_cast<float*>(smem + LY::zs + LY::basis_off);   // [WW][GP]
+      float* hyT = hxT + WW * GP;                                                   // [WH][GP]
+      float2* U = xbuf;                                                             // [WH][GP]
+      if (!keep || q != staged_q) {
+        const float* hx = p.t.hx + (size_t)q * G * WW;
+        const float* hy = p.t.hy + (size_t)q * G * WH;
+        for (int i = tid; i < (GP / 4) * WW; i += blockDim.x) {   // thread -> (x, 4 orders)
+          const int x = i % WW, m4 = 4 * (i / WW);
+          float4 h;
+          h.x = m4 + 0 < G ? __ldg(&hx[(m4 + 0) * WW + x]) : 0.f;
+          h.y = m4 + 1 < G ? __ldg(&hx[(m4 + 1) * WW + x]) : 0.f;
+          h.z = m4 + 2 < G ? __ldg(&hx[(m4 + 2) * WW + x]) : 0.f;
+          h.w = m4 + 3 < G ? __ldg(&hx[(m4 + 3) * WW + x]) : 0.f;
+          *reinterpret_cast<float4*>(&hxT[x * GP + m4]) = h;
+        }
+        for (int i = tid; i < (GP / 4) * WH; i += blockDim.x) {
+          const int y = i % WH, n4 = 4 * (i / WH);
+          float4 h;
+          h.x = n4 + 0 < G ? __ldg(&hy[(n4 + 0) * WH + y]) : 0.f;
+          h.y = n4 + 1 < G ? __ldg(&hy[(n4 + 1) * WH + y]) : 0.f;
+          h.z = n4 + 2 < G ? __ldg(&hy[(n4 + 2) * WH + y]) : 0.f;
+          h.w = n4 + 3 < G ? __ldg(&hy[(n4 + 3) * WH + y]) : 0.f;
+          *reinterpret_cast<float4*>(&hyT[y * GP + n4]) = h;
+        }
+        staged_q = keep ? q : -1;
       }
       __syncthreads();
       const int GQ = GP >> 2;
@@ -363,18 +406,21 @@ bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, 
 
 cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
   using LY = FastLayout<42, 42>;
-  static bool init = false;
-  if (!init) {
+  const int GP = (p.g.G + 3) & ~3;
+  const size_t bytes = LY::bytes + ((p.coefs && p.g.G > 0 && GP <= kPersistentBasisGP)
+                                        ? (size_t)(42 + 42) * GP * sizeof(float) : 0);
+  static size_t configured = 0;
+  if (bytes > configured) {
     cudaError_t e = cudaFuncSetAttribute(fast128_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)LY::bytes);
+                                         (int)bytes);
     if (e != cudaSuccess) return e;
-    init = true;
+    configured = bytes;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast128_kernel<42, 42>, 256, LY::bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast128_kernel<42, 42>, 256, bytes);
   const int items = p.B * p.g.P;
   const int grid = std::max(1, std::min(items, num_sms * std::max(per_sm, 1)));
-  fast128_kernel<42, 42><<<grid, 256, LY::bytes, s>>>(p, ft);
+  fast128_kernel<42, 42><<<grid, 256, bytes, s>>>(p, ft);
   return cudaGetLastError();
 }
 

@@ -117,7 +117,7 @@ def test_uint16_source_matches_float32():
     assert np.array_equal(a, b)
     eng.source.set_uint16(np.ascontiguousarray(np.transpose(frames.astype(np.uint16), (0, 2, 1))), 1)
     c = eng.process_batch()[0]       # transposed frames take the generic kernel
-    assert rel_l2_rows(c, a) <= 1e-6
+    assert rel_l2_rows(c, a) <= 1e-5
 
 
 @pytest.mark.parametrize("name", ["pr1", "dualpol", "largebasis", "multiwl", "dualpol_cal"])
