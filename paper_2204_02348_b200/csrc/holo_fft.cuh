@@ -228,16 +228,59 @@ template <bool INV>
 HOLO_DEV void stockham_stage_generic(const float2* src, float2* dst, int n, int L, int P,
                                      int count, int sstride, int estride, const float2* tw,
                                      int tid, int nthr) {
+  // odd prime radix P: inputs loaded and twiddled once, then the conjugate-pair
+  // DFT (same algebra as dft_odd) with the W_P powers read from the W_n table
+  constexpr int PMAX = 128;
   const int m_in = n / L, mp = m_in / P;
   const int per = n / P;
   const int total = count * per;
-  const int np = n / P;  // W_P^{st} = W_n^{(st mod P) * n/P}
+  const int np = n / P;  // W_P^{e} = W_n^{e * n/P}
+  const int H = (P - 1) / 2;
   for (int task = tid; task < total; task += nthr) {
     const int q = task / per, r = task - q * per;
     const int k = r / mp, qp = r - k * mp;
     const float2* s = src + (size_t)q * sstride;
     float2* d = dst + (size_t)q * sstride;
-    for (int t = 0; t < P; ++t) {
+    if (P <= PMAX && (P & 1)) {
+      float2 sp[PMAX / 2], sm[PMAX / 2];
+      float2 v0 = s[(size_t)(k * m_in + qp) * estride];
+      float2 tot = v0;
+      int e1 = 0, e2 = 0;  // (j k mp) mod n and ((P-j) k mp) mod n, updated incrementally
+      const int stepw = (k * mp) % n;
+      e2 = (P * stepw) % n;
+      for (int j = 1; j <= H; ++j) {
+        e1 += stepw; if (e1 >= n) e1 -= n;
+        e2 -= stepw; if (e2 < 0) e2 += n;
+        float2 a = s[(size_t)(k * m_in + qp + mp * j) * estride];
+        float2 b = s[(size_t)(k * m_in + qp + mp * (P - j)) * estride];
+        if (L > 1) {
+          a = cmul(a, twid<INV>(tw[e1]));
+          b = cmul(b, twid<INV>(tw[e2]));
+        }
+        sp[j - 1] = cadd(a, b);
+        sm[j - 1] = csub(a, b);
+        tot = cadd(tot, sp[j - 1]);
+      }
+      d[(size_t)(k * mp + qp) * estride] = tot;
+      for (int t = 1; t <= H; ++t) {
+        float2 re = v0, im = make_float2(0.f, 0.f);
+        int e = 0;
+        for (int j = 1; j <= H; ++j) {
+          e += t; if (e >= P) e -= P;
+          const float2 w = tw[e * np];            // cos(2 pi e/P) - i sin(2 pi e/P)
+          const float c = w.x, sn = -w.y;
+          re.x = fmaf(c, sp[j - 1].x, re.x);
+          re.y = fmaf(c, sp[j - 1].y, re.y);
+          im.x = fmaf(sn, sm[j - 1].x, im.x);
+          im.y = fmaf(sn, sm[j - 1].y, im.y);
+        }
+        const float2 rr = rot90<INV>(im);
+        d[(size_t)((k + L * t) * mp + qp) * estride] = cadd(re, rr);
+        d[(size_t)((k + L * (P - t)) * mp + qp) * estride] = csub(re, rr);
+      }
+      continue;
+    }
+    for (int t = 0; t < P; ++t) {   // any other radix: direct O(P^2)
       float2 acc = make_float2(0.f, 0.f);
       for (int j = 0; j < P; ++j) {
         float2 v = s[(size_t)(k * m_in + qp + mp * j) * estride];
