@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "../../include/holo_b200.h"
 #include "holo_internal.h"
 
@@ -16,14 +18,12 @@ cudaError_t launch_finalize(const RunParams& p, float* total, cudaStream_t s);
 cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s);
 cudaError_t launch_fourier_full(const RunParams& p, int64_t F, float2* plane, cudaStream_t s);
 cudaError_t set_smem_limits();
-struct FastTables {
-  const float2* px;
-  const float2* py;
-  const int16_t* crange;
-};
 bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
                     unsigned flags, const void* windows);
 cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
+bool tc_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
+                  const void* windows);
+cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
 cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
                                  const double* ya, float* params, int slots, float* total, double* pol_total,
                                  char* work, int grid, cudaStream_t s);
@@ -385,9 +385,39 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
     crange[2 * c] = (int16_t)lo;
     crange[2 * c + 1] = (int16_t)hi;
   }
+  // tensor-core row DFT (holo_fast_tc.cu): A[n][x], n < 64 -> Re, n >= 64 -> Im of
+  // exp(-2 pi i kx_c x / nx) * px[c] = exp(-2 pi i kx_c (x - xi_x + nx/2) / nx), c = n mod 64,
+  // split into fp16 hi + lo; rows c >= ww are zero.  Only for nx == 128, wavelength 0.
+  std::vector<uint32_t> a_tc;
+  if (g.nx == 128 && g.ww <= 64) {
+    a_tc.assign((size_t)g.P * 2 * 128 * 64, 0u);
+    for (int q = 0; q < g.P; ++q) {
+      const int kx = g.k0[q][0][0];
+      for (int n = 0; n < 128; ++n) {
+        const int c = n & 63;
+        if (c >= g.ww) continue;
+        const double kc = (double)(kx + c - g.ww / 2);
+        for (int x2 = 0; x2 < 64; ++x2) {
+          uint16_t hh[2], ll[2];
+          for (int e = 0; e < 2; ++e) {
+            const int x = 2 * x2 + e;
+            const double ang = -2.0 * kPi * kc * ((double)x - xi[q][0] + g.nx / 2.0) / g.nx;
+            const double v = n < 64 ? std::cos(ang) : std::sin(ang);
+            const __half h = __double2half(v);
+            const __half l = __double2half(v - (double)__half2float(h));
+            hh[e] = __half_as_ushort(h);
+            ll[e] = __half_as_ushort(l);
+          }
+          a_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + x2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + x2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+        }
+      }
+    }
+  }
+  if (a_tc.empty()) a_tc.push_back(0u);
   P->fill = d->fill_factor;
   std::vector<char> blob;
-  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange);
+  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange), o_atc = push(blob, a_tc);
   const size_t o_nx = push(blob, tw_nx), o_ny = push(blob, tw_ny), o_gw = push(blob, tw_gw), o_gh = push(blob, tw_gh);
   const size_t o_w = push(blob, wtab), o_rx = push(blob, remx), o_ry = push(blob, remy);
   std::vector<float> hxv = P->hx, hyv = P->hy;
@@ -423,6 +453,7 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.px = reinterpret_cast<const float2*>(base + o_px);
   P->ft.py = reinterpret_cast<const float2*>(base + o_py);
   P->ft.crange = reinterpret_cast<const int16_t*>(base + o_cr);
+  P->ft.a_tc = reinterpret_cast<const uint32_t*>(base + o_atc);
   e = set_smem_limits();
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
   *out = P;
@@ -557,7 +588,10 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
   if ((rp.lay.slab_bytes > 0 || (flags & HPG_FLAG_SUMMARY)) && (!o->workspace || (int64_t)o->workspace_bytes < need))
     return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
   cudaError_t e;
-  if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&
+  if (!(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
+      tc_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows))
+    e = launch_fast_tc(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+  else if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&
       !b->members)
     e = launch_fast(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
   else

@@ -1,0 +1,481 @@
+// Tensor-core variant of the specialised 128-window kernel (tcgen05, sm_100a).
+//
+// The row pass -- a pruned 128-point R2C DFT of every window row, the largest
+// block of floating-point work on the path -- is one GEMM on the 5th-generation
+// tensor cores per window:
+//
+//   D[n][y] = sum_x A[n][x] * f[y][x]        M = 128 (n), N = 128 (y), K = 128 (x)
+//   A[n][x] = Re / Im of exp(-2 pi i kx_c x / 128) * px[c]   (n = c / 64 + c)
+//
+// so D holds Re and Im of R[y][c] * px[c] for the WW bins the Fourier window
+// keeps, with the recentring phase already applied (holopipe/pipeline.py:79-127).
+// Precision is fp32-class through an fp16 split of both operands,
+// A*f ~= Ah*fh + Al*fh + Ah*fl (products exact, fp32 accumulation; the frame is
+// scaled by an exact power of two so fh+fl keep 22 bits).
+//
+//   A  (constant per pol)   TMEM columns [0,128): hi | lo, loaded once per CTA
+//   f  (window, per item)   shared memory, canonical K-major layout, two K chunks
+//   D  (accumulator)        TMEM columns [128,256), drained to shared memory
+//
+// One elected thread issues 24 tcgen05.mma per window and commits to an
+// mbarrier.  Everything after the row pass -- column FFTs, 42x42 IFFT,
+// removal phase, int16 packing, HG overlap -- is the SIMT code of holo_fast.cu
+// (shared helpers in holo_fast_common.cuh).  Two 384-thread CTAs per SM
+// (256 TMEM columns each).
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "holo_fast_common.cuh"
+#include "holo_internal.h"
+
+namespace holo {
+
+namespace {
+
+constexpr int kTcThreads = 384;
+constexpr int kTcGroups = kTcThreads / 8;
+constexpr int kZP = 136;  // T plane row pitch (floats)
+
+HOLO_DEV uint32_t smem_u32(const void* ptr) { return static_cast<uint32_t>(__cvta_generic_to_shared(ptr)); }
+
+// UMMA shared-memory descriptor, K-major, no swizzle (version 1 = sm_100)
+HOLO_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+
+HOLO_DEV void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{.reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+HOLO_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase));
+  }
+}
+
+HOLO_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+
+HOLO_DEV void tmem_ld16(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+
+HOLO_DEV uint32_t pack_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+}  // namespace
+
+template <int WH, int WW>
+struct TcLayout {
+  static constexpr int XG = 72;        // 8x8 exchange tile per 8-thread group (float2)
+  static constexpr int GMAX = 48;
+  static constexpr size_t planes_bytes = 2 * (size_t)WW * kZP * sizeof(float);     // Re/Im of T[c][y]
+  static constexpr size_t stage_bytes = 2 * 4 * 4096;                               // f hi/lo, 4 K-steps
+  static constexpr size_t region0 = ((planes_bytes > stage_bytes ? planes_bytes : stage_bytes) + 1023) & ~size_t(1023);
+  static constexpr size_t xbuf = region0;                                           // [48][XG]
+  static constexpr size_t twt = xbuf + kTcGroups * XG * sizeof(float2);             // [128]
+  static constexpr size_t twh = twt + 128 * sizeof(float2);
+  static constexpr size_t tww = twh + WH * sizeof(float2);
+  static constexpr size_t ph = tww + WW * sizeof(float2);                           // py[WH] ex[WW] ey[WH]
+  static constexpr size_t basis = (ph + (2 * WH + WW) * sizeof(float2) + 15) & ~size_t(15);
+  static constexpr size_t basis_stage_off = ((WH * WW * sizeof(float2)) + 255) & ~size_t(255);  // in region0
+  static_assert(WH * WW * sizeof(float2) <= planes_bytes, "W / F must fit region0");
+  static_assert(basis_stage_off + (WH + WW) * GMAX * sizeof(float) <= region0, "basis staging must fit region0");
+  static_assert(WH * WW * sizeof(float2) <= kTcGroups * XG * sizeof(float2), "IFFT ping-pong must fit xbuf");
+  static_assert(WH * GMAX * sizeof(float2) <= kTcGroups * XG * sizeof(float2), "overlap U must fit xbuf");
+  static_assert(WW <= 64 && WW <= kTcGroups, "one column round");
+};
+
+constexpr int kTcPersistentGP = 36;
+
+template <int WH, int WW>
+__global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_constant__ RunParams p,
+                                                                 const __grid_constant__ FastTables ft) {
+  using LY = TcLayout<WH, WW>;
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ float redf[kTcThreads / 32];
+  __shared__ __align__(8) uint64_t mbar;
+  __shared__ uint32_t tbase;
+  char* r0 = smem;                                       // stage / T planes / W / F / basis staging
+  float* planeRe = reinterpret_cast<float*>(r0);
+  float* planeIm = planeRe + WW * kZP;
+  float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
+  float2* twt = reinterpret_cast<float2*>(smem + LY::twt);
+  float2* twh = reinterpret_cast<float2*>(smem + LY::twh);
+  float2* tww = reinterpret_cast<float2*>(smem + LY::tww);
+  float2* s_py = reinterpret_cast<float2*>(smem + LY::ph);
+  float2* s_ex = s_py + WH;
+  float2* s_ey = s_ex + WW;
+  const Geometry& g = p.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = tid & 7, grp = tid >> 3;
+  float2* xg = xbuf + grp * LY::XG;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int i = tid; i < 128; i += blockDim.x) twt[i] = p.t.tw_nx[((i >> 3) * (i & 7)) & 127];
+  for (int i = tid; i < WH; i += blockDim.x) twh[i] = p.t.tw_gh[i];
+  for (int i = tid; i < WW; i += blockDim.x) tww[i] = p.t.tw_gw[i];
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tm = tbase;                  // A hi [0,64) lo [64,128), D [128,256)
+  const uint32_t d_tm = tm + 128;
+  // instruction descriptor: F16 x F16 -> F32, K-major A and B, N = 128, M = 128
+  const uint32_t idesc = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+  uint32_t phase = 0;
+  int loaded_q = -1, staged_q = -1;
+  const int items = p.B * g.P;
+  const int W = g.W, H = g.H;
+
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int b = item / g.P, q = item - b * g.P;
+    const int kys = (g.k0[q][0][1] - WH / 2) & 127;
+    __syncthreads();  // previous item done with every buffer
+    for (int i = tid; i < WH; i += blockDim.x) {
+      s_py[i] = ft.py[q * WH + i];
+      s_ey[i] = p.t.rem_y[q * WH + i];
+    }
+    for (int i = tid; i < WW; i += blockDim.x) s_ex[i] = p.t.rem_x[q * WW + i];
+    if (q != loaded_q) {
+      // row-DFT matrix of this pol into TMEM lanes 0..127, columns [0,128)
+      if (warp < 4) {
+        const uint32_t* src = ft.a_tc + ((size_t)q * 2 * 128 + warp * 32 + lane) * 64;
+        uint32_t r[32];
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const uint32_t* s2 = src + (size_t)part * 128 * 64 + half * 32;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
+            tmem_st32(tm + ((uint32_t)(warp * 32) << 16) + part * 64 + half * 32, r);
+          }
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+      }
+      loaded_q = q;
+    }
+
+    // ------------------------------------------------ window -> registers, peak
+    const int row0 = g.row0[q], col0 = g.col0[q];
+    float v[6][8];
+    float amax = 0.f;
+#pragma unroll
+    for (int it = 0; it < 6; ++it) {
+      const int idx = it * kTcThreads + tid;
+      if (idx < 2048) {
+        const int y = idx >> 4, o = idx & 15;
+        const int64_t base = (int64_t)b * W * H + (int64_t)(row0 + y) * W + col0 + 8 * o;
+        if (p.fmt == 0) {
+          const float* src = reinterpret_cast<const float*>(p.frames) + base;
+          if ((col0 & 3) == 0) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(src));
+            const float4 c = __ldg(reinterpret_cast<const float4*>(src + 4));
+            v[it][0] = a.x; v[it][1] = a.y; v[it][2] = a.z; v[it][3] = a.w;
+            v[it][4] = c.x; v[it][5] = c.y; v[it][6] = c.z; v[it][7] = c.w;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[it][e] = __ldg(src + e);
+          }
+        } else {
+          const unsigned short* src = reinterpret_cast<const unsigned short*>(p.frames) + base;
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[it][e] = (float)__ldg(src + e);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) amax = fmaxf(amax, fabsf(v[it][e]));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) redf[warp] = amax;
+    __syncthreads();
+    amax = redf[0];
+#pragma unroll
+    for (int j = 1; j < kTcThreads / 32; ++j) amax = fmaxf(amax, redf[j]);
+    // exact power-of-two scale: |f| * s < 2^14 keeps fh + fl within fp16 range with 22 bits
+    int ex2 = 0;
+    frexpf(amax, &ex2);
+    const float s = amax > 0.f ? ldexpf(1.f, 14 - ex2) : 1.f;
+    const float inv_s = amax > 0.f ? ldexpf(1.f, ex2 - 14) : 1.f;
+
+    // ------------------------------------------------ row DFT on tensor cores
+#pragma unroll 1
+    for (int ch = 0; ch < 2; ++ch) {
+      if (ch == 1) {  // chunk-0 MMAs must have finished reading the stage buffer
+        mbar_wait(&mbar, phase);
+        phase ^= 1;
+      }
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        const int idx = it * kTcThreads + tid;
+        if (idx < 2048 && ((idx >> 3) & 1) == ch) {
+          const int y = idx >> 4, ol = idx & 7;                 // octet within the chunk
+          const int kstep = ol >> 1, kh = ol & 1;
+          const uint32_t off = (uint32_t)kstep * 4096 + ((uint32_t)((y >> 3) * 2 + kh) * 8 + (y & 7)) * 16;
+          float sc[8], lo[8];
+          uint32_t hi2[4], lo2[4];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) sc[e] = v[it][e] * s;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            hi2[e] = pack_h2(sc[2 * e], sc[2 * e + 1]);
+            const __half2 hh = *reinterpret_cast<const __half2*>(&hi2[e]);
+            const float2 back = __half22float2(hh);
+            lo[2 * e] = sc[2 * e] - back.x;
+            lo[2 * e + 1] = sc[2 * e + 1] - back.y;
+            lo2[e] = pack_h2(lo[2 * e], lo[2 * e + 1]);
+          }
+          *reinterpret_cast<uint4*>(r0 + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+          *reinterpret_cast<uint4*>(r0 + 16384 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      if (tid == 0) {
+        const uint32_t sb = smem_u32(r0);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const uint32_t gk = ch * 4 + ks;              // K step over x
+          const uint64_t bh = umma_desc(sb + ks * 4096, 128, 256);
+          const uint64_t bl = umma_desc(sb + 16384 + ks * 4096, 128, 256);
+          mma_f16_ts(d_tm, tm + gk * 8, bh, idesc, (ch | ks) != 0);
+          mma_f16_ts(d_tm, tm + 64 + gk * 8, bh, idesc, 1);
+          mma_f16_ts(d_tm, tm + gk * 8, bl, idesc, 1);
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&mbar)));
+      }
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    asm volatile("tcgen05.fence::after_thread_sync;");
+
+    // ------------------------------------------------ drain D -> T planes [c][y]
+    {
+      const int quarter = warp & 3, part = warp >> 2;
+      const int n = quarter * 32 + lane, c = n & 63;
+      float* plane = (n < 64 ? planeRe : planeIm) + c * kZP;
+      const int y_begin = part * 48, y_end = part == 2 ? 128 : y_begin + 48;
+#pragma unroll 1
+      for (int y0 = y_begin; y0 < y_end; y0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(d_tm + ((uint32_t)(quarter * 32) << 16) + y0, r);
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (c < WW) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4*>(plane + y0 + j) =
+                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                            __uint_as_float(r[j + 3]));
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+
+    // --------------------------------------------------------- column pass
+    float2 o0[8], o1[8];
+    const int c = grp;
+    const bool active = c < WW;
+    if ((warp * 4) < WW) {   // warp-uniform: at least one active group in this warp
+      float2 z[16];
+      if (active) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = make_float2(planeRe[c * kZP + t + 8 * j], planeIm[c * kZP + t + 8 * j]);
+        fft128_stage1(z, t, twt);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) z[j] = make_float2(0.f, 0.f);
+      }
+      fft128_stage2(z, 0, xg, t, o0);
+      fft128_stage2(z, 1, xg, t, o1);
+    }
+    __syncthreads();   // every T plane read: region0 now hosts W (column-major)
+    float2* Wt = reinterpret_cast<float2*>(r0);
+    if (active) {
+      const int rlo = ft.crange[2 * c], rhi = ft.crange[2 * c + 1];
+#pragma unroll
+      for (int k2 = 0; k2 < 8; ++k2) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = (t + 8 * h + 16 * k2 - kys) & 127;
+          if (r < WH) {
+            float2 val = make_float2(0.f, 0.f);
+            if (r >= rlo && r <= rhi) val = cmul(h ? o1[k2] : o0[k2], s_py[r]);
+            Wt[c * WH + r] = val;
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ------------------------------------------------ IFFT (along y, then along x)
+    float2* T = xbuf;
+    float2* F = reinterpret_cast<float2*>(r0);
+    ct_stage<6, WH, 1, WW, WH, 1, true>(Wt, T, twh);
+    __syncthreads();
+    ct_stage<7, WH, 6, WW, WH, 1, true>(T, F, twh);
+    __syncthreads();
+    ct_stage<6, WW, 1, WH, 1, WH, true>(F, T, tww);
+    __syncthreads();
+    // ------------------------------------------- removal phase, peak, int16
+    float2 bc = make_float2(1.f, 0.f);
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc, inv_s);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    __syncthreads();   // redf reuse
+    if (lane == 0) redf[warp] = lmax;
+    __syncthreads();
+    lmax = redf[0];
+#pragma unroll
+    for (int j = 1; j < kTcThreads / 32; ++j) lmax = fmaxf(lmax, redf[j]);
+    if (p.raw)
+      for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = F[i];
+    const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
+    int16_t* fro = p.fr + (size_t)item * WH * WW;
+    int16_t* fio = p.fi + (size_t)item * WH * WW;
+    for (int i = tid; i < WH * WW / 2; i += blockDim.x) {
+      const float4 vv = reinterpret_cast<const float4*>(F)[i];
+      const int ra = __float2int_rn(__fmul_rn(vv.x, scale)), ia = __float2int_rn(__fmul_rn(vv.y, scale));
+      const int rb = __float2int_rn(__fmul_rn(vv.z, scale)), ib = __float2int_rn(__fmul_rn(vv.w, scale));
+      reinterpret_cast<int*>(fro)[i] = (ra & 0xffff) | (rb << 16);
+      reinterpret_cast<int*>(fio)[i] = (ia & 0xffff) | (ib << 16);
+      reinterpret_cast<float4*>(F)[i] = make_float4((float)ra, (float)ia, (float)rb, (float)ib);
+    }
+    if (tid == 0) p.scale[item] = scale;
+
+    // ---------------------------------------------------------- HG overlap
+    if (p.coefs && g.G > 0) {
+      const int G = g.G, GP = (G + 3) & ~3;
+      const bool keep = GP <= kTcPersistentGP;
+      float* hxT = keep ? reinterpret_cast<float*>(smem + LY::basis)
+                        : reinterpret_cast<float*>(r0 + LY::basis_stage_off);
+      float* hyT = hxT + WW * GP;
+      float2* U = xbuf;
+      if (!keep || q != staged_q) {
+        const float* hx = p.t.hx + (size_t)q * G * WW;
+        const float* hy = p.t.hy + (size_t)q * G * WH;
+        for (int i = tid; i < (GP / 4) * WW; i += blockDim.x) {
+          const int x = i % WW, m4 = 4 * (i / WW);
+          float4 hv;
+          hv.x = m4 + 0 < G ? __ldg(&hx[(m4 + 0) * WW + x]) : 0.f;
+          hv.y = m4 + 1 < G ? __ldg(&hx[(m4 + 1) * WW + x]) : 0.f;
+          hv.z = m4 + 2 < G ? __ldg(&hx[(m4 + 2) * WW + x]) : 0.f;
+          hv.w = m4 + 3 < G ? __ldg(&hx[(m4 + 3) * WW + x]) : 0.f;
+          *reinterpret_cast<float4*>(&hxT[x * GP + m4]) = hv;
+        }
+        for (int i = tid; i < (GP / 4) * WH; i += blockDim.x) {
+          const int y = i % WH, n4 = 4 * (i / WH);
+          float4 hv;
+          hv.x = n4 + 0 < G ? __ldg(&hy[(n4 + 0) * WH + y]) : 0.f;
+          hv.y = n4 + 1 < G ? __ldg(&hy[(n4 + 1) * WH + y]) : 0.f;
+          hv.z = n4 + 2 < G ? __ldg(&hy[(n4 + 2) * WH + y]) : 0.f;
+          hv.w = n4 + 3 < G ? __ldg(&hy[(n4 + 3) * WH + y]) : 0.f;
+          *reinterpret_cast<float4*>(&hyT[y * GP + n4]) = hv;
+        }
+        staged_q = keep ? q : -1;
+      }
+      __syncthreads();
+      const int GQ = GP >> 2;
+      for (int idx = tid; idx < WH * GQ; idx += blockDim.x) {
+        const int y = idx / GQ, mq = idx - y * GQ;
+        const float2* row = F + y * WW;
+        float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
+#pragma unroll 6
+        for (int x = 0; x < WW; ++x) {
+          const float2 vx = row[x];
+          const float4 hv = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+          ar.x = fmaf(vx.x, hv.x, ar.x); ai.x = fmaf(vx.y, hv.x, ai.x);
+          ar.y = fmaf(vx.x, hv.y, ar.y); ai.y = fmaf(vx.y, hv.y, ai.y);
+          ar.z = fmaf(vx.x, hv.z, ar.z); ai.z = fmaf(vx.y, hv.z, ai.z);
+          ar.w = fmaf(vx.x, hv.w, ar.w); ai.w = fmaf(vx.y, hv.w, ai.w);
+        }
+        float2* u = U + y * GP + 4 * mq;
+        u[0] = make_float2(ar.x, ai.x);
+        u[1] = make_float2(ar.y, ai.y);
+        u[2] = make_float2(ar.z, ai.z);
+        u[3] = make_float2(ar.w, ai.w);
+      }
+      __syncthreads();
+      const float d = __fdiv_rn(g.dxdy[q], scale);
+      float2* out = p.coefs + (size_t)item * g.M;
+      for (int i = tid; i < g.M; i += blockDim.x) {
+        const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+        float ax = 0.f, ay = 0.f;
+#pragma unroll 6
+        for (int y = 0; y < WH; ++y) {
+          const float2 uv = U[y * GP + m];
+          const float hv = hyT[y * GP + n];
+          ax = fmaf(uv.x, hv, ax);
+          ay = fmaf(uv.y, hv, ay);
+        }
+        out[i] = make_float2(ax * d, ay * d);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+}
+
+bool tc_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
+                  const void* windows) {
+  return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 && g.L == 1 &&
+         g.G <= TcLayout<42, 42>::GMAX && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
+         (flags & 1u) == 0 && windows == nullptr;
+}
+
+cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
+  using LY = TcLayout<42, 42>;
+  const int GP = (p.g.G + 3) & ~3;
+  size_t bytes = LY::basis + ((p.coefs && p.g.G > 0 && GP <= kTcPersistentGP)
+                                  ? (size_t)(42 + 42) * GP * sizeof(float) : 0) + 64;
+  // at most two CTAs per SM: each holds 256 of the SM's 512 TMEM columns
+  bytes = std::max(bytes, (size_t)80 * 1024);
+  static size_t configured = 0;
+  if (bytes > configured) {
+    cudaError_t e = cudaFuncSetAttribute(fast128tc_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e != cudaSuccess) return e;
+    configured = bytes;
+  }
+  const int items = p.B * p.g.P;
+  const int grid = std::max(1, std::min(items, num_sms * 2));
+  fast128tc_kernel<42, 42><<<grid, kTcThreads, bytes, s>>>(p, ft);
+  return cudaGetLastError();
+}
+
+}  // namespace holo

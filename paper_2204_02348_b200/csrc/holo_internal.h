@@ -31,6 +31,14 @@ struct DevTables {
   const int16_t* mode_n;  // [M]
 };
 
+// Tables of the specialised 128-window kernels (holo_fast.cu, holo_fast_tc.cu).
+struct FastTables {
+  const float2* px;        // [P][L][WW] recentring phase along x
+  const float2* py;        // [P][L][WH] recentring phase along y
+  const int16_t* crange;   // [WW][2] first/last row inside the circular mask, per column
+  const uint32_t* a_tc;    // [P][2][128][64] f16x2: row-DFT matrix (hi, lo) for wavelength 0
+};
+
 struct Geometry {
   int W, H, P;
   int nx, ny, wh, ww, gh, gw;

@@ -149,3 +149,20 @@ def test_window_upload_from_host_matches_device_source():
     eng.source.set_float32(torch.from_numpy(frames).cuda())
     eng.process_fft()
     assert np.array_equal(plane_host, eng.get_fourier_plane_full()[0])
+
+
+@pytest.mark.parametrize("name", ["pr1", "dualpol", "largebasis", "dualpol_cal"])
+def test_tensor_core_row_dft_matches_simt_fft(name):
+    """tcgen05 row DFT (fp16 split operands) vs the register FFT path: same fields/coefs."""
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.run_pipeline(0)
+    tc = [t.cpu().numpy().copy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy().copy()]
+    eng.force_simt = True
+    eng.run_pipeline(0)
+    simt = [t.cpu().numpy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()]
+    assert np.abs(tc[0].astype(int) - simt[0]).max() <= 2 and np.abs(tc[1].astype(int) - simt[1]).max() <= 2
+    assert np.allclose(tc[2], simt[2], rtol=1e-5)
+    assert rel_l2_rows(tc[3], simt[3]) <= 2e-5
+    ef = rel_l2_rows(dequant(tc[0], tc[1], tc[2]), dequant(g["fr"], g["fi"], g["scale"]))
+    assert ef <= FIELD_TOL
