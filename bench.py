@@ -208,6 +208,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tc", action="store_true", help="use the tcgen05 row-pass kernel (HPG_FLAG_TC)")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture")
     args = ap.parse_args()
@@ -228,6 +229,7 @@ def main():
 
     h = api.create_handle()
     eng = api.engine(h)
+    eng.use_tc = args.tc
     for k, v in cfg.items():
         setattr(eng.config, k, v)
     frames_dev = torch.from_numpy(frames_host).to(dev)
@@ -321,7 +323,7 @@ def main():
                        "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": args.traffic_bytes,
-                         "kernel": "holo::fast128_kernel<42,42>", "bytes_per_frame": bpf,
+                         "kernel": "holo::fast128tc_kernel<42,42>" if args.tc else "holo::fast128_kernel<42,42>", "bytes_per_frame": bpf,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -588,7 +588,7 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
   if ((rp.lay.slab_bytes > 0 || (flags & HPG_FLAG_SUMMARY)) && (!o->workspace || (int64_t)o->workspace_bytes < need))
     return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
   cudaError_t e;
-  if (!(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
+  if ((flags & HPG_FLAG_TC) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
       tc_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows))
     e = launch_fast_tc(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
   else if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&

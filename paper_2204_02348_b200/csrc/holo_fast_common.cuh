@@ -19,9 +19,11 @@ template <int ZS> HOLO_DEV int w_addr(int i) { return (i >> 6) * ZS + (i & 63); 
 // in holo_fft.cuh); element e of sequence q at q*SS + e*ES.  MAPPED: the source
 // is W inside zs (w_addr).
 template <int P, int N, int L, int COUNT, int SS, int ES, bool INV, int MAPPED_ZS = 0>
-HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw) {
+HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw, int tid0 = -1,
+                       int nthr = -1) {
   constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
-  for (int task = threadIdx.x; task < total; task += blockDim.x) {
+  if (tid0 < 0) { tid0 = threadIdx.x; nthr = blockDim.x; }
+  for (int task = tid0; task < total; task += nthr) {
     int q, r;
     if (SS == 1) { q = task % COUNT; r = task / COUNT; }
     else { q = task / per; r = task - q * per; }
@@ -49,11 +51,13 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
 // |Re|,|Im| for the int16 scale.
 template <int P, int N, int L, int COUNT>
 HOLO_DEV float ct_stage_final_rows(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw,
-                                   const float2* ey, const float2* ex, bool use_bc, float2 bc, float osc = 1.f) {
+                                   const float2* ey, const float2* ex, bool use_bc, float2 bc, float osc = 1.f,
+                                   int tid0 = -1, int nthr = -1) {
   constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
   static_assert(mp == 1, "final stage");
   float lmax = 0.f;
-  for (int task = threadIdx.x; task < total; task += blockDim.x) {
+  if (tid0 < 0) { tid0 = threadIdx.x; nthr = blockDim.x; }
+  for (int task = tid0; task < total; task += nthr) {
     const int y = task % COUNT, k = task / COUNT;
     float2 v[P];
 #pragma unroll

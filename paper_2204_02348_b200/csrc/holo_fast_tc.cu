@@ -33,8 +33,7 @@ namespace holo {
 
 namespace {
 
-constexpr int kTcThreads = 384;
-constexpr int kTcGroups = kTcThreads / 8;
+constexpr int kTcGroups = 48;   // consumer 8-thread groups
 constexpr int kZP = 136;  // T plane row pitch (floats)
 
 HOLO_DEV uint32_t smem_u32(const void* ptr) { return static_cast<uint32_t>(__cvta_generic_to_shared(ptr)); }
@@ -91,34 +90,52 @@ template <int WH, int WW>
 struct TcLayout {
   static constexpr int XG = 72;        // 8x8 exchange tile per 8-thread group (float2)
   static constexpr int GMAX = 48;
-  static constexpr size_t planes_bytes = 2 * (size_t)WW * kZP * sizeof(float);     // Re/Im of T[c][y]
-  static constexpr size_t stage_bytes = 2 * 4 * 4096;                               // f hi/lo, 4 K-steps
-  static constexpr size_t region0 = ((planes_bytes > stage_bytes ? planes_bytes : stage_bytes) + 1023) & ~size_t(1023);
-  static constexpr size_t xbuf = region0;                                           // [48][XG]
+  static constexpr size_t stage = 0;                                                // f hi | lo, 8 K-steps
+  static constexpr size_t stage_bytes = 2 * 8 * 4096;
+  static constexpr size_t r0 = stage + stage_bytes;                                 // T planes / W / F / basis
+  static constexpr size_t planes_bytes = 2 * (size_t)WW * kZP * sizeof(float);
+  static constexpr size_t xbuf = (r0 + planes_bytes + 255) & ~size_t(255);          // [48][XG]
   static constexpr size_t twt = xbuf + kTcGroups * XG * sizeof(float2);             // [128]
   static constexpr size_t twh = twt + 128 * sizeof(float2);
   static constexpr size_t tww = twh + WH * sizeof(float2);
   static constexpr size_t ph = tww + WW * sizeof(float2);                           // py[WH] ex[WW] ey[WH]
-  static constexpr size_t basis = (ph + (2 * WH + WW) * sizeof(float2) + 15) & ~size_t(15);
-  static constexpr size_t basis_stage_off = ((WH * WW * sizeof(float2)) + 255) & ~size_t(255);  // in region0
-  static_assert(WH * WW * sizeof(float2) <= planes_bytes, "W / F must fit region0");
-  static_assert(basis_stage_off + (WH + WW) * GMAX * sizeof(float) <= region0, "basis staging must fit region0");
+  static constexpr size_t invs = (ph + (2 * WH + WW) * sizeof(float2) + 15) & ~size_t(15);   // [2][128]
+  static constexpr size_t basis = invs + 2 * 128 * sizeof(float);
+  static constexpr size_t basis_stage_off = ((WH * WW * sizeof(float2)) + 255) & ~size_t(255);  // in r0
+  static_assert(WH * WW * sizeof(float2) <= planes_bytes, "W / F must fit r0");
+  static_assert(basis_stage_off + (WH + WW) * GMAX * sizeof(float) <= planes_bytes, "basis staging must fit r0");
   static_assert(WH * WW * sizeof(float2) <= kTcGroups * XG * sizeof(float2), "IFFT ping-pong must fit xbuf");
   static_assert(WH * GMAX * sizeof(float2) <= kTcGroups * XG * sizeof(float2), "overlap U must fit xbuf");
   static_assert(WW <= 64 && WW <= kTcGroups, "one column round");
 };
 
-constexpr int kTcPersistentGP = 36;
+constexpr int kTcPersistentGP = 48;
+constexpr int kProd = 128;           // producer threads (warps 0-3)
+constexpr int kCons = 384;           // consumer threads (warps 4-15)
+constexpr int kBarCons = 1, kBarProd = 2;
 
+HOLO_DEV void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+HOLO_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Warp-specialised, software-pipelined over the CTA's windows k = 0, 1, ...:
+//   producer (warps 0-3): window k -> registers (per-row power-of-two scale) ->
+//     fp16 hi/lo in the canonical K-major layout -> 24 tcgen05.mma into
+//     accumulator D[k & 1] -> commit (mbarrier fullD[k & 1])
+//   consumer (warps 4-15): drain D[k & 1] (x 1/scale per row) -> release
+//     (emptyD[k & 1]) -> column FFTs, IFFT, removal, int16, overlap
+// so the tensor core, the HBM reads and the SIMT tail of consecutive windows overlap.
 template <int WH, int WW>
-__global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_constant__ RunParams p,
-                                                                 const __grid_constant__ FastTables ft) {
+__global__ void __launch_bounds__(kProd + kCons, 1) fast128tc_kernel(const __grid_constant__ RunParams p,
+                                                                    const __grid_constant__ FastTables ft) {
   using LY = TcLayout<WH, WW>;
   extern __shared__ __align__(1024) char smem[];
-  __shared__ float redf[kTcThreads / 32];
-  __shared__ __align__(8) uint64_t mbar;
+  __shared__ float redf[16];
+  __shared__ __align__(8) uint64_t fullD[2], emptyD[2], invsB[2];
   __shared__ uint32_t tbase;
-  char* r0 = smem;                                       // stage / T planes / W / F / basis staging
+  char* stage = smem + LY::stage;
+  char* r0 = smem + LY::r0;
   float* planeRe = reinterpret_cast<float*>(r0);
   float* planeIm = planeRe + WW * kZP;
   float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
@@ -128,46 +145,89 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
   float2* s_py = reinterpret_cast<float2*>(smem + LY::ph);
   float2* s_ex = s_py + WH;
   float2* s_ey = s_ex + WW;
+  float* invs = reinterpret_cast<float*>(smem + LY::invs);
   const Geometry& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int t = tid & 7, grp = tid >> 3;
-  float2* xg = xbuf + grp * LY::XG;
+  const int G = g.G, GP = (G + 3) & ~3;
+  const bool keep_basis = p.coefs && G > 0 && GP <= kTcPersistentGP;
+  float* hxP = reinterpret_cast<float*>(smem + LY::basis);   // [P][WW][GP] when kept
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    for (int i = 0; i < 2; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&fullD[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&emptyD[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&invsB[i])));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   for (int i = tid; i < 128; i += blockDim.x) twt[i] = p.t.tw_nx[((i >> 3) * (i & 7)) & 127];
   for (int i = tid; i < WH; i += blockDim.x) twh[i] = p.t.tw_gh[i];
   for (int i = tid; i < WW; i += blockDim.x) tww[i] = p.t.tw_gw[i];
+  if (keep_basis) {   // every pol's basis, transposed [x][m] / [y][n], for the CTA's lifetime
+    for (int i = tid; i < g.P * (GP / 4) * WW; i += blockDim.x) {
+      const int q = i / ((GP / 4) * WW), r = i - q * (GP / 4) * WW, x = r % WW, m4 = 4 * (r / WW);
+      const float* hx = p.t.hx + (size_t)q * G * WW;
+      float4 hv;
+      hv.x = m4 + 0 < G ? __ldg(&hx[(m4 + 0) * WW + x]) : 0.f;
+      hv.y = m4 + 1 < G ? __ldg(&hx[(m4 + 1) * WW + x]) : 0.f;
+      hv.z = m4 + 2 < G ? __ldg(&hx[(m4 + 2) * WW + x]) : 0.f;
+      hv.w = m4 + 3 < G ? __ldg(&hx[(m4 + 3) * WW + x]) : 0.f;
+      *reinterpret_cast<float4*>(&hxP[(q * (WW + WH) + x) * GP + m4]) = hv;
+    }
+    for (int i = tid; i < g.P * (GP / 4) * WH; i += blockDim.x) {
+      const int q = i / ((GP / 4) * WH), r = i - q * (GP / 4) * WH, y = r % WH, n4 = 4 * (r / WH);
+      const float* hy = p.t.hy + (size_t)q * G * WH;
+      float4 hv;
+      hv.x = n4 + 0 < G ? __ldg(&hy[(n4 + 0) * WH + y]) : 0.f;
+      hv.y = n4 + 1 < G ? __ldg(&hy[(n4 + 1) * WH + y]) : 0.f;
+      hv.z = n4 + 2 < G ? __ldg(&hy[(n4 + 2) * WH + y]) : 0.f;
+      hv.w = n4 + 3 < G ? __ldg(&hy[(n4 + 3) * WH + y]) : 0.f;
+      *reinterpret_cast<float4*>(&hxP[(q * (WW + WH) + WW + y) * GP + n4]) = hv;
+    }
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
-  const uint32_t tm = tbase;                  // A hi [0,64) lo [64,128), D [128,256)
-  const uint32_t d_tm = tm + 128;
-  // instruction descriptor: F16 x F16 -> F32, K-major A and B, N = 128, M = 128
-  const uint32_t idesc = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-  uint32_t phase = 0;
-  int loaded_q = -1, staged_q = -1;
+  const uint32_t tm = tbase;   // A hi [0,64) lo [64,128); D0 [128,256); D1 [256,384)
   const int items = p.B * g.P;
   const int W = g.W, H = g.H;
 
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int b = item / g.P, q = item - b * g.P;
-    const int kys = (g.k0[q][0][1] - WH / 2) & 127;
-    __syncthreads();  // previous item done with every buffer
-    for (int i = tid; i < WH; i += blockDim.x) {
-      s_py[i] = ft.py[q * WH + i];
-      s_ey[i] = p.t.rem_y[q * WH + i];
-    }
-    for (int i = tid; i < WW; i += blockDim.x) s_ex[i] = p.t.rem_x[q * WW + i];
-    if (q != loaded_q) {
-      // row-DFT matrix of this pol into TMEM lanes 0..127, columns [0,128)
-      if (warp < 4) {
+  if (warp < 4) {
+    // ================================= producer =================================
+    const uint32_t idesc = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const int seg = tid & 3, rs = tid >> 2;   // 4 threads per row, 32 x each
+    int loaded_q = -1;
+    int k = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++k) {
+      const int s = k & 1;
+      const int b = item / g.P, q = item - b * g.P;
+      const int row0 = g.row0[q], col0 = g.col0[q];
+      {   // warm L2 with the next window of this CTA
+        const int nitem = item + gridDim.x;
+        if (nitem < items) {
+          const int nb = nitem / g.P, nq = nitem - nb * g.P;
+          const int es = p.fmt == 0 ? 4 : 2;
+          const char* base = reinterpret_cast<const char*>(p.frames) +
+                             ((int64_t)nb * W * H + (int64_t)g.row0[nq] * W + g.col0[nq]) * es;
+          for (int i = tid; i < 128 * 5; i += kProd) {
+            const int row = i / 5, part = i - row * 5;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)row * W * es + min(part * 128, 128 * es - 1)));
+          }
+        }
+      }
+      if (k >= 1) {   // previous window's MMAs finished: stage buffer and A are free
+        mbar_wait(&fullD[(k - 1) & 1], ((k - 1) >> 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
+      if (k >= 2) {   // the consumer drained D[s] (and read invs[s]) two windows ago
+        mbar_wait(&emptyD[s], ((k >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
+      if (q != loaded_q) {
         const uint32_t* src = ft.a_tc + ((size_t)q * 2 * 128 + warp * 32 + lane) * 64;
         uint32_t r[32];
 #pragma unroll
@@ -181,135 +241,137 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
           }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;");
+        loaded_q = q;
       }
-      loaded_q = q;
-    }
-
-    // ------------------------------------------------ window -> registers, peak
-    const int row0 = g.row0[q], col0 = g.col0[q];
-    float v[6][8];
-    float amax = 0.f;
+#pragma unroll 1
+      for (int rp = 0; rp < 2; ++rp) {   // two rows per thread per pass, loads in flight together
+        float v[2][32];
 #pragma unroll
-    for (int it = 0; it < 6; ++it) {
-      const int idx = it * kTcThreads + tid;
-      if (idx < 2048) {
-        const int y = idx >> 4, o = idx & 15;
-        const int64_t base = (int64_t)b * W * H + (int64_t)(row0 + y) * W + col0 + 8 * o;
-        if (p.fmt == 0) {
-          const float* src = reinterpret_cast<const float*>(p.frames) + base;
-          if ((col0 & 3) == 0) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(src));
-            const float4 c = __ldg(reinterpret_cast<const float4*>(src + 4));
-            v[it][0] = a.x; v[it][1] = a.y; v[it][2] = a.z; v[it][3] = a.w;
-            v[it][4] = c.x; v[it][5] = c.y; v[it][6] = c.z; v[it][7] = c.w;
+        for (int rr = 0; rr < 2; ++rr) {
+          const int y = rs + 32 * (2 * rp + rr);
+          const int64_t base = (int64_t)b * W * H + (int64_t)(row0 + y) * W + col0 + 32 * seg;
+          if (p.fmt == 0) {
+            const float* src = reinterpret_cast<const float*>(p.frames) + base;
+            if ((col0 & 3) == 0) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(src) + j);
+                v[rr][4 * j] = a.x; v[rr][4 * j + 1] = a.y; v[rr][4 * j + 2] = a.z; v[rr][4 * j + 3] = a.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[rr][j] = __ldg(src + j);
+            }
           } else {
+            const unsigned short* src = reinterpret_cast<const unsigned short*>(p.frames) + base;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) v[it][e] = __ldg(src + e);
+            for (int j = 0; j < 32; ++j) v[rr][j] = (float)__ldg(src + j);
           }
-        } else {
-          const unsigned short* src = reinterpret_cast<const unsigned short*>(p.frames) + base;
-#pragma unroll
-          for (int e = 0; e < 8; ++e) v[it][e] = (float)__ldg(src + e);
         }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) amax = fmaxf(amax, fabsf(v[it][e]));
-      }
-    }
+        for (int rr = 0; rr < 2; ++rr) {
+          const int y = rs + 32 * (2 * rp + rr);
+          float m = 0.f;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-    if (lane == 0) redf[warp] = amax;
-    __syncthreads();
-    amax = redf[0];
+          for (int j = 0; j < 32; ++j) m = fmaxf(m, fabsf(v[rr][j]));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+          m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+          // exact power-of-two row scale: |f| * s < 2^14, fh + fl keep 22 bits
+          int e2 = 0;
+          frexpf(m, &e2);
+          const float sc = m > 0.f ? ldexpf(1.f, 14 - e2) : 1.f;
+          if (seg == 0) invs[s * 128 + y] = m > 0.f ? ldexpf(1.f, e2 - 14) : 1.f;
 #pragma unroll
-    for (int j = 1; j < kTcThreads / 32; ++j) amax = fmaxf(amax, redf[j]);
-    // exact power-of-two scale: |f| * s < 2^14 keeps fh + fl within fp16 range with 22 bits
-    int ex2 = 0;
-    frexpf(amax, &ex2);
-    const float s = amax > 0.f ? ldexpf(1.f, 14 - ex2) : 1.f;
-    const float inv_s = amax > 0.f ? ldexpf(1.f, ex2 - 14) : 1.f;
-
-    // ------------------------------------------------ row DFT on tensor cores
-#pragma unroll 1
-    for (int ch = 0; ch < 2; ++ch) {
-      if (ch == 1) {  // chunk-0 MMAs must have finished reading the stage buffer
-        mbar_wait(&mbar, phase);
-        phase ^= 1;
-      }
+          for (int j = 0; j < 4; ++j) {          // octet j: x = 32 seg + 8 j
+            const int gk = 2 * seg + (j >> 1), kh = j & 1;
+            const uint32_t off = (uint32_t)gk * 4096 + ((uint32_t)((y >> 3) * 2 + kh) * 8 + (y & 7)) * 16;
+            uint32_t hi2[4], lo2[4];
 #pragma unroll
-      for (int it = 0; it < 6; ++it) {
-        const int idx = it * kTcThreads + tid;
-        if (idx < 2048 && ((idx >> 3) & 1) == ch) {
-          const int y = idx >> 4, ol = idx & 7;                 // octet within the chunk
-          const int kstep = ol >> 1, kh = ol & 1;
-          const uint32_t off = (uint32_t)kstep * 4096 + ((uint32_t)((y >> 3) * 2 + kh) * 8 + (y & 7)) * 16;
-          float sc[8], lo[8];
-          uint32_t hi2[4], lo2[4];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) sc[e] = v[it][e] * s;
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            hi2[e] = pack_h2(sc[2 * e], sc[2 * e + 1]);
-            const __half2 hh = *reinterpret_cast<const __half2*>(&hi2[e]);
-            const float2 back = __half22float2(hh);
-            lo[2 * e] = sc[2 * e] - back.x;
-            lo[2 * e + 1] = sc[2 * e + 1] - back.y;
-            lo2[e] = pack_h2(lo[2 * e], lo[2 * e + 1]);
+            for (int e = 0; e < 4; ++e) {
+              const float a = v[rr][8 * j + 2 * e] * sc, c = v[rr][8 * j + 2 * e + 1] * sc;
+              hi2[e] = pack_h2(a, c);
+              const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi2[e]));
+              lo2[e] = pack_h2(a - back.x, c - back.y);
+            }
+            *reinterpret_cast<uint4*>(stage + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+            *reinterpret_cast<uint4*>(stage + 32768 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
           }
-          *reinterpret_cast<uint4*>(r0 + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-          *reinterpret_cast<uint4*>(r0 + 16384 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
         }
       }
       asm volatile("fence.proxy.async.shared::cta;");
       asm volatile("tcgen05.fence::before_thread_sync;");
-      __syncthreads();
+      nbar(kBarProd, kProd);
       asm volatile("tcgen05.fence::after_thread_sync;");
       if (tid == 0) {
-        const uint32_t sb = smem_u32(r0);
+        const uint32_t d = tm + 128 + 128 * s;
+        const uint32_t sb = smem_u32(stage);
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const uint32_t gk = ch * 4 + ks;              // K step over x
-          const uint64_t bh = umma_desc(sb + ks * 4096, 128, 256);
-          const uint64_t bl = umma_desc(sb + 16384 + ks * 4096, 128, 256);
-          mma_f16_ts(d_tm, tm + gk * 8, bh, idesc, (ch | ks) != 0);
-          mma_f16_ts(d_tm, tm + 64 + gk * 8, bh, idesc, 1);
-          mma_f16_ts(d_tm, tm + gk * 8, bl, idesc, 1);
+        for (int gk = 0; gk < 8; ++gk) {
+          const uint64_t bh = umma_desc(sb + gk * 4096, 128, 256);
+          const uint64_t bl = umma_desc(sb + 32768 + gk * 4096, 128, 256);
+          mma_f16_ts(d, tm + gk * 8, bh, idesc, gk != 0);
+          mma_f16_ts(d, tm + 64 + gk * 8, bh, idesc, 1);
+          mma_f16_ts(d, tm + gk * 8, bl, idesc, 1);
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&mbar)));
+            smem_u32(&fullD[s])));
+        mbar_arrive(&invsB[s]);
       }
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
+  } else {
+
+  // ================================= consumer =================================
+  const int ct = tid - kProd, t = ct & 7, grp = ct >> 3, cw = ct >> 5;
+  float2* xg = xbuf + grp * LY::XG;
+  int staged_q = -1;
+  int k = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, ++k) {
+    const int s = k & 1;
+    const int b = item / g.P, q = item - b * g.P;
+    const int kys = (g.k0[q][0][1] - WH / 2) & 127;
+    for (int i = ct; i < WH; i += kCons) {
+      s_py[i] = ft.py[q * WH + i];
+      s_ey[i] = p.t.rem_y[q * WH + i];
+    }
+    for (int i = ct; i < WW; i += kCons) s_ex[i] = p.t.rem_x[q * WW + i];
+    mbar_wait(&fullD[s], (k >> 1) & 1);
+    mbar_wait(&invsB[s], (k >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
+    nbar(kBarCons, kCons);
 
     // ------------------------------------------------ drain D -> T planes [c][y]
     {
-      const int quarter = warp & 3, part = warp >> 2;
+      const int quarter = warp & 3, part = (warp - 4) >> 2;
       const int n = quarter * 32 + lane, c = n & 63;
       float* plane = (n < 64 ? planeRe : planeIm) + c * kZP;
+      const float* iv = invs + s * 128;
       const int y_begin = part * 48, y_end = part == 2 ? 128 : y_begin + 48;
+      const uint32_t d = tm + 128 + 128 * s;
 #pragma unroll 1
       for (int y0 = y_begin; y0 < y_end; y0 += 16) {
         uint32_t r[16];
-        tmem_ld16(d_tm + ((uint32_t)(quarter * 32) << 16) + y0, r);
+        tmem_ld16(d + ((uint32_t)(quarter * 32) << 16) + y0, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;");
         if (c < WW) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
+          for (int j = 0; j < 16; j += 4) {
+            const float4 sc = *reinterpret_cast<const float4*>(iv + y0 + j);
             *reinterpret_cast<float4*>(plane + y0 + j) =
-                make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                            __uint_as_float(r[j + 3]));
+                make_float4(__uint_as_float(r[j]) * sc.x, __uint_as_float(r[j + 1]) * sc.y,
+                            __uint_as_float(r[j + 2]) * sc.z, __uint_as_float(r[j + 3]) * sc.w);
+          }
         }
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
-    __syncthreads();
+    nbar(kBarCons, kCons);
+    if (ct == 0) mbar_arrive(&emptyD[s]);
 
     // --------------------------------------------------------- column pass
     float2 o0[8], o1[8];
     const int c = grp;
     const bool active = c < WW;
-    if ((warp * 4) < WW) {   // warp-uniform: at least one active group in this warp
+    if ((cw * 4) < WW) {
       float2 z[16];
       if (active) {
 #pragma unroll
@@ -322,7 +384,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
       fft128_stage2(z, 0, xg, t, o0);
       fft128_stage2(z, 1, xg, t, o1);
     }
-    __syncthreads();   // every T plane read: region0 now hosts W (column-major)
+    nbar(kBarCons, kCons);   // every T plane read: r0 now hosts W (column-major)
     float2* Wt = reinterpret_cast<float2*>(r0);
     if (active) {
       const int rlo = ft.crange[2 * c], rhi = ft.crange[2 * c + 1];
@@ -339,35 +401,34 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
         }
       }
     }
-    __syncthreads();
+    nbar(kBarCons, kCons);
 
     // ------------------------------------------------ IFFT (along y, then along x)
     float2* T = xbuf;
     float2* F = reinterpret_cast<float2*>(r0);
-    ct_stage<6, WH, 1, WW, WH, 1, true>(Wt, T, twh);
-    __syncthreads();
-    ct_stage<7, WH, 6, WW, WH, 1, true>(T, F, twh);
-    __syncthreads();
-    ct_stage<6, WW, 1, WH, 1, WH, true>(F, T, tww);
-    __syncthreads();
+    ct_stage<6, WH, 1, WW, WH, 1, true>(Wt, T, twh, ct, kCons);
+    nbar(kBarCons, kCons);
+    ct_stage<7, WH, 6, WW, WH, 1, true>(T, F, twh, ct, kCons);
+    nbar(kBarCons, kCons);
+    ct_stage<6, WW, 1, WH, 1, WH, true>(F, T, tww, ct, kCons);
+    nbar(kBarCons, kCons);
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
-    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc, inv_s);
+    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc, 1.f, ct, kCons);
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    __syncthreads();   // redf reuse
-    if (lane == 0) redf[warp] = lmax;
-    __syncthreads();
+    if (lane == 0) redf[cw] = lmax;
+    nbar(kBarCons, kCons);
     lmax = redf[0];
 #pragma unroll
-    for (int j = 1; j < kTcThreads / 32; ++j) lmax = fmaxf(lmax, redf[j]);
+    for (int j = 1; j < kCons / 32; ++j) lmax = fmaxf(lmax, redf[j]);
     if (p.raw)
-      for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = F[i];
+      for (int i = ct; i < WH * WW; i += kCons) p.raw[(size_t)item * WH * WW + i] = F[i];
     const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
     int16_t* fro = p.fr + (size_t)item * WH * WW;
     int16_t* fio = p.fi + (size_t)item * WH * WW;
-    for (int i = tid; i < WH * WW / 2; i += blockDim.x) {
+    for (int i = ct; i < WH * WW / 2; i += kCons) {
       const float4 vv = reinterpret_cast<const float4*>(F)[i];
       const int ra = __float2int_rn(__fmul_rn(vv.x, scale)), ia = __float2int_rn(__fmul_rn(vv.y, scale));
       const int rb = __float2int_rn(__fmul_rn(vv.z, scale)), ib = __float2int_rn(__fmul_rn(vv.w, scale));
@@ -375,42 +436,45 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
       reinterpret_cast<int*>(fio)[i] = (ia & 0xffff) | (ib << 16);
       reinterpret_cast<float4*>(F)[i] = make_float4((float)ra, (float)ia, (float)rb, (float)ib);
     }
-    if (tid == 0) p.scale[item] = scale;
+    if (ct == 0) p.scale[item] = scale;
 
     // ---------------------------------------------------------- HG overlap
-    if (p.coefs && g.G > 0) {
-      const int G = g.G, GP = (G + 3) & ~3;
-      const bool keep = GP <= kTcPersistentGP;
-      float* hxT = keep ? reinterpret_cast<float*>(smem + LY::basis)
-                        : reinterpret_cast<float*>(r0 + LY::basis_stage_off);
-      float* hyT = hxT + WW * GP;
-      float2* U = xbuf;
-      if (!keep || q != staged_q) {
-        const float* hx = p.t.hx + (size_t)q * G * WW;
-        const float* hy = p.t.hy + (size_t)q * G * WH;
-        for (int i = tid; i < (GP / 4) * WW; i += blockDim.x) {
-          const int x = i % WW, m4 = 4 * (i / WW);
-          float4 hv;
-          hv.x = m4 + 0 < G ? __ldg(&hx[(m4 + 0) * WW + x]) : 0.f;
-          hv.y = m4 + 1 < G ? __ldg(&hx[(m4 + 1) * WW + x]) : 0.f;
-          hv.z = m4 + 2 < G ? __ldg(&hx[(m4 + 2) * WW + x]) : 0.f;
-          hv.w = m4 + 3 < G ? __ldg(&hx[(m4 + 3) * WW + x]) : 0.f;
-          *reinterpret_cast<float4*>(&hxT[x * GP + m4]) = hv;
+    if (p.coefs && G > 0) {
+      float* hxT;
+      float* hyT;
+      if (keep_basis) {
+        hxT = hxP + (size_t)q * (WW + WH) * GP;
+        hyT = hxT + WW * GP;
+      } else {
+        hxT = reinterpret_cast<float*>(r0 + LY::basis_stage_off);
+        hyT = hxT + WW * GP;
+        if (q != staged_q) {
+          const float* hx = p.t.hx + (size_t)q * G * WW;
+          const float* hy = p.t.hy + (size_t)q * G * WH;
+          for (int i = ct; i < (GP / 4) * WW; i += kCons) {
+            const int x = i % WW, m4 = 4 * (i / WW);
+            float4 hv;
+            hv.x = m4 + 0 < G ? __ldg(&hx[(m4 + 0) * WW + x]) : 0.f;
+            hv.y = m4 + 1 < G ? __ldg(&hx[(m4 + 1) * WW + x]) : 0.f;
+            hv.z = m4 + 2 < G ? __ldg(&hx[(m4 + 2) * WW + x]) : 0.f;
+            hv.w = m4 + 3 < G ? __ldg(&hx[(m4 + 3) * WW + x]) : 0.f;
+            *reinterpret_cast<float4*>(&hxT[x * GP + m4]) = hv;
+          }
+          for (int i = ct; i < (GP / 4) * WH; i += kCons) {
+            const int y = i % WH, n4 = 4 * (i / WH);
+            float4 hv;
+            hv.x = n4 + 0 < G ? __ldg(&hy[(n4 + 0) * WH + y]) : 0.f;
+            hv.y = n4 + 1 < G ? __ldg(&hy[(n4 + 1) * WH + y]) : 0.f;
+            hv.z = n4 + 2 < G ? __ldg(&hy[(n4 + 2) * WH + y]) : 0.f;
+            hv.w = n4 + 3 < G ? __ldg(&hy[(n4 + 3) * WH + y]) : 0.f;
+            *reinterpret_cast<float4*>(&hyT[y * GP + n4]) = hv;
+          }
         }
-        for (int i = tid; i < (GP / 4) * WH; i += blockDim.x) {
-          const int y = i % WH, n4 = 4 * (i / WH);
-          float4 hv;
-          hv.x = n4 + 0 < G ? __ldg(&hy[(n4 + 0) * WH + y]) : 0.f;
-          hv.y = n4 + 1 < G ? __ldg(&hy[(n4 + 1) * WH + y]) : 0.f;
-          hv.z = n4 + 2 < G ? __ldg(&hy[(n4 + 2) * WH + y]) : 0.f;
-          hv.w = n4 + 3 < G ? __ldg(&hy[(n4 + 3) * WH + y]) : 0.f;
-          *reinterpret_cast<float4*>(&hyT[y * GP + n4]) = hv;
-        }
-        staged_q = keep ? q : -1;
       }
-      __syncthreads();
+      nbar(kBarCons, kCons);
+      float2* U = xbuf;
       const int GQ = GP >> 2;
-      for (int idx = tid; idx < WH * GQ; idx += blockDim.x) {
+      for (int idx = ct; idx < WH * GQ; idx += kCons) {
         const int y = idx / GQ, mq = idx - y * GQ;
         const float2* row = F + y * WW;
         float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
@@ -429,10 +493,10 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
         u[2] = make_float2(ar.z, ai.z);
         u[3] = make_float2(ar.w, ai.w);
       }
-      __syncthreads();
-      const float d = __fdiv_rn(g.dxdy[q], scale);
+      nbar(kBarCons, kCons);
+      const float dd = __fdiv_rn(g.dxdy[q], scale);
       float2* out = p.coefs + (size_t)item * g.M;
-      for (int i = tid; i < g.M; i += blockDim.x) {
+      for (int i = ct; i < g.M; i += kCons) {
         const int m = p.t.mode_m[i], n = p.t.mode_n[i];
         float ax = 0.f, ay = 0.f;
 #pragma unroll 6
@@ -442,13 +506,18 @@ __global__ void __launch_bounds__(kTcThreads, 2) fast128tc_kernel(const __grid_c
           ax = fmaf(uv.x, hv, ax);
           ay = fmaf(uv.y, hv, ay);
         }
-        out[i] = make_float2(ax * d, ay * d);
+        out[i] = make_float2(ax * dd, ay * dd);
       }
+      staged_q = keep_basis ? -1 : q;
     }
+    nbar(kBarCons, kCons);   // window done: r0, xbuf and the per-window tables may be reused
   }
+  }
+  // every accumulator was drained by the consumer: the allocating warp frees TMEM
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tm));
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
 }
 
 bool tc_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
@@ -462,9 +531,9 @@ cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms
   using LY = TcLayout<42, 42>;
   const int GP = (p.g.G + 3) & ~3;
   size_t bytes = LY::basis + ((p.coefs && p.g.G > 0 && GP <= kTcPersistentGP)
-                                  ? (size_t)(42 + 42) * GP * sizeof(float) : 0) + 64;
-  // at most two CTAs per SM: each holds 256 of the SM's 512 TMEM columns
-  bytes = std::max(bytes, (size_t)80 * 1024);
+                                  ? (size_t)p.g.P * (42 + 42) * GP * sizeof(float) : 0) + 64;
+  // one CTA per SM: it owns all 512 TMEM columns
+  bytes = std::max(bytes, (size_t)120 * 1024);
   static size_t configured = 0;
   if (bytes > configured) {
     cudaError_t e = cudaFuncSetAttribute(fast128tc_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -473,8 +542,8 @@ cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms
     configured = bytes;
   }
   const int items = p.B * p.g.P;
-  const int grid = std::max(1, std::min(items, num_sms * 2));
-  fast128tc_kernel<42, 42><<<grid, kTcThreads, bytes, s>>>(p, ft);
+  const int grid = std::max(1, std::min(items, num_sms));
+  fast128tc_kernel<42, 42><<<grid, kProd + kCons, bytes, s>>>(p, ft);
   return cudaGetLastError();
 }
 

@@ -93,6 +93,7 @@ class Engine:
         self._device = device
         self.force_generic = False      # diagnostic: bypass the specialised kernels
         self.force_simt = False         # diagnostic: specialised kernel without tensor cores
+        self.use_tc = False             # tcgen05 row-pass kernel (HPG_FLAG_TC)
         self.last_h2d_bytes = 0
         self._plans = collections.OrderedDict()
         self._bufs = {}
@@ -414,7 +415,7 @@ class Engine:
         L.sc = self._buf("scale", (B, P), torch.float32)
         L.coefs = self._buf("coefs", (B, P * plan.mode_count), torch.complex64) if (with_coefs and G > 0) else None
         L.flags = ((native.HPG_FLAG_SUMMARY if summary else 0) | (native.HPG_FLAG_GENERIC if self.force_generic else 0)
-                   | (native.HPG_FLAG_SIMT if self.force_simt else 0))
+                   | (native.HPG_FLAG_SIMT if self.force_simt else 0) | (native.HPG_FLAG_TC if self.use_tc else 0))
         L.params = L.inten = None
         slots = B * A + 1
         if summary:

@@ -23,6 +23,7 @@ c_int32, c_int64, c_double, c_void_p, c_size_t = (ctypes.c_int32, ctypes.c_int64
 HPG_FLAG_SUMMARY = 1
 HPG_FLAG_GENERIC = 2
 HPG_FLAG_SIMT = 4
+HPG_FLAG_TC = 8
 
 # Every symbol include/holo_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [

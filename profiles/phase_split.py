@@ -1,7 +1,7 @@
 """Per-phase instruction / stall-sample split of an ncu report of fast128_kernel.
 
 usage: ncu -i X.ncu-rep --page source --csv --print-source cuda,sass > src.csv
-       python profiles/phase_split.py src.csv ITEMS
+       python profiles/phase_split.py src.csv ITEMS [KERNEL_SOURCE_PATH]
 SASS instructions are sorted by address and assigned to the phase of the
 nearest preceding holo_fast.cu source line (inlined FFT helpers inherit it).
 """
@@ -11,10 +11,10 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 items = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
-src_path = rows[0][1]
+src_path = sys.argv[3] if len(sys.argv) > 3 else rows[0][1]
 markers = {}
 for i, line in enumerate(open(src_path), 1):
-    m = re.search(r"// -+ (row pass|column pass|IFFT|removal phase|HG overlap)", line)
+    m = re.search(r"// [-=]+ (row pass|producer|consumer|drain D|column pass|IFFT|removal phase|HG overlap)", line)
     if re.search(r"__global__ void", line) and "kernel_line" not in markers.values():
         markers[i] = "setup"
         kernel_start = i

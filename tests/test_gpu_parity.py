@@ -156,9 +156,10 @@ def test_tensor_core_row_dft_matches_simt_fft(name):
     """tcgen05 row DFT (fp16 split operands) vs the register FFT path: same fields/coefs."""
     case, g, frames = load(name)
     eng = _engine(case, frames)
+    eng.use_tc = True
     eng.run_pipeline(0)
     tc = [t.cpu().numpy().copy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy().copy()]
-    eng.force_simt = True
+    eng.use_tc = False
     eng.run_pipeline(0)
     simt = [t.cpu().numpy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()]
     assert np.abs(tc[0].astype(int) - simt[0]).max() <= 2 and np.abs(tc[1].astype(int) - simt[1]).max() <= 2
