@@ -167,6 +167,13 @@ int hpg_plane_summary(const void* data, int64_t count, int32_t P, int32_t h, int
 int hpg_field_intensity(const int16_t* field_r, const int16_t* field_i, const float* field_scale,
                         int32_t batch_count, int32_t P, int32_t h, int32_t w, double* out, void* stream);
 
+/* Reference-wave calibration correction (holopipe/engine.py:276-335): from the
+ * tilt-removed, unquantised calibration fields a [n] (and b [n] or NULL, the
+ * second real part of a complex calibration, so proc = a + i b) computes
+ * applied = conj(proc) / max(|proc|^2, 1e-6) in fp64, stored complex64 [n].
+ * The fields themselves come from hpg_run(raw_fields) on the calibration frames. */
+int hpg_ref_calibration_finish(const void* a, const void* b, int64_t n, void* applied, void* stream);
+
 /* Coefficients of already-quantised fields (engine.py:353-370): fields int16
  * [B][P][gh][gw] + scale [B][P] -> coefs complex64 [B][P*M]. */
 int hpg_extract_coefs(const hpg_plan* plan, const int16_t* field_r, const int16_t* field_i,

@@ -472,12 +472,62 @@ def metrics(coefs, M, P, wl_of_row, L, pol_indep=0, conj_trans=0, groups=None):
 
 # ------------------------------------------------------------ full chain
 
-def run_chain(cfg, frames, batch_cal=None, stop_after=None):
+CAL_EPS = 1e-6   # holopipe/engine.py:332-333 (_CAL_EPS)
+
+
+def ref_calibration(cfg, kind, raw, origins, xis, lams, wh, ww, mask, xa, ya):
+    """Processed reference-wave calibration (holopipe/engine.py:276-335).
+
+    kind 1 (intensity): sqrt of the max-normalised intensity window, carrier at DC,
+    no removal phase; kind 2 (field): full complex FFT of conj(raw), window at the
+    carrier k0 (no fill-factor envelope, pipeline.py:107-111), removal phase.
+    Returns conj(proc) / max(|proc|^2, 1e-6), complex64 (Lc, P, gh, gw).
+    """
+    nx, ny, p = cfg.fftWindowSizeX, cfg.fftWindowSizeY, cfg.framePixelSize
+    P = cfg.polCount
+    tilt, defocus, _ = effective_params(cfg)
+    if kind == 1:
+        inten = np.asarray(raw, np.float32).astype(np.float64)
+    else:
+        inten = np.abs(np.asarray(raw, np.complex64).astype(np.complex128)) ** 2
+    peak = inten.max()
+    inten = np.ones_like(inten) if peak <= 0 else inten / peak     # frames.py:175-187
+    Lc = inten.shape[0]
+    out = np.empty((Lc, P, ya.size, xa.size), np.complex64)
+    for ci in range(Lc):
+        lam = lams[min(ci, len(lams) - 1)]
+        for q in range(P):
+            c0, r0 = origins[q]
+            if kind == 1:
+                amp = np.sqrt(inten[ci, r0:r0 + ny, c0:c0 + nx])
+                spec = scipy.fft.rfft2(amp[None].astype(np.float32), axes=(-2, -1)).astype(np.complex64)[0]
+                g = crop_window(spec, 0, 0, wh, ww, nx, ny, bool(cfg.fillFactorCorrectionEnabled))
+                proc = inverse_window((g * mask * centre_shift(0, 0, wh, ww, nx, ny, *xis[q]))[None],
+                                      cfg.resolutionMode, nx, ny)[0]
+            else:
+                ref = np.conj(np.asarray(raw, np.complex64)[ci, r0:r0 + ny, c0:c0 + nx])
+                spec = np.fft.fft2(ref).astype(np.complex64)
+                kx = carrier_bin(tilt[0][q], nx, p, lam)
+                ky = carrier_bin(tilt[1][q], ny, p, lam)
+                tx = np.mod(kx + np.arange(ww) - ww // 2, nx)
+                ty = np.mod(ky + np.arange(wh) - wh // 2, ny)
+                g = spec[ty[:, None], tx[None, :]].astype(np.complex64)
+                proc = inverse_window((g * mask * centre_shift(kx, ky, wh, ww, nx, ny, *xis[q]))[None],
+                                      cfg.resolutionMode, nx, ny)[0]
+                proc = proc * tilt_defocus_phase(xa, ya, tilt[0][q], tilt[1][q], defocus[q], lam, kx, ky,
+                                                 nx, ny, p, cfg.beamCentre[0][q], cfg.beamCentre[1][q])
+            mag2 = np.maximum(np.abs(proc.astype(np.complex128)) ** 2, CAL_EPS)
+            out[ci, q] = (np.conj(proc) / mag2).astype(np.complex64)
+    return out
+
+
+def run_chain(cfg, frames, batch_cal=None, stop_after=None, ref_cal=None):
     """Reference pipeline on host frames; returns a dict of stage products.
 
     Follows holopipe/engine.py:135-385 (process_fft, process_ifft,
     process_remove_tilt, extract_coefs) for float32 frames (B*A, H, W).
-    Reference calibration is not restated (SURVEY.md 8(f) 'next').
+    ``ref_cal`` = (kind, raw) enables the reference-wave calibration
+    (kind 1 intensity (Lc, H, W) float32, kind 2 field complex64).
     """
     W, H = cfg.frameWidth, cfg.frameHeight
     nx, ny, p = cfg.fftWindowSizeX, cfg.fftWindowSizeY, cfg.framePixelSize
@@ -516,6 +566,10 @@ def run_chain(cfg, frames, batch_cal=None, stop_after=None):
     raw = inverse_window(win, cfg.resolutionMode, nx, ny)
     xa, ya = out_axes(cfg, wh, ww)
     out.update(window=win, k0=k0, raw=raw, xa=xa, ya=ya, wh=wh, ww=ww)
+    applied = None
+    if ref_cal is not None:
+        applied = ref_calibration(cfg, ref_cal[0], ref_cal[1], origins, xis, lams, wh, ww, mask, xa, ya)
+        out["ref_applied"] = applied
     if stop_after == "ifft":
         return out
     fields = raw.copy()
@@ -533,6 +587,9 @@ def run_chain(cfg, frames, batch_cal=None, stop_after=None):
         for b in range(B):
             for q in range(P):
                 fields[b, q] *= cal[min(q, cal.shape[0] - 1), b % cal.shape[1]]
+    if applied is not None:   # engine.py:250-255
+        for b in range(B):
+            fields[b] *= applied[int(wl[b]) % applied.shape[0]]
     params, inten = plane_stats(fields, xa, ya)
     full = np.zeros((N_ANALYSIS, P, B * A + 1), np.float32)
     full[:, :, :B] = params[:, :, :B]

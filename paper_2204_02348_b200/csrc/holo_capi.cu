@@ -29,6 +29,7 @@ cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h
                                  char* work, int grid, cudaStream_t s);
 cudaError_t launch_field_intensity(const int16_t* fr, const int16_t* fi, const float* scale, int B, int P, int hw,
                                    double* out, cudaStream_t s);
+cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, float2* out, cudaStream_t s);
 }  // namespace holo
 
 using namespace holo;
@@ -654,6 +655,15 @@ int hpg_field_intensity(const int16_t* fr, const int16_t* fi, const float* scale
   if (B < 1 || P < 1 || h < 1 || w < 1) return fail(HPG_INVALIDDIMENSION, "dimensions");
   cudaError_t e = launch_field_intensity(fr, fi, scale, B, P, h * w, out, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "field intensity launch");
+  return HPG_SUCCESS;
+}
+
+int hpg_ref_calibration_finish(const void* a, const void* b, int64_t n, void* applied, void* stream) {
+  if (!a || !applied) return fail(HPG_NULLPOINTER, "null argument");
+  if (n < 1) return fail(HPG_INVALIDDIMENSION, "count");
+  cudaError_t e = launch_refcal_finish(static_cast<const float2*>(a), static_cast<const float2*>(b), n,
+                                       static_cast<float2*>(applied), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "reference calibration launch");
   return HPG_SUCCESS;
 }
 

@@ -586,6 +586,25 @@ cudaError_t launch_field_intensity(const int16_t* fr, const int16_t* fi, const f
   return cudaGetLastError();
 }
 
+// applied = conj(proc) / max(|proc|^2, eps) with proc = a (+ i b), fp64 (engine.py:332-334)
+__global__ void refcal_finish_kernel(const float2* a, const float2* b, int64_t n, float2* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float2 v = a[i];
+  if (b) {   // a + i b, rounded to complex64 like the reference's complex64 field
+    const float2 w = b[i];
+    v = make_float2(v.x - w.y, v.y + w.x);
+  }
+  const double re = (double)v.x, im = (double)v.y;
+  const double mag2 = fmax(re * re + im * im, 1e-6);
+  out[i] = make_float2((float)(re / mag2), (float)(-im / mag2));
+}
+
+cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, float2* out, cudaStream_t s) {
+  refcal_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n, out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_fused(const RunParams& p, cudaStream_t s) {
   fused_kernel<<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p);

@@ -95,6 +95,7 @@ class Engine:
         self.force_simt = False         # diagnostic: specialised kernel without tensor cores
         self.use_tc = False             # tcgen05 row-pass kernel (HPG_FLAG_TC)
         self.last_h2d_bytes = 0
+        self._ref_applied = None        # processed reference calibration (engine.py:75)
         self._plans = collections.OrderedDict()
         self._bufs = {}
         self._clear_products()
@@ -332,23 +333,104 @@ class Engine:
                 k0[self._plan["wl_of_batch"] == w, q] = plan.k0(q, w)
         self._window_meta = {"wh": plan.wh, "ww": plan.ww, "k0": k0}
         if self.ref_cal.enabled and self.ref_cal.kind:
-            raise HoloError(ErrorCode.INVALIDARGUMENT, "reference calibration is not supported by the GPU path yet")
+            self._process_ref_calibration()
         return ErrorCode.SUCCESS
+
+    def _process_ref_calibration(self):
+        """Reference-wave calibration -> applied correction (engine.py:276-335), on the GPU.
+
+        The calibration windows run through the same fused kernel as the frames:
+        * intensity: sqrt(normalised intensity) with the carrier at DC (k0 = 0), no
+          removal phase -- a plan with zero tilt / defocus reproduces exactly
+          forward_fft -> fill_window_r2c(0, 0) -> mask * recentring -> inverse_fft;
+        * field: conj(raw) = a + i b with a = Re raw, b = -Im raw; every step after the
+          C2C transform is linear, so proc = chain(a) + i chain(b) with the r2c window
+          sampling of each real part equal to fill_window_c2c of the complex spectrum
+          (no fill-factor envelope on this path, engine.py:314-316), removal phase at
+          the configured tilt / defocus / beam centre.
+        hpg_ref_calibration_finish then forms conj(proc) / max(|proc|^2, 1e-6)."""
+        torch = _torch()
+        cal = self.ref_cal
+        inten = cal.normalised_intensity()
+        if inten is None:
+            return
+        st0, st1, cfg = self._st0, self._st1, self.config
+        if inten.shape[1] != st0["H"] or inten.shape[2] != st0["W"]:
+            raise HoloError(ErrorCode.INVALIDARGUMENT, "calibration dimensions do not match the frames")
+        tilt, defocus, _ = self._effective()
+        Lc, L, P = cal.wavelength_count, len(st0["lambdas"]), st0["P"]
+        centre = tuple(map(tuple, st0["centre"]))
+        if cal.kind == CAL_INTENSITY:
+            frames = np.sqrt(inten).astype(np.float32)
+            zero = ((0.0, 0.0), (0.0, 0.0))
+            key = (st0["W"], st0["H"], P, st0["nx"], st0["ny"], st1["mode"], st1["fill"], 0, tuple(st0["lambdas"]),
+                   st0["pixel"], st1["lamc"], st1["radius"], centre, zero, zero, centre, (0.0, 0.0), (1.0, 1.0))
+            wl_rows = None
+        else:
+            raw = cal.raw
+            frames = np.concatenate([raw.real, -raw.imag]).astype(np.float32)
+            tl = tuple(tuple(float(v) for v in tilt[a][:2]) for a in range(2))
+            rcentre = tuple(tuple(float(v) for v in cfg.beamCentre[a][:2]) for a in range(2))
+            key = (st0["W"], st0["H"], P, st0["nx"], st0["ny"], st1["mode"], 0, 0, tuple(st0["lambdas"]),
+                   st0["pixel"], st1["lamc"], st1["radius"], centre, tl, tl, rcentre,
+                   (float(defocus[0]), float(defocus[1])), (1.0, 1.0))
+            wl_rows = [min(ci, L - 1) for ci in range(Lc)] * 2
+        plan = self._native_plan(key)
+        B = frames.shape[0]
+        gh, gw = plan.gh, plan.gw
+        dev = self.device
+        with torch.cuda.device(dev):
+            fr_dev = torch.from_numpy(np.ascontiguousarray(frames)).to(dev)
+            raw_out = torch.empty((B, P, gh, gw), dtype=torch.complex64, device=dev)
+            fr16 = torch.empty((B, P, gh, gw), dtype=torch.int16, device=dev)
+            fi16 = torch.empty_like(fr16)
+            sc = torch.empty((B, P), dtype=torch.float32, device=dev)
+            ws_bytes = plan.workspace_size(B, 0)
+            ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+            b = native.Batch()
+            b.frames, b.frame_format, b.transpose = fr_dev.data_ptr(), 0, 0
+            b.frame_count, b.batch_count, b.avg_count = B, B, 1
+            keep = [fr_dev]
+            if wl_rows is not None and L > 1:
+                wl = torch.as_tensor(np.asarray(wl_rows, np.int32), device=dev)
+                b.wl_of_row = wl.data_ptr()
+                keep.append(wl)
+            o = native.Outputs()
+            o.field_r, o.field_i, o.field_scale = fr16.data_ptr(), fi16.data_ptr(), sc.data_ptr()
+            o.raw_fields = raw_out.data_ptr()
+            o.workspace, o.workspace_bytes = ws.data_ptr(), ws_bytes
+            lib = native.lib()
+            native.check(lib.hpg_run(plan.handle, ctypes.byref(b), ctypes.byref(o), 0, native.stream_handle()),
+                         "hpg_run (reference calibration)")
+            applied = torch.empty((Lc, P, gh, gw), dtype=torch.complex64, device=dev)
+            second = raw_out[Lc:].data_ptr() if wl_rows is not None else None
+            native.check(lib.hpg_ref_calibration_finish(raw_out[:Lc].data_ptr(), second, Lc * P * gh * gw,
+                                                        applied.data_ptr(), native.stream_handle()),
+                         "hpg_ref_calibration_finish")
+        self._ref_applied = applied
 
     def process_remove_tilt(self):
         """Stage 2: removal phase, calibrations, int16 packing (engine.py:222-274)."""
         if self._st1 is None:
             raise HoloError(ErrorCode.NULLPOINTER, "IFFT stage has not run")
-        cfg = self.config
-        tilt, defocus, _ = self._effective()
-        self._st2 = {"tilt": [list(map(float, tilt[0])), list(map(float, tilt[1]))],
-                     "centre": [list(map(float, cfg.beamCentre[0][:2])), list(map(float, cfg.beamCentre[1][:2]))],
-                     "defocus": [float(defocus[0]), float(defocus[1])],
-                     "bcal": self.batch_cal.copy() if (self.batch_cal_enabled and self.batch_cal is not None) else None}
+        self._st2 = self._stage2_snapshot()
         self._st3 = None
         self._coefs = None
         self._run_fused(with_coefs=False)
         return ErrorCode.SUCCESS
+
+    def _stage2_snapshot(self):
+        """What process_remove_tilt depends on (engine.py:226-255)."""
+        cfg = self.config
+        tilt, defocus, _ = self._effective()
+        rcal = None
+        if self.ref_cal.enabled and self.ref_cal.kind and self._ref_applied is not None:
+            rcal = self._ref_applied
+        return {"tilt": [list(map(float, tilt[0])), list(map(float, tilt[1]))],
+                "centre": [list(map(float, cfg.beamCentre[0][:2])), list(map(float, cfg.beamCentre[1][:2]))],
+                "defocus": [float(defocus[0]), float(defocus[1])],
+                "bcal": self.batch_cal.copy() if (self.batch_cal_enabled and self.batch_cal is not None) else None,
+                "rcal": rcal}
 
     def extract_coefs(self):
         """Stage 3: separable HG overlap of the int16 fields (engine.py:353-385)."""
@@ -442,6 +524,10 @@ class Engine:
             b.batch_cal = bcal.data_ptr()
             b.cal_pols, b.cal_batch = cal.shape
             L.keep.append(bcal)
+        if self._st2 is not None and self._st2.get("rcal") is not None:
+            rcal = self._st2["rcal"]
+            b.ref_cal, b.ref_cal_count = rcal.data_ptr(), rcal.shape[0]
+            L.keep.append(rcal)
         o = native.Outputs()
         o.field_r, o.field_i, o.field_scale = L.fr.data_ptr(), L.fi.data_ptr(), L.sc.data_ptr()
         o.coefs = L.coefs.data_ptr() if L.coefs is not None else None
@@ -491,12 +577,7 @@ class Engine:
         if from_stage <= 1 or self._st1 is None:
             self.process_ifft()
         if from_stage <= 2 or self._field_r is None:
-            cfg = self.config
-            tilt, defocus, _ = self._effective()
-            self._st2 = {"tilt": [list(map(float, tilt[0])), list(map(float, tilt[1]))],
-                         "centre": [list(map(float, cfg.beamCentre[0][:2])), list(map(float, cfg.beamCentre[1][:2]))],
-                         "defocus": [float(defocus[0]), float(defocus[1])],
-                         "bcal": self.batch_cal.copy() if (self.batch_cal_enabled and self.batch_cal is not None) else None}
+            self._st2 = self._stage2_snapshot()
             self._summary_field = None
             self._window = None
             if self.config.basisGroupCount >= 1:
@@ -679,7 +760,12 @@ class Engine:
         return AnalysisSummary(params, inten, x_axis, y_axis, plane_idx)
 
     def get_ref_calibration_fields(self):
-        return None
+        """(applied, wavelength_count, pol_count, x, y, nx, ny) (engine.py:484-490)."""
+        if self._ref_applied is None:
+            return None
+        x_axis, y_axis = self._field_axes
+        return (self._ref_applied.cpu().numpy(), self.ref_cal.wavelength_count, self._st0["P"],
+                x_axis, y_axis, x_axis.size, y_axis.size)
 
     def basis_get_fields(self):
         cfg = self.config

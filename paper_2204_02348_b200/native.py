@@ -29,7 +29,7 @@ HPG_FLAG_TC = 8
 EXPORTS = [
     "hpg_version", "hpg_plan_create", "hpg_plan_destroy", "hpg_plan_get_info", "hpg_plan_get_axes",
     "hpg_plan_get_basis", "hpg_workspace_size", "hpg_run", "hpg_finalize_summary",
-    "hpg_fourier_full", "hpg_extract_coefs", "hpg_metric_partials", "hpg_plane_summary",
+    "hpg_fourier_full", "hpg_extract_coefs", "hpg_ref_calibration_finish", "hpg_metric_partials", "hpg_plane_summary",
     "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_upload_windows", "hpg_last_error",
 ]
 
@@ -120,6 +120,7 @@ def lib():
     L.hpg_field_intensity.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,
                                       c_void_p, c_void_p]
     L.hpg_plane_summary_workspace.argtypes = [c_int64, c_int32, c_int32, c_int32]
+    L.hpg_ref_calibration_finish.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     L.hpg_upload_windows.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]
     for name in EXPORTS:
         getattr(L, name).restype = c_int32

@@ -118,4 +118,53 @@ CASES = {
         config=_cfg(frameWidth=256, frameHeight=256, polCount=1, batchCount=2,
                     fftWindowSizeX=256, fftWindowSizeY=256, tilt=[[1.0, 1.0], [1.0, 1.0]],
                     basisGroupCount=6, basisWaist=[256 * PIX / 6] * 2)),
+    # reference-wave calibration, intensity kind (holopipe/engine.py:276-335)
+    "refcal_int": dict(
+        frames=dict(width=256, height=256, pol_count=1, batch=3, group_count=6,
+                    waist=200e-6, tilt=(1.0, 1.0), noise="gauss", seed=19),
+        config=_cfg(frameWidth=256, frameHeight=256, polCount=1, batchCount=3,
+                    tilt=[[1.0, 1.0], [1.0, 1.0]], basisGroupCount=6,
+                    basisWaist=[200e-6, 200e-6]),
+        ref_cal=dict(kind=1, wavelengths=[LAM], seed=21)),
+    # reference-wave calibration, field kind, dual-pol, two wavelengths
+    "refcal_field": dict(
+        frames=dict(width=320, height=128, pol_count=2, batch=4, group_count=4,
+                    waist=120e-6, tilt=(1.0, 1.0), noise="gauss", seed=20),
+        config=_cfg(frameWidth=320, frameHeight=128, polCount=2, batchCount=4,
+                    wavelengths=[1550e-9, 1580e-9],
+                    tilt=[[1.0, 1.0], [1.0, 1.0]], defocus=[0.1, 0.1], basisGroupCount=4,
+                    basisWaist=[120e-6, 120e-6],
+                    beamCentre=[[-80 * PIX, 80 * PIX], [0.0, 0.0]]),
+        ref_cal=dict(kind=2, wavelengths=[1550e-9, 1580e-9], seed=22, tilt=(1.0, 1.0))),
 }
+
+
+def make_ref_cal(case):
+    """Seeded calibration frames for a case's ``ref_cal`` spec: (kind, raw).
+
+    kind 1: a broad Gaussian beam intensity with 1 % multiplicative noise,
+    float32 (Lc, H, W); kind 2: a reference-wave field -- Gaussian amplitude,
+    carrier exp(-2 pi i (fx x + fy y)) at the configured tilt and a weak
+    low-order phase -- complex64 (Lc, H, W)."""
+    import numpy as np
+    spec = case["ref_cal"]
+    cfg = case["config"]
+    W, H = cfg["frameWidth"], cfg["frameHeight"]
+    rng = np.random.default_rng(spec["seed"])
+    x = (np.arange(W) - W / 2.0) * PIX
+    y = (np.arange(H) - H / 2.0) * PIX
+    X, Y = np.meshgrid(x, y)
+    out = []
+    for lam in spec["wavelengths"]:
+        x0, y0 = rng.uniform(-0.2, 0.2, 2) * W * PIX / 4
+        w0 = W * PIX * rng.uniform(0.6, 0.9)
+        amp = np.exp(-((X - x0) ** 2 + (Y - y0) ** 2) / w0 ** 2)
+        if spec["kind"] == 1:
+            out.append((amp ** 2 * (1.0 + 0.01 * rng.standard_normal(X.shape))).astype(np.float32))
+        else:
+            tx, ty = spec["tilt"]
+            fx, fy = math.sin(math.radians(tx)) / lam, math.sin(math.radians(ty)) / lam
+            a, b, c = rng.normal(0.0, 0.5, 3)
+            phi = a * (X / w0) + b * (Y / w0) + c * ((X ** 2 + Y ** 2) / w0 ** 2)
+            out.append((amp * np.exp(-2j * np.pi * (fx * X + fy * Y) + 1j * phi)).astype(np.complex64))
+    return spec["kind"], np.stack(out)

@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from paper_2204_02348_b200.synth import FrameSpec, make_frames, frames_digest  # noqa: E402
-from tests.golden.cases import CASES  # noqa: E402
+from tests.golden.cases import CASES, make_ref_cal  # noqa: E402
 
 
 def run_reference(case):
@@ -45,6 +45,13 @@ def run_reference(case):
     if batch_cal is not None:
         arr = np.asarray(batch_cal, np.complex64)
         eng.set_batch_calibration(arr.reshape(-1), arr.shape[0], arr.shape[1])
+    if case.get("ref_cal") is not None:
+        kind, raw = make_ref_cal(case)
+        Lc, Hc, Wc = raw.shape
+        if kind == 1:
+            eng.ref_cal.set_intensity(raw, Lc, Wc, Hc)
+        else:
+            eng.ref_cal.set_field(raw, Lc, Wc, Hc)
     eng.run_pipeline(0)
     out = {
         "frames_sha256": np.array(frames_digest(frames)),
@@ -55,6 +62,8 @@ def run_reference(case):
         "k0": eng._window_meta["k0"],
         "origins": np.array(eng._plan["origins"]),
     }
+    if case.get("ref_cal") is not None:
+        out["ref_applied"] = eng._ref_applied
     if case.get("store_fourier"):
         out["fourier_params"] = eng._summary_fourier.parameters
         out["fourier_inten"] = eng._summary_fourier.total_intensity

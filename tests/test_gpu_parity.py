@@ -4,7 +4,7 @@ reference's own outputs (golden fixtures) and the oracle on the same frames."""
 import numpy as np
 import pytest
 
-from tests.golden.cases import CASES
+from tests.golden.cases import CASES, make_ref_cal
 from tests.golden_util import dequant, load, rel_l2_rows
 
 pytestmark = pytest.mark.gpu
@@ -23,6 +23,10 @@ def _engine(case, frames):
     if case.get("batch_cal") is not None:
         cal = np.asarray(case["batch_cal"], np.complex64)
         eng.set_batch_calibration(cal.reshape(-1), cal.shape[0], cal.shape[1])
+    if case.get("ref_cal") is not None:
+        kind, raw = make_ref_cal(case)
+        Lc, Hc, Wc = raw.shape
+        (eng.ref_cal.set_intensity if kind == 1 else eng.ref_cal.set_field)(raw, Lc, Wc, Hc)
     return eng
 
 
@@ -167,3 +171,22 @@ def test_tensor_core_row_dft_matches_simt_fft(name):
     assert rel_l2_rows(tc[3], simt[3]) <= 2e-5
     ef = rel_l2_rows(dequant(tc[0], tc[1], tc[2]), dequant(g["fr"], g["fi"], g["scale"]))
     assert ef <= FIELD_TOL
+
+
+@pytest.mark.parametrize("name", ["refcal_int", "refcal_field"])
+def test_reference_calibration_table_matches_reference(name):
+    """Processed reference-wave calibration (engine.py:276-335) vs the reference's own table."""
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.run_pipeline(0)
+    got = eng.get_ref_calibration_fields()
+    assert got is not None
+    applied, lc, pols, xa, ya, nx, ny = got
+    assert applied.shape == g["ref_applied"].shape and lc == applied.shape[0] and pols == applied.shape[1]
+    ref = g["ref_applied"].reshape(-1, applied.shape[-2] * applied.shape[-1])
+    assert rel_l2_rows(applied.reshape(ref.shape), ref) <= 1e-4
+    # disabling the calibration drops it from the next tilt-removal stage (engine.py:250-251)
+    eng.ref_cal.enabled = 0
+    eng.run_pipeline(2)
+    fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
+    assert rel_l2_rows(dequant(fr, fi, sc), dequant(g["fr"], g["fi"], g["scale"])) > 1e-2
