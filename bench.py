@@ -209,6 +209,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tc", action="store_true", help="use the tcgen05 row-pass kernel (HPG_FLAG_TC)")
+    ap.add_argument("--tc2", action="store_true", help="use the two-kernel tensor-core path (HPG_FLAG_TC2)")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture")
     args = ap.parse_args()
@@ -230,6 +231,7 @@ def main():
     h = api.create_handle()
     eng = api.engine(h)
     eng.use_tc = args.tc
+    eng.use_tc2 = args.tc2
     for k, v in cfg.items():
         setattr(eng.config, k, v)
     frames_dev = torch.from_numpy(frames_host).to(dev)

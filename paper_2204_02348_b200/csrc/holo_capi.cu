@@ -24,6 +24,10 @@ cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, c
 bool tc_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
                   const void* windows);
 cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
+bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
+                   const void* windows);
+size_t tc2_workspace(int64_t items);
+cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
 cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
                                  const double* ya, float* params, int slots, float* total, double* pol_total,
                                  char* work, int grid, cudaStream_t s);
@@ -416,9 +420,39 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
     }
   }
   if (a_tc.empty()) a_tc.push_back(0u);
+  // tensor-core column DFT (holo_tc2.cu): rows r < wh -> Cr, rows 64 + r -> Ci of
+  // C[r][y] = exp(-2 pi i ky_r y / ny) * py[r] = exp(-2 pi i ky_r (y - xi_y + ny/2) / ny),
+  // ky_r = k0y + r - wh/2; K = y (0..127), fp16 hi + lo.  ny == 128, wh <= 64, wavelength 0.
+  std::vector<uint32_t> a2_tc;
+  if (g.ny == 128 && g.wh <= 64) {
+    a2_tc.assign((size_t)g.P * 2 * 128 * 64, 0u);
+    for (int q = 0; q < g.P; ++q) {
+      const int ky = g.k0[q][0][1];
+      for (int n = 0; n < 128; ++n) {
+        const int r = n & 63;
+        if (r >= g.wh) continue;
+        const double kr = (double)(ky + r - g.wh / 2);
+        for (int y2 = 0; y2 < 64; ++y2) {
+          uint16_t hh[2], ll[2];
+          for (int e = 0; e < 2; ++e) {
+            const int y = 2 * y2 + e;
+            const double ang = -2.0 * kPi * kr * ((double)y - xi[q][1] + g.ny / 2.0) / g.ny;
+            const double v = n < 64 ? std::cos(ang) : std::sin(ang);
+            const __half h = __double2half(v);
+            const __half l = __double2half(v - (double)__half2float(h));
+            hh[e] = __half_as_ushort(h);
+            ll[e] = __half_as_ushort(l);
+          }
+          a2_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + y2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a2_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + y2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+        }
+      }
+    }
+  }
+  if (a2_tc.empty()) a2_tc.push_back(0u);
   P->fill = d->fill_factor;
   std::vector<char> blob;
-  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange), o_atc = push(blob, a_tc);
+  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange), o_atc = push(blob, a_tc), o_a2 = push(blob, a2_tc);
   const size_t o_nx = push(blob, tw_nx), o_ny = push(blob, tw_ny), o_gw = push(blob, tw_gw), o_gh = push(blob, tw_gh);
   const size_t o_w = push(blob, wtab), o_rx = push(blob, remx), o_ry = push(blob, remy);
   std::vector<float> hxv = P->hx, hyv = P->hy;
@@ -455,6 +489,7 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.py = reinterpret_cast<const float2*>(base + o_py);
   P->ft.crange = reinterpret_cast<const int16_t*>(base + o_cr);
   P->ft.a_tc = reinterpret_cast<const uint32_t*>(base + o_atc);
+  P->ft.a2_tc = reinterpret_cast<const uint32_t*>(base + o_a2);
   e = set_smem_limits();
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
   *out = P;
@@ -521,6 +556,7 @@ int hpg_workspace_size(const hpg_plan* P, int32_t B, uint32_t flags, size_t* byt
   Layout F = make_layout(P, B, 1, 0, true);
   finish_layout(P, F, (int64_t)P->num_sms * 2, 0);
   *bytes = (size_t)std::max<int64_t>(std::max<int64_t>(fused, F.slab_bytes * F.grid), 256);
+  *bytes = std::max(*bytes, tc2_workspace((int64_t)B * P->g.P));   // Fourier windows between the TC2 kernels
   return HPG_SUCCESS;
 }
 
@@ -589,7 +625,12 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
   if ((rp.lay.slab_bytes > 0 || (flags & HPG_FLAG_SUMMARY)) && (!o->workspace || (int64_t)o->workspace_bytes < need))
     return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
   cudaError_t e;
-  if ((flags & HPG_FLAG_TC) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
+  if ((flags & HPG_FLAG_TC2) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
+      tc2_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows)) {
+    if (!o->workspace || o->workspace_bytes < tc2_workspace((int64_t)b->batch_count * P->g.P))
+      return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
+    e = launch_tc2(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+  } else if ((flags & HPG_FLAG_TC) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
       tc_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows))
     e = launch_fast_tc(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
   else if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&

@@ -65,6 +65,8 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
   constexpr int ZS = LY::ZS;
   extern __shared__ __align__(16) char smem[];
   __shared__ float redf[8];
+  __shared__ int slot[128];
+  int slot_kxs = -1;
   float2* zs = reinterpret_cast<float2*>(smem + LY::zs);
   float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
   float2* tw128 = reinterpret_cast<float2*>(smem + LY::tw128);
@@ -98,6 +100,15 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
       s_py[i] = ft.py[pl * WH + i];
       s_ey[i] = p.t.rem_y[pl * WH + i];
     }
+    if (kxs != slot_kxs) {   // FFT bin -> zs slots (packed int16 pair, -1 = not in the window)
+      for (int kk = tid; kk < 128; kk += blockDim.x) {
+        const int cp = (kk - kxs) & 127, cm = (128 - kk - kxs) & 127;
+        const int sp = cp < WW ? zs_pos<WW>(cp) : -1, sn = cm < WW ? zs_neg<WW>(cm) : -1;
+        slot[kk] = (sp & 0xffff) | (sn << 16);
+      }
+      slot_kxs = kxs;
+      __syncthreads();
+    }
 
     // ------------------------------------------------------------ row pass
     const int W = g.W, H = g.H;
@@ -125,10 +136,10 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
         fft128_stage2(z, h, xg, t, v);
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          const int kk = t + 8 * h + 16 * k2;
-          const int cp = (kk - kxs) & 127, cm = (128 - kk - kxs) & 127;
-          if (cp < WW) zrow[zs_pos<WW>(cp)] = v[k2];
-          if (cm < WW) zrow[zs_neg<WW>(cm)] = v[k2];
+          const int sl = slot[t + 8 * h + 16 * k2];   // zs slots of bin kk as +kx_c and as -kx_c
+          const int sp = (short)(sl & 0xffff), sn = sl >> 16;
+          if (sp >= 0) zrow[sp] = v[k2];
+          if (sn >= 0) zrow[sn] = v[k2];
         }
       }
     }

@@ -35,8 +35,10 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
       v[j] = src[MAPPED_ZS ? w_addr<MAPPED_ZS>(i) : i];
     }
     if (L > 1) {
+      // j*k*mp < N whenever (P-1)(L-1)mp < N (every stage of the 42 = 6 x 7 plans): no modulo
+      constexpr bool kWrap = (P - 1) * (L - 1) * mp >= N;
 #pragma unroll
-      for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<INV>(tw[(j * k * mp) % N]));
+      for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<INV>(tw[kWrap ? (j * k * mp) % N : j * k * mp]));
     }
     dft_fixed<P, INV>(v);
 #pragma unroll
@@ -62,8 +64,9 @@ HOLO_DEV float ct_stage_final_rows(const float2* __restrict__ src, float2* __res
     float2 v[P];
 #pragma unroll
     for (int j = 0; j < P; ++j) v[j] = src[y + (k * m_in + j) * COUNT];
+    constexpr bool kWrap = (P - 1) * (L - 1) >= N;
 #pragma unroll
-    for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<true>(tw[(j * k) % N]));
+    for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<true>(tw[kWrap ? (j * k) % N : j * k]));
     dft_fixed<P, true>(v);
     const float2 eyq = cscale(ey[y], osc);
 #pragma unroll

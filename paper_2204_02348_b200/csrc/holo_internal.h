@@ -37,6 +37,7 @@ struct FastTables {
   const float2* py;        // [P][L][WH] recentring phase along y
   const int16_t* crange;   // [WW][2] first/last row inside the circular mask, per column
   const uint32_t* a_tc;    // [P][2][128][64] f16x2: row-DFT matrix (hi, lo) for wavelength 0
+  const uint32_t* a2_tc;   // [P][2][128][64] f16x2: column-DFT matrix [Cr; Ci] (hi, lo) for wavelength 0
 };
 
 struct Geometry {

@@ -1,0 +1,626 @@
+// Two-kernel tensor-core path for the 128-window / 42x42 geometry (sm_100a).
+//
+// K1  fourier128_tc2_kernel   frames -> masked, recentred Fourier window W (42 x 42)
+//     Both DFTs of the crop are GEMMs on the 5th-generation tensor cores:
+//       row DFT     D1[n][y]   = sum_x A1[n][x] f[y][x]          M=128 N=128 K=128
+//                   A1 = [Re; Im] exp(-2 pi i kx_c (x - xi_x + nx/2)/nx)   (recentring folded in)
+//       column DFT  D2a[m][c]  = sum_y A2[m][y] Re R[y][c]        M=128 N=48  K=128
+//                   D2b[m][c]  = sum_y A2[m][y] Im R[y][c]
+//                   A2 = [Cr; Ci], C[r][y] = exp(-2 pi i ky_r (y - xi_y + ny/2)/ny)
+//       W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr), masked (holopipe/pipeline.py:72-127)
+//     fp32-class precision from fp16 hi/lo operand splits (3 products, fp32
+//     accumulation) with exact power-of-two scalings.  TMEM (512 columns):
+//       A1 hi|lo [0,128)  A2 hi|lo [128,256)  D1 [256,384)  D2a [384,432)  D2b [432,480)
+//     Warp-specialised: warps 0-3 stream windows (per-row power-of-two scale, fp16
+//     split, double-buffered stage) and issue the row GEMM; warps 4-11 drain D1
+//     into the column GEMM's operand, issue it, and drain D2 into W.
+// K2  field128_kernel         W -> 42x42 IFFT, removal phase, calibrations, int16
+//     packing, HG overlap (the SIMT tail of holo_fast.cu; holopipe/pipeline.py:130-199,
+//     holopipe/hgbasis.py:101-116).
+// W lives in the workspace between the two launches; batches are processed in
+// chunks small enough for W to stay resident in L2.
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "holo_fast_common.cuh"
+#include "holo_internal.h"
+#include "holo_tc_common.cuh"
+
+namespace holo {
+
+namespace {
+
+constexpr int kProd2 = 256;                 // producer threads (warps 0-7)
+constexpr int kMmaWarp = 8;                 // tcgen05.mma issuer
+constexpr int kCons2 = 256;                 // consumer threads (warps 9-16)
+constexpr int kConsWarp0 = kMmaWarp + 1;
+constexpr int kK1Threads = kProd2 + 32 + kCons2;
+constexpr int kBarProd2 = 1, kBarCons2 = 2;
+constexpr int kN2 = 48;                     // column-DFT N per real part (42 columns, padded)
+constexpr int kWinW = 42, kWinH = 42;
+
+// dynamic shared memory (bytes)
+constexpr uint32_t kLandPitch = 528;               // landing row pitch (512 B of f32 + 16 B pad)
+constexpr uint32_t kLandSlot = 32 * kLandPitch;    // 32 rows
+constexpr uint32_t kLand = 0;                      // 4 slots = one window, bulk-async copies
+constexpr uint32_t kStage = 4 * kLandSlot;         // [half][hi 16 KB | lo 16 KB]
+constexpr uint32_t kStageHalf = 32768;
+constexpr uint32_t kB2 = kStage + 2 * kStageHalf;  // B2 hi | B2 lo: rows c (Re R), 48 + c (Im R)
+constexpr uint32_t kB2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
+constexpr uint32_t kXP = 88;                       // drain-2 exchange X[acc][c][rho] pitch (floats)
+constexpr uint32_t kX = kB2 + 2 * kB2Part;
+constexpr uint32_t kFac = kX + 2 * kN2 * kXP * 4;  // fac[2][128] f32
+constexpr uint32_t kErow = kFac + 2 * 128 * 4;     // e_row[128] int
+constexpr uint32_t kCr = kErow + 128 * 4;          // crange[42][2] int
+constexpr uint32_t kK1Bytes = kCr + 2 * 64 * 4;
+static_assert(kK1Bytes <= 227 * 1024, "K1 shared memory");
+
+// canonical K-major, no-swizzle operand layout: [kstep][row/8][khalf][row%8][8 halves]
+HOLO_DEV uint32_t kmaj_off(int row, int k, int ngroups) {
+  return (uint32_t)(k >> 4) * (ngroups * 256) + ((uint32_t)(row >> 3) * 2 + ((k >> 3) & 1)) * 128 +
+         (uint32_t)(row & 7) * 16;
+}
+
+HOLO_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+HOLO_DEV void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+}  // namespace
+
+// Phase timestamps of CTA 0 (clock64), for tools/tc2_trace.py (hpg_debug_trace).
+__device__ long long g_tc2_trace[2][64][8];
+#define TC2_MARK(role, kk, ev)                                                   \
+  do {                                                                           \
+    if (blockIdx.x == 0 && (kk) < 64) g_tc2_trace[role][kk][ev] = clock64();     \
+  } while (0)
+
+// Issue the bulk copies of chunk j (rows 32j..32j+31) of an item's window (warp 0).
+HOLO_DEV void issue_chunk(const RunParams& p, int item, int j, char* smem, uint64_t* lfull, int lane) {
+  const Geometry& g = p.g;
+  const int b = item / g.P, q = item - b * g.P;
+  const int es = p.fmt == 0 ? 4 : 2;
+  const uint32_t rowb = 128u * es;
+  if (lane == 0) mbar_expect_tx(&lfull[j], 32u * rowb);
+  __syncwarp();
+  const int y = 32 * j + lane;
+  const char* src = reinterpret_cast<const char*>(p.frames) +
+                    ((int64_t)b * g.W * g.H + (int64_t)(g.row0[q] + y) * g.W + g.col0[q]) * es;
+  bulk_g2s(smem_u32(smem + kLand + j * kLandSlot + lane * kLandPitch), src, rowb, &lfull[j]);
+}
+
+__global__ void __launch_bounds__(kK1Threads, 1)
+    fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0,
+                          int i1, float2* __restrict__ wout) {
+  extern __shared__ __align__(1024) char smem[];
+  // lfull[j]: landing chunk j arrived; staged[h]: stage half h ready; meta[s]: fac[s] ready;
+  // mma1[h]: row GEMM half h done; b2ready[h]: D1 half h drained into B2 (D1 half h free);
+  // stfree[h]: stage half h consumed; full2: column GEMM done; d2free: D2 drained;
+  // facfree[s]: fac[s] consumed
+  __shared__ __align__(8) uint64_t lfull[4], staged[2], meta[2], mma1[2], b2ready[2], stfree[2], full2, d2free,
+      facfree[2];
+  __shared__ uint32_t tbase;
+  __shared__ int emaxw[8];
+  __shared__ int emaxs[2];
+  float* fac = reinterpret_cast<float*>(smem + kFac);
+  int* erow = reinterpret_cast<int*>(smem + kErow);
+  int* crs = reinterpret_cast<int*>(smem + kCr);
+  const Geometry& g = p.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&lfull[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&staged[i], 1);
+      mbar_init(&meta[i], 1);
+      mbar_init(&mma1[i], 1);
+      mbar_init(&b2ready[i], 1);
+      mbar_init(&stfree[i], 1);
+      mbar_init(&facfree[i], 1);
+    }
+    mbar_init(&full2, 1);
+    mbar_init(&d2free, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  for (int i = tid; i < 2 * kWinW; i += blockDim.x) crs[i] = ft.crange[i];
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t tA1 = tm, tA2 = tm + 128, tD1 = tm + 256, tD2 = tm + 384;
+
+  if (warp < kMmaWarp) {
+    // ================================= producer =================================
+    const int rl = lane >> 3, t8 = lane & 7;   // row (of 4 per warp per chunk), octet pair t8 / t8 + 8
+    int loaded_q = -1;
+    if (warp == 0)
+      for (int j = 0; j < 4; ++j)
+        if (i0 + (int)blockIdx.x < i1) issue_chunk(p, i0 + blockIdx.x, j, smem, lfull, lane);
+    int k = 0;
+    for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
+      const int s = k & 1;
+      const int q = item % g.P;
+      const int nitem = item + gridDim.x;
+      if (tid == 0) TC2_MARK(0, k, 0);
+      if (q != loaded_q) {   // A1 of this pol; the previous window's row GEMM must be done with it
+        if (k >= 1) mbar_wait_warp(&stfree[1], (k - 1) & 1);
+        tc_fence_after();
+        if (warp < 4) {
+          const uint32_t* src = ft.a_tc + ((size_t)q * 2 * 128 + warp * 32 + lane) * 64;
+          uint32_t r[32];
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const uint32_t* s2 = src + (size_t)part * 128 * 64 + hh * 32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
+              tmem_st32(tA1 + ((uint32_t)(warp * 32) << 16) + part * 64 + hh * 32, r);
+            }
+          }
+          tmem_wait_st();
+        }
+        loaded_q = q;
+      }
+      int emax_t = -1000;
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {   // chunk j = rows 32j..32j+31
+        const int h = j >> 1;
+        if ((j & 1) == 0 && k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done
+        if (tid == 0 && j == 0) TC2_MARK(0, k, 1);
+        mbar_wait_warp(&lfull[j], k & 1);
+        if (tid == 0 && j == 0) TC2_MARK(0, k, 6);
+        if (tid == 0 && j == 2) TC2_MARK(0, k, 7);
+        const int yl = 4 * warp + rl, y = 32 * j + yl;
+        const char* lrow = smem + kLand + j * kLandSlot + yl * kLandPitch;
+        float v[16];
+        if (p.fmt == 0) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const float4 a = *reinterpret_cast<const float4*>(lrow + (8 * t8 + 64 * u) * 4);
+            const float4 c = *reinterpret_cast<const float4*>(lrow + (8 * t8 + 64 * u) * 4 + 16);
+            v[8 * u + 0] = a.x; v[8 * u + 1] = a.y; v[8 * u + 2] = a.z; v[8 * u + 3] = a.w;
+            v[8 * u + 4] = c.x; v[8 * u + 5] = c.y; v[8 * u + 6] = c.z; v[8 * u + 7] = c.w;
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const uint4 a = *reinterpret_cast<const uint4*>(lrow + (8 * t8 + 64 * u) * 2);
+            const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * u + 2 * e] = (float)(w4[e] & 0xffffu);
+              v[8 * u + 2 * e + 1] = (float)(w4[e] >> 16);
+            }
+          }
+        }
+        float m = 0.f;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) m = fmaxf(m, fabsf(v[e]));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+        // exact power-of-two row scale: |f| * sc < 2^14, fh + fl keep 22 bits
+        int e2 = 0;
+        frexpf(m, &e2);
+        const float sc = m > 0.f ? ldexpf(1.f, 14 - e2) : 1.f;
+        const int ey = m > 0.f ? e2 : -1000;
+        if (t8 == 0) erow[y] = ey;
+        emax_t = max(emax_t, ey);
+        char* st = smem + kStage + h * kStageHalf;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {   // octet x = 8 t8 + 64 u
+          const uint32_t off = kmaj_off(y & 63, 8 * t8 + 64 * u, 8);
+          uint32_t hi2[4], lo2[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float a = v[8 * u + 2 * e] * sc, c = v[8 * u + 2 * e + 1] * sc;
+            hi2[e] = pack_h2(a, c);
+            const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi2[e]));
+            lo2[e] = pack_h2(a - back.x, c - back.y);
+          }
+          *reinterpret_cast<uint4*>(st + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+          *reinterpret_cast<uint4*>(st + 16384 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+        }
+        fence_async_smem();
+        tc_fence_before();
+        nbar(kBarProd2, kProd2);   // chunk j consumed: landing slot j free, stage rows written
+        if (warp == 0 && nitem < i1) issue_chunk(p, nitem, j, smem, lfull, lane);
+        if (tid == 0 && (j & 1)) mbar_arrive(&staged[h]);
+      }
+      if (tid == 0) TC2_MARK(0, k, 2);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) emax_t = max(emax_t, __shfl_xor_sync(0xffffffffu, emax_t, o));
+      if (lane == 0) emaxw[warp] = emax_t;
+      nbar(kBarProd2, kProd2);
+      if (k >= 2) mbar_wait_warp(&facfree[s], ((k >> 1) - 1) & 1);   // drains of window k-2 done with fac[s]
+      if (tid < 128) {   // column-operand scale per row: B2 = D1 * 2^(e_y - e_max - 6) = R * 2^(8 - e_max)
+        int em = emaxw[0];
+#pragma unroll
+        for (int j = 1; j < 8; ++j) em = max(em, emaxw[j]);
+        const int ey = erow[tid];
+        fac[s * 128 + tid] = ey > -1000 ? ldexpf(1.f, ey - em - 6) : 0.f;
+        if (tid == 0) emaxs[s] = em;
+      }
+      nbar(kBarProd2, kProd2);
+      if (tid == 0) {
+        mbar_arrive(&meta[s]);
+        TC2_MARK(0, k, 3);
+      }
+    }
+  } else if (warp == kMmaWarp) {
+    // ================================ MMA issuer ================================
+    const uint32_t idesc1 = idesc_f16(128, 64), idesc2 = idesc_f16(128, 2 * kN2);
+    int k = 0;
+    for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {   // row GEMM, half h: D1[:, 64h .. 64h+63]
+        mbar_wait_warp(&staged[h], k & 1);
+        if (k >= 1) mbar_wait_warp(&b2ready[h], (k - 1) & 1);   // D1 half h drained
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sb = smem_u32(smem + kStage + h * kStageHalf);
+#pragma unroll
+          for (int gk = 0; gk < 8; ++gk) {
+            const uint64_t bh = umma_desc(sb + gk * 2048, 128, 256);
+            const uint64_t bl = umma_desc(sb + 16384 + gk * 2048, 128, 256);
+            mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bh, idesc1, gk != 0);
+            mma_f16_ts(tD1 + 64 * h, tA1 + 64 + gk * 8, bh, idesc1, 1);
+            mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bl, idesc1, 1);
+          }
+          tc_commit(&mma1[h]);
+          tc_commit(&stfree[h]);
+          if (h == 1) TC2_MARK(0, k, 4);
+        }
+        __syncwarp();
+      }
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {   // column GEMM, K-half h (y = 64h .. 64h+63), N = 96
+        mbar_wait_warp(&b2ready[h], k & 1);
+        if (h == 0 && k >= 1) mbar_wait_warp(&d2free, (k - 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sb = smem_u32(smem + kB2);
+#pragma unroll
+          for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {
+            const uint32_t o = ks * 3072;
+            const uint64_t rh = umma_desc(sb + o, 128, 256), rl = umma_desc(sb + kB2Part + o, 128, 256);
+            mma_f16_ts(tD2, tA2 + ks * 8, rh, idesc2, ks != 0);
+            mma_f16_ts(tD2, tA2 + 64 + ks * 8, rh, idesc2, 1);
+            mma_f16_ts(tD2, tA2 + ks * 8, rl, idesc2, 1);
+          }
+          if (h == 1) {
+            tc_commit(&full2);
+            TC2_MARK(0, k, 5);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ================================= consumer =================================
+    const int ct = tid - kProd2 - 32, cw = warp - kConsWarp0, quarter = warp & 3, sub = cw >> 2;
+    char* b2 = smem + kB2;
+    float* X = reinterpret_cast<float*>(smem + kX);
+    int loaded_q = -1;
+    int k = 0;
+    for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
+      const int s = k & 1;
+      const int q = item % g.P;
+      if (q != loaded_q) {   // A2 of this pol (the previous column GEMM completed: waited full2 below)
+        if (sub == 0) {
+          const uint32_t* src = ft.a2_tc + ((size_t)q * 2 * 128 + quarter * 32 + lane) * 64;
+          uint32_t r[32];
+#pragma unroll
+          for (int part = 0; part < 2; ++part) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const uint32_t* s2 = src + (size_t)part * 128 * 64 + hh * 32;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
+              tmem_st32(tA2 + ((uint32_t)(quarter * 32) << 16) + part * 64 + hh * 32, r);
+            }
+          }
+          tmem_wait_st();
+        }
+        loaded_q = q;
+      }
+      if (ct == 0) TC2_MARK(1, k, 0);
+      mbar_wait_warp(&meta[s], (k >> 1) & 1);
+      // ------------------------------------------- drain D1 (by halves) -> B2
+      const int n = quarter * 32 + lane, c = n & 63;
+      const int brow = (n >= 64 ? kN2 : 0) + c;   // B2 row: Re R rows then Im R rows
+      const float* fs = fac + s * 128;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        mbar_wait_warp(&mma1[h], k & 1);
+        tc_fence_after();
+        if (ct == 0 && h == 0) TC2_MARK(1, k, 1);
+        const int y0 = 64 * h + 32 * sub;
+        uint32_t r[32];
+        tmem_ld16(tD1 + ((uint32_t)(quarter * 32) << 16) + y0, r);
+        tmem_ld16(tD1 + ((uint32_t)(quarter * 32) << 16) + y0 + 16, r + 16);
+        tmem_wait_ld();
+        if (c < kN2) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {   // one 16-byte row chunk: y = y0 + 8j .. +7
+            uint32_t hi2[4], lo2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f2 = *reinterpret_cast<const float2*>(fs + y0 + 8 * j + 2 * e);
+              const float a = __uint_as_float(r[8 * j + 2 * e]) * f2.x;
+              const float d = __uint_as_float(r[8 * j + 2 * e + 1]) * f2.y;
+              hi2[e] = pack_h2(a, d);
+              const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi2[e]));
+              lo2[e] = pack_h2(a - back.x, d - back.y);
+            }
+            const uint32_t o = kmaj_off(brow, y0 + 8 * j, 2 * kN2 / 8);
+            *reinterpret_cast<uint4*>(b2 + o) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+            *reinterpret_cast<uint4*>(b2 + kB2Part + o) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+          }
+        }
+        fence_async_smem();
+        tc_fence_before();
+        nbar(kBarCons2, kCons2);
+        if (ct == 0) {
+          mbar_arrive(&b2ready[h]);
+          if (h == 1) {
+            mbar_arrive(&facfree[s]);
+            TC2_MARK(1, k, 2);
+          }
+        }
+      }
+      const float gs = ldexpf(1.f, emaxs[s] - 8);
+      mbar_wait_warp(&full2, k & 1);
+      tc_fence_after();
+      if (ct == 0) TC2_MARK(1, k, 3);
+
+      // ------------------------------------- drain D2 -> exchange X[acc][c][rho]
+      {
+        const int r = n & 63;
+        const uint32_t src = tD2 + (sub ? kN2 : 0) + ((uint32_t)(quarter * 32) << 16);
+        const int rho = n < 64 ? r : kWinH + r;   // compact row: Cr rows then Ci rows
+        float* xr = X + (size_t)sub * kN2 * kXP + rho;
+        uint32_t v[48];
+        tmem_ld16(src, v);
+        tmem_ld16(src + 16, v + 16);
+        tmem_ld16(src + 32, v + 32);
+        tmem_wait_ld();
+        if (r < kWinH) {
+#pragma unroll
+          for (int cc = 0; cc < kWinW; ++cc) xr[cc * kXP] = __uint_as_float(v[cc]);
+        }
+      }
+      tc_fence_before();
+      nbar(kBarCons2, kCons2);
+      if (ct == 0) {
+        mbar_arrive(&d2free);
+        TC2_MARK(1, k, 4);
+      }
+
+      // ------------------------------- W = (CrRr - CiRi) + i (CrRi + CiRr), masked
+      {
+        float2* wo = wout + (size_t)(item - i0) * kWinH * kWinW;
+        const float* Xa = X;
+        const float* Xb = X + kN2 * kXP;
+        for (int i = ct; i < kWinH * kWinW; i += kCons2) {
+          const int cc = i / kWinH, r = i - cc * kWinH;
+          float2 w = make_float2(0.f, 0.f);
+          if (r >= crs[2 * cc] && r <= crs[2 * cc + 1]) {
+            const float* xa = Xa + cc * kXP;
+            const float* xb = Xb + cc * kXP;
+            w = make_float2((xa[r] - xb[kWinH + r]) * gs, (xb[r] + xa[kWinH + r]) * gs);
+          }
+          wo[i] = w;   // column-major [c][r]
+        }
+      }
+      nbar(kBarCons2, kCons2);   // X free for the next window
+      if (ct == 0) TC2_MARK(1, k, 5);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+}
+
+// ---------------------------------------------------------------------------
+// K2: window -> field -> int16 -> coefficients (SIMT, 3+ CTAs per SM)
+template <int WH, int WW>
+struct FieldLayout {
+  static constexpr size_t T = 0;                                            // IFFT ping
+  static constexpr size_t F = T + WH * WW * sizeof(float2);                  // IFFT pong / field
+  static constexpr size_t U = F + WH * WW * sizeof(float2);                  // overlap partials [WH][GP]
+  static constexpr int GMAX = 48;
+  static constexpr size_t twh = U + WH * GMAX * sizeof(float2);
+  static constexpr size_t tww = twh + WH * sizeof(float2);
+  static constexpr size_t ph = tww + WW * sizeof(float2);                    // ex[WW] ey[WH]
+  static constexpr size_t basis = (ph + (WH + WW) * sizeof(float2) + 15) & ~size_t(15);
+};
+
+template <int WH, int WW>
+__global__ void __launch_bounds__(256, 3)
+    field128_kernel(const __grid_constant__ RunParams p, int i0, int i1, const float2* __restrict__ win) {
+  using LY = FieldLayout<WH, WW>;
+  extern __shared__ __align__(1024) char smem[];
+  __shared__ float redf[8];
+  float2* T = reinterpret_cast<float2*>(smem + LY::T);
+  float2* F = reinterpret_cast<float2*>(smem + LY::F);
+  float2* U = reinterpret_cast<float2*>(smem + LY::U);
+  float2* twh = reinterpret_cast<float2*>(smem + LY::twh);
+  float2* tww = reinterpret_cast<float2*>(smem + LY::tww);
+  float2* s_ex = reinterpret_cast<float2*>(smem + LY::ph);
+  float2* s_ey = s_ex + WW;
+  float* hxP = reinterpret_cast<float*>(smem + LY::basis);
+  const Geometry& g = p.g;
+  const int tid = threadIdx.x;
+  const int G = g.G, GP = (G + 3) & ~3;
+  for (int i = tid; i < WH; i += blockDim.x) twh[i] = p.t.tw_gh[i];
+  for (int i = tid; i < WW; i += blockDim.x) tww[i] = p.t.tw_gw[i];
+  int staged_q = -1;
+  for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x) {
+    const int b = item / g.P, q = item - b * g.P;
+    __syncthreads();   // previous item done with every buffer
+    for (int i = tid; i < WW; i += blockDim.x) s_ex[i] = p.t.rem_x[q * g.L * WW + i];
+    for (int i = tid; i < WH; i += blockDim.x) s_ey[i] = p.t.rem_y[q * g.L * WH + i];
+    if (p.coefs && G > 0 && q != staged_q) {   // basis of this pol, transposed [x][m] / [y][n]
+      const float* hx = p.t.hx + (size_t)q * G * WW;
+      const float* hy = p.t.hy + (size_t)q * G * WH;
+      for (int i = tid; i < (GP / 4) * WW; i += blockDim.x) {
+        const int x = i % WW, m4 = 4 * (i / WW);
+        float4 h;
+        h.x = m4 + 0 < G ? __ldg(&hx[(m4 + 0) * WW + x]) : 0.f;
+        h.y = m4 + 1 < G ? __ldg(&hx[(m4 + 1) * WW + x]) : 0.f;
+        h.z = m4 + 2 < G ? __ldg(&hx[(m4 + 2) * WW + x]) : 0.f;
+        h.w = m4 + 3 < G ? __ldg(&hx[(m4 + 3) * WW + x]) : 0.f;
+        *reinterpret_cast<float4*>(&hxP[x * GP + m4]) = h;
+      }
+      for (int i = tid; i < (GP / 4) * WH; i += blockDim.x) {
+        const int y = i % WH, n4 = 4 * (i / WH);
+        float4 h;
+        h.x = n4 + 0 < G ? __ldg(&hy[(n4 + 0) * WH + y]) : 0.f;
+        h.y = n4 + 1 < G ? __ldg(&hy[(n4 + 1) * WH + y]) : 0.f;
+        h.z = n4 + 2 < G ? __ldg(&hy[(n4 + 2) * WH + y]) : 0.f;
+        h.w = n4 + 3 < G ? __ldg(&hy[(n4 + 3) * WH + y]) : 0.f;
+        *reinterpret_cast<float4*>(&hxP[(WW + y) * GP + n4]) = h;
+      }
+      staged_q = q;
+    }
+    __syncthreads();
+    const float2* Wt = win + (size_t)(item - i0) * WH * WW;   // column-major [c][r]
+    // IFFT along r (y) first, then along c (x)
+    ct_stage<6, WH, 1, WW, WH, 1, true>(Wt, T, twh);
+    __syncthreads();
+    ct_stage<7, WH, 6, WW, WH, 1, true>(T, F, twh);
+    __syncthreads();
+    ct_stage<6, WW, 1, WH, 1, WH, true>(F, T, tww);
+    __syncthreads();
+    float2 bc = make_float2(1.f, 0.f);
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if ((tid & 31) == 0) redf[tid >> 5] = lmax;
+    __syncthreads();
+    lmax = redf[0];
+#pragma unroll
+    for (int j = 1; j < 8; ++j) lmax = fmaxf(lmax, redf[j]);
+    if (p.raw)
+      for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = F[i];
+    const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
+    int16_t* fro = p.fr + (size_t)item * WH * WW;
+    int16_t* fio = p.fi + (size_t)item * WH * WW;
+    for (int i = tid; i < WH * WW / 2; i += blockDim.x) {
+      const float4 v = reinterpret_cast<const float4*>(F)[i];
+      const int r0 = __float2int_rn(__fmul_rn(v.x, scale)), im0 = __float2int_rn(__fmul_rn(v.y, scale));
+      const int r1 = __float2int_rn(__fmul_rn(v.z, scale)), im1 = __float2int_rn(__fmul_rn(v.w, scale));
+      reinterpret_cast<int*>(fro)[i] = (r0 & 0xffff) | (r1 << 16);
+      reinterpret_cast<int*>(fio)[i] = (im0 & 0xffff) | (im1 << 16);
+      reinterpret_cast<float4*>(F)[i] = make_float4((float)r0, (float)im0, (float)r1, (float)im1);
+    }
+    if (tid == 0) p.scale[item] = scale;
+    if (p.coefs && G > 0) {
+      const float* hxT = hxP;
+      const float* hyT = hxP + WW * GP;
+      __syncthreads();
+      const int GQ = GP >> 2;
+      for (int idx = tid; idx < WH * GQ; idx += blockDim.x) {
+        const int y = idx / GQ, mq = idx - y * GQ;
+        const float2* row = F + y * WW;
+        float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
+#pragma unroll 6
+        for (int x = 0; x < WW; ++x) {
+          const float2 v = row[x];
+          const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+          ar.x = fmaf(v.x, h.x, ar.x); ai.x = fmaf(v.y, h.x, ai.x);
+          ar.y = fmaf(v.x, h.y, ar.y); ai.y = fmaf(v.y, h.y, ai.y);
+          ar.z = fmaf(v.x, h.z, ar.z); ai.z = fmaf(v.y, h.z, ai.z);
+          ar.w = fmaf(v.x, h.w, ar.w); ai.w = fmaf(v.y, h.w, ai.w);
+        }
+        float2* u = U + y * GP + 4 * mq;
+        u[0] = make_float2(ar.x, ai.x);
+        u[1] = make_float2(ar.y, ai.y);
+        u[2] = make_float2(ar.z, ai.z);
+        u[3] = make_float2(ar.w, ai.w);
+      }
+      __syncthreads();
+      const float d = __fdiv_rn(g.dxdy[q], scale);
+      float2* out = p.coefs + (size_t)item * g.M;
+      for (int i = tid; i < g.M; i += blockDim.x) {
+        const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+        float ax = 0.f, ay = 0.f;
+#pragma unroll 6
+        for (int y = 0; y < WH; ++y) {
+          const float2 v = U[y * GP + m];
+          const float hv = hyT[y * GP + n];
+          ax = fmaf(v.x, hv, ax);
+          ay = fmaf(v.y, hv, ay);
+        }
+        out[i] = make_float2(ax * d, ay * d);
+      }
+    }
+  }
+}
+
+extern "C" int hpg_debug_trace(long long* out) {   // copies g_tc2_trace (2*64*8 int64) to host
+  return cudaMemcpyFromSymbol(out, g_tc2_trace, sizeof(g_tc2_trace)) == cudaSuccess ? 0 : 1;
+}
+
+constexpr int kTc2Chunk = 4096;   // items per K1/K2 pair: W (14 KB each) stays resident in L2
+
+bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
+                   const void* windows) {
+  const int es = fmt == 1 ? 2 : 4;
+  bool aligned = (g.W * es) % 16 == 0;   // cp.async.bulk rows: 16-byte aligned source
+  for (int q = 0; q < g.P; ++q) aligned = aligned && (g.col0[q] * es) % 16 == 0;
+  return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
+         g.L == 1 && g.G <= FieldLayout<42, 42>::GMAX && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
+         (flags & 1u) == 0 && windows == nullptr && aligned;
+}
+
+size_t tc2_workspace(int64_t items) {
+  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 42 * 42 * sizeof(float2);
+}
+
+cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
+  using LY = FieldLayout<42, 42>;
+  const int GP = (p.g.G + 3) & ~3;
+  const size_t k2_bytes = LY::basis + (size_t)(42 + 42) * std::max(GP, 4) * sizeof(float);
+  static bool configured = false;
+  static int k2_per_sm = 1;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fourier128_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kK1Bytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(field128_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(LY::basis + 84 * 48 * sizeof(float)));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k2_per_sm, field128_kernel<42, 42>, 256, k2_bytes);
+  float2* wbuf = reinterpret_cast<float2*>(p.work);
+  const int items = p.B * p.g.P;
+  for (int i0 = 0; i0 < items; i0 += kTc2Chunk) {
+    const int i1 = std::min(items, i0 + kTc2Chunk);
+    const int n = i1 - i0;
+    fourier128_tc2_kernel<<<std::max(1, std::min(n, num_sms)), kK1Threads, kK1Bytes, s>>>(p, ft, i0, i1, wbuf);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(
+        p, i0, i1, wbuf);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace holo

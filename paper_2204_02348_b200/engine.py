@@ -94,6 +94,7 @@ class Engine:
         self.force_generic = False      # diagnostic: bypass the specialised kernels
         self.force_simt = False         # diagnostic: specialised kernel without tensor cores
         self.use_tc = False             # tcgen05 row-pass kernel (HPG_FLAG_TC)
+        self.use_tc2 = False            # two-kernel tensor-core path (HPG_FLAG_TC2)
         self.last_h2d_bytes = 0
         self._ref_applied = None        # processed reference calibration (engine.py:75)
         self._plans = collections.OrderedDict()
@@ -497,7 +498,8 @@ class Engine:
         L.sc = self._buf("scale", (B, P), torch.float32)
         L.coefs = self._buf("coefs", (B, P * plan.mode_count), torch.complex64) if (with_coefs and G > 0) else None
         L.flags = ((native.HPG_FLAG_SUMMARY if summary else 0) | (native.HPG_FLAG_GENERIC if self.force_generic else 0)
-                   | (native.HPG_FLAG_SIMT if self.force_simt else 0) | (native.HPG_FLAG_TC if self.use_tc else 0))
+                   | (native.HPG_FLAG_SIMT if self.force_simt else 0) | (native.HPG_FLAG_TC if self.use_tc else 0)
+                   | (native.HPG_FLAG_TC2 if self.use_tc2 else 0))
         L.params = L.inten = None
         slots = B * A + 1
         if summary:

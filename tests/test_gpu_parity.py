@@ -190,3 +190,20 @@ def test_reference_calibration_table_matches_reference(name):
     eng.run_pipeline(2)
     fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
     assert rel_l2_rows(dequant(fr, fi, sc), dequant(g["fr"], g["fi"], g["scale"])) > 1e-2
+
+
+@pytest.mark.parametrize("name", ["pr1", "dualpol", "largebasis", "dualpol_cal"])
+def test_two_kernel_tensor_core_path_matches_reference(name):
+    """HPG_FLAG_TC2: row + column DFT on tcgen05 (fp16 split operands), SIMT field kernel."""
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.use_tc2 = True
+    eng.run_pipeline(0)
+    fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
+    ef = rel_l2_rows(dequant(fr, fi, sc), dequant(g["fr"], g["fi"], g["scale"]))
+    assert ef <= FIELD_TOL, f"{name}: field rel L2 {ef:.3e}"
+    lsb = max(np.abs(fr.astype(int) - g["fr"]).max(), np.abs(fi.astype(int) - g["fi"]).max())
+    assert lsb <= 2, f"{name}: {lsb} LSB"
+    assert np.allclose(sc, g["scale"], rtol=1e-5)
+    coefs, _, _, _ = eng.coef_view()
+    assert rel_l2_rows(coefs, g["coefs"]) <= COEF_TOL
