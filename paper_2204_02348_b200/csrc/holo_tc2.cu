@@ -19,6 +19,7 @@
 //     holopipe/hgbasis.py:101-116).
 // W lives in the workspace between the two launches; batches are processed in
 // chunks small enough for W to stay resident in L2.
+#include <cuda.h>
 #include <cuda_fp16.h>
 
 #include <algorithm>
@@ -41,10 +42,9 @@ constexpr int kN2 = 48;                     // column-DFT N per real part (42 co
 constexpr int kWinW = 42, kWinH = 42;
 
 // dynamic shared memory (bytes)
-constexpr uint32_t kLandPitch = 528;               // landing row pitch (512 B of f32 + 16 B pad)
-constexpr uint32_t kLandSlot = 32 * kLandPitch;    // 32 rows
-constexpr uint32_t kLand = 0;                      // 4 slots = one window, bulk-async copies
-constexpr uint32_t kStage = 4 * kLandSlot;         // [half][hi 16 KB | lo 16 KB]
+constexpr uint32_t kBox = 4096;                    // TMA box: 32 rows x 128 B (32 f32 / 64 u16), 128B swizzle
+constexpr uint32_t kLand = 0;                      // [chunk 4][box 4] = one window
+constexpr uint32_t kStage = 16 * kBox;             // [half][hi 16 KB | lo 16 KB]
 constexpr uint32_t kStageHalf = 32768;
 constexpr uint32_t kB2 = kStage + 2 * kStageHalf;  // B2 hi | B2 lo: rows c (Re R), 48 + c (Im R)
 constexpr uint32_t kB2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
@@ -80,29 +80,37 @@ __device__ long long g_tc2_trace[2][64][8];
     if (blockIdx.x == 0 && (kk) < 64) g_tc2_trace[role][kk][ev] = clock64();     \
   } while (0)
 
-// Issue the bulk copies of chunk j (rows 32j..32j+31) of an item's window (warp 0).
-HOLO_DEV void issue_chunk(const RunParams& p, int item, int j, char* smem, uint64_t* lfull, int lane) {
+// TMA (tensor map over the frame buffer [F][H][W]) of half h of an item's window:
+// chunks 2h, 2h+1 (32 rows each) x 4 boxes of 128 bytes per row, one thread.
+HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, int h, char* smem, uint64_t* bar) {
   const Geometry& g = p.g;
   const int b = item / g.P, q = item - b * g.P;
-  const int es = p.fmt == 0 ? 4 : 2;
-  const uint32_t rowb = 128u * es;
-  if (lane == 0) mbar_expect_tx(&lfull[j], 32u * rowb);
-  __syncwarp();
-  const int y = 32 * j + lane;
-  const char* src = reinterpret_cast<const char*>(p.frames) +
-                    ((int64_t)b * g.W * g.H + (int64_t)(g.row0[q] + y) * g.W + g.col0[q]) * es;
-  bulk_g2s(smem_u32(smem + kLand + j * kLandSlot + lane * kLandPitch), src, rowb, &lfull[j]);
+  const int bw = p.fmt == 0 ? 32 : 64;   // box width in elements (128 bytes)
+  const int nbox = 128 / bw;
+  mbar_expect_tx(bar, 2u * nbox * kBox);
+#pragma unroll 1
+  for (int jj = 0; jj < 2; ++jj) {
+    const int j = 2 * h + jj;
+    for (int qx = 0; qx < nbox; ++qx) {
+      const uint32_t dst = smem_u32(smem + kLand + (j * 4 + qx) * kBox);
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+          "l"(reinterpret_cast<uint64_t>(tmap)), "r"(g.col0[q] + qx * bw), "r"(g.row0[q] + 32 * j), "r"(b),
+          "r"(smem_u32(bar))
+          : "memory");
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kK1Threads, 1)
-    fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0,
-                          int i1, float2* __restrict__ wout) {
+    fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft,
+                          const __grid_constant__ CUtensorMap tmap, int i0, int i1, float2* __restrict__ wout) {
   extern __shared__ __align__(1024) char smem[];
   // lfull[j]: landing chunk j arrived; staged[h]: stage half h ready; meta[s]: fac[s] ready;
   // mma1[h]: row GEMM half h done; b2ready[h]: D1 half h drained into B2 (D1 half h free);
   // stfree[h]: stage half h consumed; full2: column GEMM done; d2free: D2 drained;
   // facfree[s]: fac[s] consumed
-  __shared__ __align__(8) uint64_t lfull[4], staged[2], meta[2], mma1[2], b2ready[2], stfree[2], full2, d2free,
+  __shared__ __align__(8) uint64_t lfull[2], staged[2], meta[2], mma1[2], b2ready[2], stfree[2], full2, d2free,
       facfree[2];
   __shared__ uint32_t tbase;
   __shared__ int emaxw[8];
@@ -118,7 +126,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&lfull[i], 1);
+    for (int i = 0; i < 2; ++i) mbar_init(&lfull[i], 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&staged[i], 1);
       mbar_init(&meta[i], 1);
@@ -140,11 +148,10 @@ __global__ void __launch_bounds__(kK1Threads, 1)
 
   if (warp < kMmaWarp) {
     // ================================= producer =================================
-    const int rl = lane >> 3, t8 = lane & 7;   // row (of 4 per warp per chunk), octet pair t8 / t8 + 8
+    const int r8 = lane & 7, gq = lane >> 3;   // row within the warp's 8, octet group
     int loaded_q = -1;
-    if (warp == 0)
-      for (int j = 0; j < 4; ++j)
-        if (i0 + (int)blockIdx.x < i1) issue_chunk(p, i0 + blockIdx.x, j, smem, lfull, lane);
+    if (tid == 0 && i0 + (int)blockIdx.x < i1)
+      for (int h = 0; h < 2; ++h) issue_half(p, &tmap, i0 + blockIdx.x, h, smem, &lfull[h]);
     int k = 0;
     for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
       const int s = k & 1;
@@ -173,57 +180,56 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       }
       int emax_t = -1000;
 #pragma unroll 1
-      for (int j = 0; j < 4; ++j) {   // chunk j = rows 32j..32j+31
-        const int h = j >> 1;
-        if ((j & 1) == 0 && k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done
-        if (tid == 0 && j == 0) TC2_MARK(0, k, 1);
-        mbar_wait_warp(&lfull[j], k & 1);
-        if (tid == 0 && j == 0) TC2_MARK(0, k, 6);
-        if (tid == 0 && j == 2) TC2_MARK(0, k, 7);
-        const int yl = 4 * warp + rl, y = 32 * j + yl;
-        const char* lrow = smem + kLand + j * kLandSlot + yl * kLandPitch;
-        float v[16];
-        if (p.fmt == 0) {
+      for (int h = 0; h < 2; ++h) {   // half h = rows 64h..64h+63; warp w -> rows 64h + 8w + r8
+        if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done
+        if (tid == 0 && h == 0) TC2_MARK(0, k, 1);
+        mbar_wait_warp(&lfull[h], k & 1);
+        if (tid == 0 && h == 0) TC2_MARK(0, k, 6);
+        if (tid == 0 && h == 1) TC2_MARK(0, k, 7);
+        const int yl = 8 * warp + r8, y = 64 * h + yl;
+        const int j = y >> 5, rb = y & 31;   // chunk, row in box
+        float v[32];   // octets o = gq + 4 i, i = 0..3
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const float4 a = *reinterpret_cast<const float4*>(lrow + (8 * t8 + 64 * u) * 4);
-            const float4 c = *reinterpret_cast<const float4*>(lrow + (8 * t8 + 64 * u) * 4 + 16);
-            v[8 * u + 0] = a.x; v[8 * u + 1] = a.y; v[8 * u + 2] = a.z; v[8 * u + 3] = a.w;
-            v[8 * u + 4] = c.x; v[8 * u + 5] = c.y; v[8 * u + 6] = c.z; v[8 * u + 7] = c.w;
-          }
-        } else {
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const uint4 a = *reinterpret_cast<const uint4*>(lrow + (8 * t8 + 64 * u) * 2);
+        for (int i = 0; i < 4; ++i) {
+          const int o = gq + 4 * i;
+          if (p.fmt == 0) {   // f32: box qx = o / 4, 16-byte chunks 2(o%4), 2(o%4)+1, swizzled by row
+            const char* box = smem + kLand + (j * 4 + (o >> 2)) * kBox + rb * 128;
+            const int c0 = (2 * (o & 3)) ^ (rb & 7), c1 = (2 * (o & 3) + 1) ^ (rb & 7);
+            const float4 a = *reinterpret_cast<const float4*>(box + c0 * 16);
+            const float4 c = *reinterpret_cast<const float4*>(box + c1 * 16);
+            v[8 * i + 0] = a.x; v[8 * i + 1] = a.y; v[8 * i + 2] = a.z; v[8 * i + 3] = a.w;
+            v[8 * i + 4] = c.x; v[8 * i + 5] = c.y; v[8 * i + 6] = c.z; v[8 * i + 7] = c.w;
+          } else {            // u16: box qx = o / 8, one 16-byte chunk o%8
+            const char* box = smem + kLand + (j * 4 + (o >> 3)) * kBox + rb * 128;
+            const uint4 a = *reinterpret_cast<const uint4*>(box + (((o & 7) ^ (rb & 7)) * 16));
             const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              v[8 * u + 2 * e] = (float)(w4[e] & 0xffffu);
-              v[8 * u + 2 * e + 1] = (float)(w4[e] >> 16);
+              v[8 * i + 2 * e] = (float)(w4[e] & 0xffffu);
+              v[8 * i + 2 * e + 1] = (float)(w4[e] >> 16);
             }
           }
         }
         float m = 0.f;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) m = fmaxf(m, fabsf(v[e]));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 1));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 2));
-        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 4));
+        for (int e = 0; e < 32; ++e) m = fmaxf(m, fabsf(v[e]));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
+        m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
         // exact power-of-two row scale: |f| * sc < 2^14, fh + fl keep 22 bits
         int e2 = 0;
         frexpf(m, &e2);
         const float sc = m > 0.f ? ldexpf(1.f, 14 - e2) : 1.f;
         const int ey = m > 0.f ? e2 : -1000;
-        if (t8 == 0) erow[y] = ey;
+        if (gq == 0) erow[y] = ey;
         emax_t = max(emax_t, ey);
         char* st = smem + kStage + h * kStageHalf;
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {   // octet x = 8 t8 + 64 u
-          const uint32_t off = kmaj_off(y & 63, 8 * t8 + 64 * u, 8);
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t off = kmaj_off(yl, 8 * (gq + 4 * i), 8);
           uint32_t hi2[4], lo2[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const float a = v[8 * u + 2 * e] * sc, c = v[8 * u + 2 * e + 1] * sc;
+            const float a = v[8 * i + 2 * e] * sc, c = v[8 * i + 2 * e + 1] * sc;
             hi2[e] = pack_h2(a, c);
             const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi2[e]));
             lo2[e] = pack_h2(a - back.x, c - back.y);
@@ -233,9 +239,11 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         }
         fence_async_smem();
         tc_fence_before();
-        nbar(kBarProd2, kProd2);   // chunk j consumed: landing slot j free, stage rows written
-        if (warp == 0 && nitem < i1) issue_chunk(p, nitem, j, smem, lfull, lane);
-        if (tid == 0 && (j & 1)) mbar_arrive(&staged[h]);
+        nbar(kBarProd2, kProd2);   // half h consumed: landing free, stage half written
+        if (tid == 0) {
+          mbar_arrive(&staged[h]);
+          if (nitem < i1) issue_half(p, &tmap, nitem, h, smem, &lfull[h]);
+        }
       }
       if (tid == 0) TC2_MARK(0, k, 2);
 #pragma unroll
@@ -580,8 +588,7 @@ constexpr int kTc2Chunk = 4096;   // items per K1/K2 pair: W (14 KB each) stays 
 bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
                    const void* windows) {
   const int es = fmt == 1 ? 2 : 4;
-  bool aligned = (g.W * es) % 16 == 0;   // cp.async.bulk rows: 16-byte aligned source
-  for (int q = 0; q < g.P; ++q) aligned = aligned && (g.col0[q] * es) % 16 == 0;
+  const bool aligned = (g.W * es) % 16 == 0;   // TMA tensor map: 16-byte row stride
   return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
          g.L == 1 && g.G <= FieldLayout<42, 42>::GMAX && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
          (flags & 1u) == 0 && windows == nullptr && aligned;
@@ -589,6 +596,32 @@ bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, c
 
 size_t tc2_workspace(int64_t items) {
   return (size_t)std::min<int64_t>(items, kTc2Chunk) * 42 * 42 * sizeof(float2);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// Tensor map over the frame buffer [B][H][W] (f32 or u16), 32-row x 128-byte boxes, 128B swizzle.
+static cudaError_t frame_tensor_map(const RunParams& p, CUtensorMap* map) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<EncodeTiledFn>(fn);
+  }
+  const cuuint64_t es = p.fmt == 0 ? 4 : 2;
+  const cuuint64_t dims[3] = {(cuuint64_t)p.g.W, (cuuint64_t)p.g.H, (cuuint64_t)std::max(p.B, 1)};
+  const cuuint64_t strides[2] = {(cuuint64_t)p.g.W * es, (cuuint64_t)p.g.W * p.g.H * es};
+  const cuuint32_t box[3] = {(cuuint32_t)(128 / es), 32, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode(map, p.fmt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
+                      const_cast<void*>(p.frames), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
@@ -608,11 +641,15 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k2_per_sm, field128_kernel<42, 42>, 256, k2_bytes);
   float2* wbuf = reinterpret_cast<float2*>(p.work);
+  CUtensorMap tmap;
+  cudaError_t te = frame_tensor_map(p, &tmap);
+  if (te != cudaSuccess) return te;
   const int items = p.B * p.g.P;
   for (int i0 = 0; i0 < items; i0 += kTc2Chunk) {
     const int i1 = std::min(items, i0 + kTc2Chunk);
     const int n = i1 - i0;
-    fourier128_tc2_kernel<<<std::max(1, std::min(n, num_sms)), kK1Threads, kK1Bytes, s>>>(p, ft, i0, i1, wbuf);
+    fourier128_tc2_kernel<<<std::max(1, std::min(n, num_sms)), kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1,
+                                                                                           wbuf);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(

@@ -33,10 +33,18 @@ HOLO_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
-// one lane polls, the rest of the warp waits at the warp barrier (keeps the
-// shared-memory pipe free for the warps doing work)
+// one lane waits (suspended in hardware up to the hint instead of spinning hot),
+// the rest of the warp waits at the warp barrier
 HOLO_DEV void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
-  if ((threadIdx.x & 31) == 0) mbar_wait(bar, phase);
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile(
+          "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p;}"
+          : "=r"(done)
+          : "r"(smem_u32(bar)), "r"(phase), "r"(1000000u));
+    }
+  }
   __syncwarp();
 }
 
