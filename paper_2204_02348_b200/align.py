@@ -103,6 +103,7 @@ def snap_estimate(eng):
         eng.process_fft()
     nx, ny, p, lam = cfg.fftWindowSizeX, cfg.fftWindowSizeY, cfg.framePixelSize, cfg.wavelengthCentre
     wmax = geometry.max_resolvable_angle(lam, p)
+    eng._fourier_axes_pair()
     tx_ax, ty_ax = eng._fourier_axes
     excl = (tx_ax[None, :].astype(np.float64) ** 2 + ty_ax[:, None].astype(np.float64) ** 2) < (wmax / 3.0) ** 2
     inten_all = eng.fourier_intensity_per_pol() if cfg.autoAlignTilt else None

@@ -97,6 +97,7 @@ class Engine:
         self.use_tc2 = False            # two-kernel tensor-core path (HPG_FLAG_TC2)
         self.last_h2d_bytes = 0
         self._ref_applied = None        # processed reference calibration (engine.py:75)
+        self._deferred = None           # host upload postponed by the pipelined process_batch
         self._plans = collections.OrderedDict()
         self._bufs = {}
         self._clear_products()
@@ -182,7 +183,7 @@ class Engine:
         plan = self._plan or self._batch_plan()
         lam = len(plan["lambdas"])
         if lam <= 1 or plan["batch"] % lam:
-            return np.arange(plan["batch"])
+            return None   # identity
         cfg = self.config
         return wavelength_reorder_indices(plan["batch"], lam,
                                           cfg.wavelengthOrdering[C.WAVELENGTHORDER_INPUT],
@@ -239,7 +240,7 @@ class Engine:
         return plan
 
     # ------------------------------------------------------------ stages
-    def process_fft(self):
+    def process_fft(self, _defer_upload=False):
         """Stage 0: window origins + frame staging (engine.py:135-168).
 
         The full R2C plane and its summary are produced on demand
@@ -257,16 +258,23 @@ class Engine:
         self._st0 = {"W": cfg.frameWidth, "H": cfg.frameHeight, "P": cfg.polCount, "nx": nx, "ny": ny,
                      "pixel": float(cfg.framePixelSize), "lambdas": [float(v) for v in plan["lambdas"]],
                      "centre": [list(map(float, cfg.beamCentre[0][:2])), list(map(float, cfg.beamCentre[1][:2]))]}
-        self._frames_dev = self._stage_frames(plan["frame_count"])
-        lam0, p = cfg.wavelengthCentre, cfg.framePixelSize
-        from .geometry import fourier_angle_axis
-        fx = fourier_angle_axis(np.arange(nx // 2 + 1), nx, p, lam0)
-        fy = fourier_angle_axis(np.fft.fftfreq(ny) * ny, ny, p, lam0)
-        self._fourier_axes_f64 = (fx, fy)
-        self._fourier_axes = (fx.astype(np.float32), fy.astype(np.float32))
+        self._frames_dev = self._stage_frames(plan["frame_count"], defer=_defer_upload)
+        self._fourier_axes_key = (nx, ny, float(cfg.framePixelSize), float(cfg.wavelengthCentre))
+        self._fourier_axes_f64 = None   # built on first use (Fourier-plane products only)
         return ErrorCode.SUCCESS
 
-    def _stage_frames(self, F):
+    def _fourier_axes_pair(self):
+        """Fourier-plane angle axes of stage 0 (engine.py:157-161), fp64 and float32."""
+        if self._fourier_axes_f64 is None:
+            from .geometry import fourier_angle_axis
+            nx, ny, p, lam0 = self._fourier_axes_key
+            fx = fourier_angle_axis(np.arange(nx // 2 + 1), nx, p, lam0)
+            fy = fourier_angle_axis(np.fft.fftfreq(ny) * ny, ny, p, lam0)
+            self._fourier_axes_f64 = (fx, fy)
+            self._fourier_axes = (fx.astype(np.float32), fy.astype(np.float32))
+        return self._fourier_axes_f64
+
+    def _stage_frames(self, F, defer=False):
         """Device copy of the frames the pipeline reads: (tensor, fmt, transpose, layout).
 
         Host sources (numpy / CPU tensors) are uploaded window-only
@@ -287,10 +295,12 @@ class Engine:
             P, nx, ny = st0["P"], st0["nx"], st0["ny"]
             packed = self._buf("packed", (F, ny, P * nx), torch.float32 if fmt == 0 else torch.int16)
             ptr = host.data_ptr() if hasattr(host, "data_ptr") else host.ctypes.data
-            with torch.cuda.device(self.device):
-                native.check(native.lib().hpg_upload_windows(plan0.handle, ctypes.c_void_p(ptr), fmt, F,
-                                                             native.ptr(packed), native.stream_handle()),
-                             "hpg_upload_windows")
+            self._deferred = (plan0, ptr, fmt, F) if defer else None
+            if not defer:
+                with torch.cuda.device(self.device):
+                    native.check(native.lib().hpg_upload_windows(plan0.handle, ctypes.c_void_p(ptr), fmt, F,
+                                                                 native.ptr(packed), native.stream_handle()),
+                                 "hpg_upload_windows")
             layout = (P * nx, ny, [q * nx for q in range(P)], [0, 0])
             self.last_h2d_bytes = packed.numel() * packed.element_size()
             return packed, fmt, 0, layout
@@ -592,8 +602,106 @@ class Engine:
         self.extract_coefs()
 
     def process_batch(self):
+        """run_pipeline(0) + coef_view (engine.py:404-417).
+
+        For host frames the upload, the fused kernel and the coefficient readback
+        are pipelined in chunks of rows (copy stream / compute stream), which is
+        the same computation on the same rows -- rows are independent."""
+        if self._pipeline_ok():
+            return self._process_batch_pipelined()
         self.run_pipeline(0)
         return self.coef_view()
+
+    _PIPE_CHUNKS = int(__import__("os").environ.get("HOLO_PIPE_CHUNKS", "4"))
+
+    def _pipeline_ok(self):
+        cfg, src = self.config, self.source
+        host = src.host_array() if src._pinned is None else None
+        return (host is not None and not (src.format() == 1 and src.transpose) and cfg.basisGroupCount >= 1
+                and max(1, cfg.avgCount) == 1 and cfg.basisType == C.BASISTYPE_HG
+                and not (self.batch_cal_enabled and self.batch_cal is not None)
+                and max(1, cfg.batchCount) >= 8 * self._PIPE_CHUNKS
+                and not (self.force_generic or self.force_simt))
+
+    def _process_batch_pipelined(self):
+        torch = _torch()
+        self.process_fft(_defer_upload=True)
+        plan0, hptr, fmt, F = self._deferred
+        self._deferred = None
+        B, P = self._plan["batch"], self._st0["P"]
+        W, H, nx, ny = self._st0["W"], self._st0["H"], self._st0["nx"], self._st0["ny"]
+        es = 4 if fmt == 0 else 2
+        packed = self._frames_dev[0]
+        dev = self.device
+        lib = native.lib()
+        bounds = np.linspace(0, B, self._PIPE_CHUNKS + 1).astype(int)
+        with torch.cuda.device(dev):
+            comp = torch.cuda.current_stream(dev)
+            copy, back = self._bufs.get("copy_stream"), self._bufs.get("back_stream")
+            if copy is None:
+                copy, back = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+                self._bufs["copy_stream"], self._bufs["back_stream"] = copy, back
+            copy.wait_stream(comp)   # buffers of the previous call are free
+            back.wait_stream(comp)
+            cs = ctypes.c_void_p(copy.cuda_stream)
+            ups = []
+            for c in range(self._PIPE_CHUNKS):   # every upload queued first: host work below overlaps them
+                r0, r1 = int(bounds[c]), int(bounds[c + 1])
+                if r1 > r0:
+                    native.check(lib.hpg_upload_windows(plan0.handle, ctypes.c_void_p(hptr + r0 * W * H * es), fmt,
+                                                        r1 - r0,
+                                                        ctypes.c_void_p(packed.data_ptr() + r0 * ny * P * nx * es),
+                                                        cs), "hpg_upload_windows")
+                ev = torch.cuda.Event()
+                ev.record(copy)
+                ups.append(ev)
+        self.process_ifft()
+        self._st2 = self._stage2_snapshot()
+        L = self._prepare_fused(with_coefs=True)
+        M = L.plan.mode_count
+        host_out = self._bufs.get("coefs_host")
+        if host_out is None or host_out.numel() < B * P * M:
+            host_out = torch.empty(B * P * M, dtype=torch.complex64).pin_memory()
+            self._bufs["coefs_host"] = host_out
+        with torch.cuda.device(dev):
+            ks = ctypes.c_void_p(comp.cuda_stream)
+            wl = L.batch.wl_of_row
+            hw = L.fr.shape[-1] * L.fr.shape[-2]
+            for c in range(self._PIPE_CHUNKS):
+                r0, r1 = int(bounds[c]), int(bounds[c + 1])
+                n = r1 - r0
+                if n == 0:
+                    continue
+                comp.wait_event(ups[c])
+                b = type(L.batch).from_buffer_copy(L.batch)
+                o = type(L.out).from_buffer_copy(L.out)
+                b.frames = packed.data_ptr() + r0 * ny * P * nx * es
+                b.frame_count = b.batch_count = n
+                if wl:
+                    b.wl_of_row = wl + r0 * 4
+                o.field_r = L.fr.data_ptr() + r0 * P * hw * 2
+                o.field_i = L.fi.data_ptr() + r0 * P * hw * 2
+                o.field_scale = L.sc.data_ptr() + r0 * P * 4
+                o.coefs = L.coefs.data_ptr() + r0 * P * M * 8
+                native.check(lib.hpg_run(L.plan.handle, ctypes.byref(b), ctypes.byref(o), L.flags, ks), "hpg_run")
+                done = torch.cuda.Event()
+                done.record(comp)
+                back.wait_event(done)   # readback on its own stream: uploads keep streaming
+                with torch.cuda.stream(back):
+                    host_out[r0 * P * M:r1 * P * M].copy_(L.coefs.view(-1)[r0 * P * M:r1 * P * M], non_blocking=True)
+            fin = torch.cuda.Event()
+            fin.record(back)
+            comp.wait_stream(copy)
+            comp.wait_stream(back)
+        self.last_h2d_bytes = packed.numel() * packed.element_size()
+        self._field_r, self._field_i, self._field_scale = L.fr, L.fi, L.sc
+        self._field_axes = L.plan.axes()
+        self._st3 = {"G": L.G, "waist": tuple(L.waist)}
+        self._finish_coefs(L.coefs, M, P)
+        fin.synchronize()
+        coefs = host_out[:B * P * M].numpy().reshape(B, P * M)
+        perm = self.output_permutation()
+        return (coefs.copy() if perm is None else coefs[perm]), B, self._mode_count, P
 
     def coef_view(self):
         plan = self._plan
@@ -602,8 +710,8 @@ class Engine:
                 return None, plan["batch"], 0, self.config.polCount
             return None, 0, 0, 0
         perm = self.output_permutation()
-        coefs = self._coefs.cpu().numpy()
-        return coefs[perm].copy(), plan["batch"], self._mode_count, self._st0["P"]
+        coefs = self._coefs.cpu().numpy()   # a fresh host array (copy-out, engine.py:416)
+        return (coefs if perm is None else coefs[perm]), plan["batch"], self._mode_count, self._st0["P"]
 
     def coefs_device(self):
         """Coefficients as a CUDA tensor (input row order), no host copy."""
@@ -635,9 +743,9 @@ class Engine:
             raise HoloError(ErrorCode.NULLPOINTER, "no processed fields")
         perm = self.output_permutation()
         x_axis, y_axis = self._field_axes
-        fr = self._field_r.cpu().numpy()[perm]
-        fi = self._field_i.cpu().numpy()[perm]
-        sc = self._field_scale.cpu().numpy()[perm]
+        fr, fi, sc = (t.cpu().numpy() for t in (self._field_r, self._field_i, self._field_scale))
+        if perm is not None:
+            fr, fi, sc = fr[perm], fi[perm], sc[perm]
         return (fr, fi, sc, x_axis, y_axis, x_axis.size, y_axis.size, self._plan["batch"], self._st0["P"])
 
     def get_fields(self):
@@ -710,7 +818,7 @@ class Engine:
     # ------------------------------------------------ AutoAlign reductions
     def fourier_intensity_per_pol(self):
         """sum_b |F|^2 over the full R2C plane per pol, fp64 (holopipe/align.py:53-55)."""
-        fx, fy = self._fourier_axes_f64
+        fx, fy = self._fourier_axes_pair()
         _, _, pt = self._plane_summary(self._fourier_plane_device(), fx, fy, pol_sums=True)
         return pt.cpu().numpy()
 
@@ -742,7 +850,7 @@ class Engine:
             if self._st0 is None:
                 raise HoloError(ErrorCode.NULLPOINTER, "plane has not been processed")
             if self._summary_fourier is None:
-                fx, fy = self._fourier_axes_f64
+                fx, fy = self._fourier_axes_pair()
                 params, inten = self._plane_summary(self._fourier_plane_device(), fx, fy)
                 self._summary_fourier = AnalysisSummary(params.cpu().numpy(), inten.cpu().numpy(),
                                                         self._fourier_axes[0], self._fourier_axes[1], plane_idx)
