@@ -279,6 +279,26 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
 
+    # DRAM traffic of the dominant kernel per launch, from the committed `ncu --set full`
+    # capture of the same command (profiles/ncu_traffic.json); rescaled per launch size
+    if args.tc2:
+        kernel_name = "holo::fourier128_tc2_kernel+holo::field128_kernel<42,42>"
+    elif args.tc:
+        kernel_name = "holo::fast128tc_kernel<42,42>"
+    elif nx == 128 and ny == 128 and gh == 42 and gw == 42:
+        kernel_name = "holo::fast128_kernel<42,42>"
+    else:
+        kernel_name = "holo::fused_kernel"
+    traffic = args.traffic_bytes
+    if traffic is None:
+        try:
+            with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")) as fh:
+                rec = json.load(fh).get(f"{args.config}/{kernel_name}")
+            if rec:
+                traffic = rec["dram_bytes_per_launch"] * B / rec["frames_per_launch"]
+        except (OSError, ValueError, KeyError):
+            traffic = None
+
     # ---------------- e2e through the public API with pinned host frames
     e2e = None
     if not args.no_e2e:
@@ -324,8 +344,8 @@ def main():
                        "pols": P, "fft_window": [ny, nx], "field": [int(gh), int(gw)], "modes_per_pol": int(M),
                        "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": args.traffic_bytes,
-                         "kernel": "holo::fast128tc_kernel<42,42>" if args.tc else "holo::fast128_kernel<42,42>", "bytes_per_frame": bpf,
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": kernel_name, "bytes_per_frame": bpf,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
