@@ -82,10 +82,26 @@ __device__ long long g_tc2_trace[2][64][8];
 
 // TMA (tensor map over the frame buffer [F][H][W]) of half h of an item's window:
 // chunks 2h, 2h+1 (32 rows each) x 4 boxes of 128 bytes per row, one thread.
+// W = (CrRr - CiRi) + i (CrRi + CiRr), masked, from the drain-2 exchange; thread -> column wc, rows wr0 + 6t
+HOLO_DEV void write_w(const float* X, float2* wo, int wc, int wr0, int wlo, int whi, float gs) {
+  if (wc >= kWinW) return;
+  wo += wc * kWinH;   // column-major [c][r]
+  const float* xa = X + wc * kXP;
+  const float* xb = X + kN2 * kXP + wc * kXP;
+#pragma unroll
+  for (int t = 0; t < 7; ++t) {
+    const int r = wr0 + 6 * t;
+    float2 w = make_float2(0.f, 0.f);
+    if (r >= wlo && r <= whi) w = make_float2((xa[r] - xb[kWinH + r]) * gs, (xb[r] + xa[kWinH + r]) * gs);
+    wo[r] = w;
+  }
+}
+
+template <int FMT>
 HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, int h, char* smem, uint64_t* bar) {
   const Geometry& g = p.g;
   const int b = item / g.P, q = item - b * g.P;
-  const int bw = p.fmt == 0 ? 32 : 64;   // box width in elements (128 bytes)
+  constexpr int bw = FMT == 0 ? 32 : 64;   // box width in elements (128 bytes)
   const int nbox = 128 / bw;
   mbar_expect_tx(bar, 2u * nbox * kBox);
 #pragma unroll 1
@@ -102,6 +118,7 @@ HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, 
   }
 }
 
+template <int FMT>
 __global__ void __launch_bounds__(kK1Threads, 1)
     fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft,
                           const __grid_constant__ CUtensorMap tmap, int i0, int i1, float2* __restrict__ wout) {
@@ -151,7 +168,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     const int r8 = lane & 7, gq = lane >> 3;   // row within the warp's 8, octet group
     int loaded_q = -1;
     if (tid == 0 && i0 + (int)blockIdx.x < i1)
-      for (int h = 0; h < 2; ++h) issue_half(p, &tmap, i0 + blockIdx.x, h, smem, &lfull[h]);
+      for (int h = 0; h < 2; ++h) issue_half<FMT>(p, &tmap, i0 + blockIdx.x, h, smem, &lfull[h]);
     int k = 0;
     for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
       const int s = k & 1;
@@ -179,7 +196,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         loaded_q = q;
       }
       int emax_t = -1000;
-#pragma unroll 1
+#pragma unroll
       for (int h = 0; h < 2; ++h) {   // half h = rows 64h..64h+63; warp w -> rows 64h + 8w + r8
         if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done
         if (tid == 0 && h == 0) TC2_MARK(0, k, 1);
@@ -192,7 +209,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int o = gq + 4 * i;
-          if (p.fmt == 0) {   // f32: box qx = o / 4, 16-byte chunks 2(o%4), 2(o%4)+1, swizzled by row
+          if (FMT == 0) {   // f32: box qx = o / 4, 16-byte chunks 2(o%4), 2(o%4)+1, swizzled by row
             const char* box = smem + kLand + (j * 4 + (o >> 2)) * kBox + rb * 128;
             const int c0 = (2 * (o & 3)) ^ (rb & 7), c1 = (2 * (o & 3) + 1) ^ (rb & 7);
             const float4 a = *reinterpret_cast<const float4*>(box + c0 * 16);
@@ -242,7 +259,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         nbar(kBarProd2, kProd2);   // half h consumed: landing free, stage half written
         if (tid == 0) {
           mbar_arrive(&staged[h]);
-          if (nitem < i1) issue_half(p, &tmap, nitem, h, smem, &lfull[h]);
+          if (nitem < i1) issue_half<FMT>(p, &tmap, nitem, h, smem, &lfull[h]);
         }
       }
       if (tid == 0) TC2_MARK(0, k, 2);
@@ -319,7 +336,10 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     const int ct = tid - kProd2 - 32, cw = warp - kConsWarp0, quarter = warp & 3, sub = cw >> 2;
     char* b2 = smem + kB2;
     float* X = reinterpret_cast<float*>(smem + kX);
-    int loaded_q = -1;
+    const int wc = ct / 6, wr0 = ct - 6 * wc;   // W pass: 42 columns x 6 row phases
+    const int wlo = wc < kWinW ? crs[2 * wc] : 0, whi = wc < kWinW ? crs[2 * wc + 1] : -1;
+    int loaded_q = -1, prev_item = 0;
+    float gs_prev = 0.f;
     int k = 0;
     for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
       const int s = k & 1;
@@ -348,7 +368,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       const int n = quarter * 32 + lane, c = n & 63;
       const int brow = (n >= 64 ? kN2 : 0) + c;   // B2 row: Re R rows then Im R rows
       const float* fs = fac + s * 128;
-#pragma unroll 1
+#pragma unroll
       for (int h = 0; h < 2; ++h) {
         mbar_wait_warp(&mma1[h], k & 1);
         tc_fence_after();
@@ -388,6 +408,9 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         }
       }
       const float gs = ldexpf(1.f, emaxs[s] - 8);
+      // W of the previous window while this window's column GEMM runs (X still holds its partials)
+      if (k >= 1) write_w(X, wout + (size_t)(prev_item - i0) * kWinH * kWinW, wc, wr0, wlo, whi, gs_prev);
+      nbar(kBarCons2, kCons2);   // X free for this window's drain
       mbar_wait_warp(&full2, k & 1);
       tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 3);
@@ -414,26 +437,11 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         mbar_arrive(&d2free);
         TC2_MARK(1, k, 4);
       }
-
-      // ------------------------------- W = (CrRr - CiRi) + i (CrRi + CiRr), masked
-      {
-        float2* wo = wout + (size_t)(item - i0) * kWinH * kWinW;
-        const float* Xa = X;
-        const float* Xb = X + kN2 * kXP;
-        for (int i = ct; i < kWinH * kWinW; i += kCons2) {
-          const int cc = i / kWinH, r = i - cc * kWinH;
-          float2 w = make_float2(0.f, 0.f);
-          if (r >= crs[2 * cc] && r <= crs[2 * cc + 1]) {
-            const float* xa = Xa + cc * kXP;
-            const float* xb = Xb + cc * kXP;
-            w = make_float2((xa[r] - xb[kWinH + r]) * gs, (xb[r] + xa[kWinH + r]) * gs);
-          }
-          wo[i] = w;   // column-major [c][r]
-        }
-      }
-      nbar(kBarCons2, kCons2);   // X free for the next window
+      prev_item = item;
+      gs_prev = gs;
       if (ct == 0) TC2_MARK(1, k, 5);
     }
+    if (k >= 1) write_w(X, wout + (size_t)(prev_item - i0) * kWinH * kWinW, wc, wr0, wlo, whi, gs_prev);
   }
   tc_fence_before();
   __syncthreads();
@@ -631,8 +639,10 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
   static bool configured = false;
   static int k2_per_sm = 1;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fourier128_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(fourier128_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kK1Bytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fourier128_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK1Bytes);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(field128_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(LY::basis + 84 * 48 * sizeof(float)));
@@ -648,8 +658,11 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
   for (int i0 = 0; i0 < items; i0 += kTc2Chunk) {
     const int i1 = std::min(items, i0 + kTc2Chunk);
     const int n = i1 - i0;
-    fourier128_tc2_kernel<<<std::max(1, std::min(n, num_sms)), kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1,
-                                                                                           wbuf);
+    const int g1 = std::max(1, std::min(n, num_sms));
+    if (p.fmt == 0)
+      fourier128_tc2_kernel<0><<<g1, kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1, wbuf);
+    else
+      fourier128_tc2_kernel<1><<<g1, kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1, wbuf);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(
