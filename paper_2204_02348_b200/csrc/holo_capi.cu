@@ -138,19 +138,37 @@ std::vector<double> hg_profiles(int G, const std::vector<float>& axis, double wa
 }
 
 // int16 quantisation + float32 dequantisation of the profiles (hgbasis.py:84-93).
-void quantised_basis(int G, const std::vector<float>& axis, double waist, float* out) {
+void quantised_basis(int G, const std::vector<float>& axis, double waist, float* out,
+                     std::vector<int16_t>* q16 = nullptr, std::vector<float>* scales = nullptr) {
   const std::vector<double> h = hg_profiles(G, axis, waist);
   const size_t n = axis.size();
+  if (q16) q16->assign((size_t)G * n, 0);
+  if (scales) scales->assign(G, 1.f);
   for (int k = 0; k < G; ++k) {
     double mx = 0.0;
     for (size_t i = 0; i < n; ++i) mx = std::fmax(mx, std::fabs(h[(size_t)k * n + i]));
     const float scale = 32767.0f / (float)mx;
+    if (scales) (*scales)[k] = scale;
     for (size_t i = 0; i < n; ++i) {
       const double qv = std::nearbyint(h[(size_t)k * n + i] * (double)scale);
       const int16_t q = (int16_t)qv;
       out[(size_t)k * n + i] = (float)q / scale;
+      if (q16) (*q16)[(size_t)k * n + i] = q;
     }
   }
+}
+
+// Tensor-core overlap operand (holo_fast.cu, TCO): int16 basis q = 32 (q >> 5) + (q & 31) split into
+// two exactly-representable fp16 parts, in the UMMA K-major layout [row/8][kstep 3][khalf][row%8][8],
+// rows = orders (GP16 = G rounded up to 16), K = the 42 axis samples padded to 48.
+void tco_image(const std::vector<int16_t>& q, int G, int GP16, int n, uint16_t* hi, uint16_t* lo) {
+  for (int m = 0; m < GP16; ++m)
+    for (int k = 0; k < 48; ++k) {
+      const int v = (m < G && k < n) ? q[(size_t)m * n + k] : 0;
+      const size_t e = ((size_t)(m >> 3) * 3 + (k >> 4)) * 128 + (size_t)((k >> 3) & 1) * 64 + (m & 7) * 8 + (k & 7);
+      hi[e] = __half_as_ushort(__float2half((float)(32 * (v >> 5))));
+      lo[e] = __half_as_ushort(__float2half((float)(v & 31)));
+    }
 }
 
 template <typename T>
@@ -352,11 +370,27 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->hx.assign((size_t)g.P * G * g.gw, 0.f);
   P->hy.assign((size_t)g.P * G * g.gh, 0.f);
   std::vector<int16_t> mm, mn;
+  const int GP16 = std::max(16, (G + 15) & ~15);
+  const bool tco_ok = G > 0 && GP16 <= 48 && g.gw == 42 && g.gh == 42;
+  const size_t tco_part = (size_t)GP16 * 48;   // halves per operand part
+  std::vector<uint16_t> tco_img(tco_ok ? (size_t)g.P * 4 * tco_part : 1, 0);
+  std::vector<float> tco_inv(tco_ok ? (size_t)g.P * 2 * GP16 : 1, 0.f);
   if (G > 0) {
     for (int q = 0; q < g.P; ++q) {
       if (!(d->waist[q] > 0)) { delete P; return fail(HPG_INVALIDDIMENSION, "basis waist must be positive"); }
-      quantised_basis(G, P->xa, d->waist[q], &P->hx[(size_t)q * G * g.gw]);
-      quantised_basis(G, P->ya, d->waist[q], &P->hy[(size_t)q * G * g.gh]);
+      std::vector<int16_t> qx, qy;
+      std::vector<float> sx, sy;
+      quantised_basis(G, P->xa, d->waist[q], &P->hx[(size_t)q * G * g.gw], &qx, &sx);
+      quantised_basis(G, P->ya, d->waist[q], &P->hy[(size_t)q * G * g.gh], &qy, &sy);
+      if (tco_ok) {
+        uint16_t* img = &tco_img[(size_t)q * 4 * tco_part];
+        tco_image(qx, G, GP16, g.gw, img, img + tco_part);
+        tco_image(qy, G, GP16, g.gh, img + 2 * tco_part, img + 3 * tco_part);
+        for (int m = 0; m < G; ++m) {
+          tco_inv[((size_t)q * 2 + 0) * GP16 + m] = 1.f / sx[m];
+          tco_inv[((size_t)q * 2 + 1) * GP16 + m] = 1.f / sy[m];
+        }
+      }
     }
     for (int gg = 0; gg < G; ++gg)
       for (int m = gg; m >= 0; --m) { mm.push_back((int16_t)m); mn.push_back((int16_t)(gg - m)); }
@@ -453,6 +487,7 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->fill = d->fill_factor;
   std::vector<char> blob;
   const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange), o_atc = push(blob, a_tc), o_a2 = push(blob, a2_tc);
+  const size_t o_timg = push(blob, tco_img), o_tinv = push(blob, tco_inv);
   const size_t o_nx = push(blob, tw_nx), o_ny = push(blob, tw_ny), o_gw = push(blob, tw_gw), o_gh = push(blob, tw_gh);
   const size_t o_w = push(blob, wtab), o_rx = push(blob, remx), o_ry = push(blob, remy);
   std::vector<float> hxv = P->hx, hyv = P->hy;
@@ -490,6 +525,9 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.crange = reinterpret_cast<const int16_t*>(base + o_cr);
   P->ft.a_tc = reinterpret_cast<const uint32_t*>(base + o_atc);
   P->ft.a2_tc = reinterpret_cast<const uint32_t*>(base + o_a2);
+  P->ft.tco_img = tco_ok ? reinterpret_cast<const uint4*>(base + o_timg) : nullptr;
+  P->ft.tco_inv = reinterpret_cast<const float*>(base + o_tinv);
+  P->ft.tco_gp = tco_ok ? GP16 : 0;
   e = set_smem_limits();
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
   *out = P;

@@ -29,6 +29,7 @@
 
 #include "holo_internal.h"
 #include "holo_fast_common.cuh"
+#include "holo_tc_common.cuh"
 
 namespace holo {
 
@@ -58,7 +59,138 @@ struct FastLayout {
 constexpr int kPersistentBasisGP = 36;
 HOLO_DEV bool persistent_basis(int GP) { return GP <= kPersistentBasisGP; }
 
+// Tensor-core HG overlap (TCO): operands in shared memory, UMMA K-major layout
+// [row/8][kstep 3][khalf][row%8][8 halves] (SBO 768 B, kstep 256 B, LBO 128 B).
+//   GEMM 1: U[(Re y | Im 48+y)][m] = sum_x F16[y][x] qx[m][x]   M=128 N=GP16 K=48
+//   GEMM 2: C[(Re m | Im 48+m)][n] = sum_y U[y][m] qy[n][y]      (U scaled by 2^-22, fp16 hi/lo)
+// F16 (the int16 field) and q (the int16 basis) split exactly as 32 (v >> 5) + (v & 31).
+constexpr unsigned kFlagNoTco = 32u;          // HPG_FLAG_SIMT_OVERLAP
+constexpr uint32_t kTcoA = 16384;              // A operand (F16 split, then U split) at zs + 16 KB
+constexpr uint32_t kTcoPart = 12 * 768;        // one part: 96 rows x 48 K halves
+HOLO_DEV uint32_t tco_off(int row, int k) {    // byte offset of (row, k) in one operand part
+  return (uint32_t)(row >> 3) * 768 + (uint32_t)(k >> 4) * 256 + (uint32_t)((k >> 3) & 1) * 128 +
+         (uint32_t)(row & 7) * 16 + (uint32_t)(k & 7) * 2;
+}
+HOLO_DEV void mma_f16_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{.reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// The overlap of one item on the tensor cores.  On entry the A operand (the int16 field split)
+// is complete in shared memory except the padding rows; B operands are staged into `bsm`.
 template <int WH, int WW>
+HOLO_DEV void tco_overlap(const RunParams& p, const FastTables& ft, int item, int q, float scale, char* A, char* bsm,
+                          uint32_t tm, uint64_t* bar, uint32_t& phase) {
+  const Geometry& g = p.g;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = g.G, GP = ft.tco_gp;
+  const uint32_t part = (uint32_t)GP * 96;   // bytes of one B part (GP rows x 48 halves)
+  {   // padding rows 42..47 and 90..95 of A (all K, both parts): 12 rows x 6 chunks x 2
+    for (int i = tid; i < 12 * 6 * 2; i += blockDim.x) {
+      const int pr = i / 12, rr = i - pr * 12, row = rr < 6 ? WH + rr : 48 + WH + (rr - 6);
+      const int kc = pr % 6, pt = pr / 6;
+      *reinterpret_cast<uint4*>(A + pt * kTcoPart + tco_off(row, 8 * kc)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    // B images of this pol (hx hi | hx lo | hy hi | hy lo)
+    const uint4* src = ft.tco_img + (size_t)q * 4 * part / 16;
+    for (int i = tid; i < (int)(4 * part / 16); i += blockDim.x) reinterpret_cast<uint4*>(bsm)[i] = __ldg(src + i);
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t idesc = idesc_f16(128, GP);
+  const uint32_t sa = smem_u32(A), sb = smem_u32(bsm);
+  if (tid == 0) {   // GEMM 1: D1[row][m] = sum_x A[row][x] qx[m][x]
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) {
+      const uint64_t ah = umma_desc(sa + ks * 256, 128, 768), al = umma_desc(sa + kTcoPart + ks * 256, 128, 768);
+      const uint64_t bh = umma_desc(sb + ks * 256, 128, 768), bl = umma_desc(sb + part + ks * 256, 128, 768);
+      mma_f16_ss(tm, ah, bh, idesc, ks != 0);
+      mma_f16_ss(tm, ah, bl, idesc, 1);
+      mma_f16_ss(tm, al, bh, idesc, 1);
+      mma_f16_ss(tm, al, bl, idesc, 1);   // all four integer products: GEMM 1 is exact
+    }
+    tc_commit(bar);
+  }
+  mbar_wait(bar, phase & 1);
+  ++phase;
+  tc_fence_after();
+  {   // drain D1 -> A (now the GEMM-2 operand U^T: rows Re m | Im 48+m, K = y), scaled by 2^-22
+    const int quarter = warp & 3, hcol = warp >> 2;
+    const int row = quarter * 32 + lane;   // D1 row: Re y (< 48) or Im y (48..95)
+    const int yy = row < 48 ? row : row - 48, im = row >= 48;
+    const int half = GP / 2;
+    for (int c0 = hcol * half; c0 < (hcol + 1) * half; c0 += 8) {
+      uint32_t r[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(tm + ((uint32_t)(quarter * 32) << 16) + c0));
+      tmem_wait_ld();
+      if (row < 96) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float u = __uint_as_float(r[e]) * 2.384185791015625e-07f;   // 2^-22
+          const __half h = __float2half_rn(u);
+          const __half l = __float2half_rn(u - __half2float(h));
+          const int m = c0 + e;
+          const uint32_t o = tco_off(im * 48 + m, yy);
+          *reinterpret_cast<__half*>(A + o) = h;
+          *reinterpret_cast<__half*>(A + kTcoPart + o) = l;
+        }
+      }
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {   // GEMM 2: D2[row2][n] = sum_y A[row2][y] qy[n][y]
+#pragma unroll
+    for (int ks = 0; ks < 3; ++ks) {
+      const uint64_t ah = umma_desc(sa + ks * 256, 128, 768), al = umma_desc(sa + kTcoPart + ks * 256, 128, 768);
+      const uint64_t bh = umma_desc(sb + 2 * part + ks * 256, 128, 768),
+                     bl = umma_desc(sb + 3 * part + ks * 256, 128, 768);
+      mma_f16_ss(tm + 64, ah, bh, idesc, ks != 0);
+      mma_f16_ss(tm + 64, al, bh, idesc, 1);
+      mma_f16_ss(tm + 64, ah, bl, idesc, 1);
+    }
+    tc_commit(bar);
+  }
+  mbar_wait(bar, phase & 1);
+  ++phase;
+  tc_fence_after();
+  {   // drain D2 -> coefficients (group-major index of (m, n), engine.py / hgbasis.py:17-27)
+    const int quarter = warp & 3, hcol = warp >> 2;
+    const int row = quarter * 32 + lane;
+    const int m = row < 48 ? row : row - 48, im = row >= 48;
+    const float d = __fdiv_rn(g.dxdy[q], scale) * 4194304.f;   // 2^22 undoes the U scaling
+    const float* invx = ft.tco_inv + (size_t)q * 2 * GP;
+    const float* invy = invx + GP;
+    float* out = reinterpret_cast<float*>(p.coefs + (size_t)item * g.M) + im;
+    const float fm = (row < 96 && m < G) ? d * __ldg(&invx[m]) : 0.f;
+    const int half = GP / 2;
+    for (int c0 = hcol * half; c0 < (hcol + 1) * half; c0 += 8) {
+      uint32_t r[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                   : "r"(tm + 64 + ((uint32_t)(quarter * 32) << 16) + c0));
+      tmem_wait_ld();
+      if (row < 96 && m < G) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int n = c0 + e, gg = m + n;
+          if (gg < G) out[2 * (gg * (gg + 1) / 2 + n)] = __uint_as_float(r[e]) * fm * __ldg(&invy[n]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+}
+
+template <int WH, int WW, bool TCO>
 __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__ RunParams p,
                                                         const __grid_constant__ FastTables ft) {
   using LY = FastLayout<WH, WW>;
@@ -83,6 +215,22 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
   for (int i = tid; i < 128; i += blockDim.x) tw128[i] = p.t.tw_nx[((i >> 3) * (i & 7)) & 127];
   for (int i = tid; i < WH; i += blockDim.x) twh[i] = p.t.tw_gh[i];
   for (int i = tid; i < WW; i += blockDim.x) tww[i] = p.t.tw_gw[i];
+  __shared__ __align__(8) uint64_t tco_bar;
+  __shared__ uint32_t tco_tbase;
+  uint32_t tco_phase = 0;
+  if (TCO) {
+    if ((tid >> 5) == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tco_tbase)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+      mbar_init(&tco_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
 
   const int items = p.B * g.P;
   int staged_q = -1;
@@ -235,14 +383,37 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
       const int r1 = __float2int_rn(__fmul_rn(v.z, scale)), i1 = __float2int_rn(__fmul_rn(v.w, scale));
       reinterpret_cast<int*>(fro)[i] = (r0 & 0xffff) | (r1 << 16);
       reinterpret_cast<int*>(fio)[i] = (i0 & 0xffff) | (i1 << 16);
-      // integer-valued copy for the overlap; the 1/scale of the dequantisation
-      // (holopipe/engine.py:367-369) is applied once to each coefficient
-      reinterpret_cast<float4*>(F)[i] = make_float4((float)r0, (float)i0, (float)r1, (float)i1);
+      if (TCO) {   // exact fp16 split of the int16 field into the GEMM-1 A operand (rows Re y | Im 48+y)
+        const int y = (2 * i) / WW, x = 2 * i - y * WW;
+        char* A = reinterpret_cast<char*>(zs) + kTcoA;
+        const uint32_t hr = pack_h2((float)(32 * (r0 >> 5)), (float)(32 * (r1 >> 5)));
+        const uint32_t lr = pack_h2((float)(r0 & 31), (float)(r1 & 31));
+        const uint32_t hi_ = pack_h2((float)(32 * (i0 >> 5)), (float)(32 * (i1 >> 5)));
+        const uint32_t li = pack_h2((float)(i0 & 31), (float)(i1 & 31));
+        if (x == WW - 2) {   // last pair of the row: also clear the K padding x = WW .. 47 (16-byte chunk)
+          *reinterpret_cast<uint4*>(A + tco_off(y, x)) = make_uint4(hr, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(A + kTcoPart + tco_off(y, x)) = make_uint4(lr, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(A + tco_off(48 + y, x)) = make_uint4(hi_, 0u, 0u, 0u);
+          *reinterpret_cast<uint4*>(A + kTcoPart + tco_off(48 + y, x)) = make_uint4(li, 0u, 0u, 0u);
+        } else {
+          *reinterpret_cast<uint32_t*>(A + tco_off(y, x)) = hr;
+          *reinterpret_cast<uint32_t*>(A + kTcoPart + tco_off(y, x)) = lr;
+          *reinterpret_cast<uint32_t*>(A + tco_off(48 + y, x)) = hi_;
+          *reinterpret_cast<uint32_t*>(A + kTcoPart + tco_off(48 + y, x)) = li;
+        }
+      } else {
+        // integer-valued copy for the overlap; the 1/scale of the dequantisation
+        // (holopipe/engine.py:367-369) is applied once to each coefficient
+        reinterpret_cast<float4*>(F)[i] = make_float4((float)r0, (float)i0, (float)r1, (float)i1);
+      }
     }
     if (tid == 0) p.scale[item] = scale;
 
     // ---------------------------------------------------------- HG overlap
-    if (p.coefs && g.G > 0) {
+    if (TCO && p.coefs && g.G > 0) {
+      tco_overlap<WH, WW>(p, ft, item, q, scale, reinterpret_cast<char*>(zs) + kTcoA,
+                          reinterpret_cast<char*>(xbuf), tco_tbase, &tco_bar, tco_phase);
+    } else if (p.coefs && g.G > 0) {
       const int G = g.G, GP = (G + 3) & ~3;
       // basis, transposed to [x][m] so one 16-byte load gives 4 orders: kept for
       // the CTA's lifetime when it fits (items of one CTA share a pol whenever
@@ -313,6 +484,12 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
       }
     }
   }
+  if (TCO) {
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if ((tid >> 5) == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tco_tbase));
+  }
 }
 
 bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
@@ -329,16 +506,28 @@ cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, c
                                         ? (size_t)(42 + 42) * GP * sizeof(float) : 0);
   static size_t configured = 0;
   if (bytes > configured) {
-    cudaError_t e = cudaFuncSetAttribute(fast128_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(fast128_kernel<42, 42, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(fast128_kernel<42, 42, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bytes);
     if (e != cudaSuccess) return e;
     configured = bytes;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast128_kernel<42, 42>, 256, bytes);
+  // tensor-core overlap pays for large bases (G > 16: config 5 G = 45 +32 %); below that its two MMA
+  // round trips per item cost more than the SIMT overlap they replace (dual-pol G = 14: -10 %)
+  const bool tco = ft.tco_gp >= 32 && p.coefs && p.g.G > 0 && !(p.flags & kFlagNoTco);
+  // same registers / shared memory for both variants; the occupancy API reports 1 CTA/SM for kernels that
+  // allocate tensor memory, but 3 x 128 TMEM columns fit the SM's 512
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast128_kernel<42, 42, false>, 256, bytes);
+  if (tco) per_sm = std::min(per_sm, 4);
   const int items = p.B * p.g.P;
   const int grid = std::max(1, std::min(items, num_sms * std::max(per_sm, 1)));
-  fast128_kernel<42, 42><<<grid, 256, bytes, s>>>(p, ft);
+  if (tco)
+    fast128_kernel<42, 42, true><<<grid, 256, bytes, s>>>(p, ft);
+  else
+    fast128_kernel<42, 42, false><<<grid, 256, bytes, s>>>(p, ft);
   return cudaGetLastError();
 }
 

@@ -95,6 +95,7 @@ class Engine:
         self.force_simt = False         # diagnostic: specialised kernel without tensor cores
         self.use_tc = False             # tcgen05 row-pass kernel (HPG_FLAG_TC)
         self.use_tc2 = False            # two-kernel tensor-core path (HPG_FLAG_TC2)
+        self.simt_overlap = False       # diagnostic: HG overlap on SIMT (HPG_FLAG_SIMT_OVERLAP)
         self.last_h2d_bytes = 0
         self._ref_applied = None        # processed reference calibration (engine.py:75)
         self._deferred = None           # host upload postponed by the pipelined process_batch
@@ -509,7 +510,8 @@ class Engine:
         L.coefs = self._buf("coefs", (B, P * plan.mode_count), torch.complex64) if (with_coefs and G > 0) else None
         L.flags = ((native.HPG_FLAG_SUMMARY if summary else 0) | (native.HPG_FLAG_GENERIC if self.force_generic else 0)
                    | (native.HPG_FLAG_SIMT if self.force_simt else 0) | (native.HPG_FLAG_TC if self.use_tc else 0)
-                   | (native.HPG_FLAG_TC2 if self.use_tc2 else 0))
+                   | (native.HPG_FLAG_TC2 if self.use_tc2 else 0)
+                   | (native.HPG_FLAG_SIMT_OVERLAP if self.simt_overlap else 0))
         L.params = L.inten = None
         slots = B * A + 1
         if summary:

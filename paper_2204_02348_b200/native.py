@@ -25,6 +25,7 @@ HPG_FLAG_GENERIC = 2
 HPG_FLAG_SIMT = 4
 HPG_FLAG_TC = 8
 HPG_FLAG_TC2 = 16
+HPG_FLAG_SIMT_OVERLAP = 32
 
 # Every symbol include/holo_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = [

@@ -118,6 +118,14 @@ CASES = {
         config=_cfg(frameWidth=256, frameHeight=256, polCount=1, batchCount=2,
                     fftWindowSizeX=256, fftWindowSizeY=256, tilt=[[1.0, 1.0], [1.0, 1.0]],
                     basisGroupCount=6, basisWaist=[256 * PIX / 6] * 2)),
+    # dual-pol with a 24-group basis (300 modes/pol): the tensor-core overlap with per-pol basis operands
+    "dualpol_g24": dict(
+        frames=dict(width=640, height=256, pol_count=2, batch=2, group_count=24,
+                    waist=200e-6, tilt=(1.2, 0.9), noise="poisson", seed=23),
+        config=_cfg(frameWidth=640, frameHeight=256, polCount=2, batchCount=2,
+                    tilt=[[1.2, 1.2], [0.9, 0.9]], basisGroupCount=24,
+                    basisWaist=[200e-6, 180e-6], polLockBasisWaist=0,
+                    beamCentre=[[-160 * PIX, 160 * PIX], [0.0, 0.0]])),
     # reference-wave calibration, intensity kind (holopipe/engine.py:276-335)
     "refcal_int": dict(
         frames=dict(width=256, height=256, pol_count=1, batch=3, group_count=6,

@@ -241,3 +241,19 @@ def test_pipelined_process_batch_matches_staged(name):
     # second call reuses the buffers
     cc, _, _, _ = a.process_batch()
     assert np.array_equal(cc, ca)
+
+
+@pytest.mark.parametrize("name", ["largebasis", "dualpol_g24"])
+def test_tensor_core_overlap_matches_simt_overlap(name):
+    """HG overlap on tcgen05 (exact int16 splits) vs the SIMT overlap: same fields, coefs within 2e-6."""
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.run_pipeline(0)
+    a = [t.cpu().numpy().copy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy().copy()]
+    eng.simt_overlap = True
+    eng.run_pipeline(0)
+    b = [t.cpu().numpy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()]
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+    assert rel_l2_rows(a[3], b[3]) <= 2e-6
+    assert rel_l2_rows(a[3], g["coefs"]) <= COEF_TOL
