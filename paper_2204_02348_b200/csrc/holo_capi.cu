@@ -2,6 +2,7 @@
 // table upload, workspace sizing and kernel launches.  No exceptions cross the
 // boundary; every entry point returns an hpg_status.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>

@@ -218,7 +218,8 @@ __device__ void overlap(const RunParams& p, int q, const float2* F, float2* U, f
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(kThreads) fused_kernel(const __grid_constant__ RunParams p) {
+template <int NT>
+__global__ void __launch_bounds__(NT) fused_kernel(const __grid_constant__ RunParams p) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double red[8][32];
   __shared__ float redf[32];
@@ -607,7 +608,10 @@ cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, fl
 
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_fused(const RunParams& p, cudaStream_t s) {
-  fused_kernel<<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p);
+  if (p.lay.slab_bytes > 0)   // large windows: latency-bound on the global slab, more warps per CTA
+    fused_kernel<512><<<p.lay.grid, 512, p.lay.smem_bytes, s>>>(p);
+  else
+    fused_kernel<kThreads><<<p.lay.grid, kThreads, p.lay.smem_bytes, s>>>(p);
   return cudaGetLastError();
 }
 cudaError_t launch_finalize(const RunParams& p, float* total, cudaStream_t s) {
@@ -655,7 +659,9 @@ static cudaError_t raise_smem(K kernel) {
                               optin - (int)fa.sharedSizeBytes);
 }
 cudaError_t set_smem_limits() {
-  cudaError_t e = raise_smem(fused_kernel);
+  cudaError_t e = raise_smem(fused_kernel<kThreads>);
+  if (e != cudaSuccess) return e;
+  e = raise_smem(fused_kernel<512>);
   if (e != cudaSuccess) return e;
   e = raise_smem(fourier_full_kernel);
   if (e != cudaSuccess) return e;
