@@ -100,9 +100,12 @@ def finish_metrics(row_power, diag_power, group_power, gram, rows, cols, have_la
         ddb = np.where(d > 0, 10.0 * np.log10(np.maximum(d, 1e-300)), _NEG)
     v[C.METRIC_DIAGBEST] = float(ddb.max())
     v[C.METRIC_DIAGWORST] = float(ddb.min())
-    snr = [_snr(float(d[i]), float(rowd[i] - d[i])) for i in range(nd)]
-    v[C.METRIC_SNRBEST] = max(snr)
-    v[C.METRIC_SNRWORST] = min(snr)
+    noise = rowd - d
+    with np.errstate(divide="ignore", invalid="ignore"):
+        snr = np.minimum(10.0 * np.log10(d / np.where(noise > 0, noise, 1.0)), SNR_CAP_DB)
+    snr = np.where(d <= 0, _NEG, np.where(noise <= 0, SNR_CAP_DB, snr))   # _snr per row, vectorised
+    v[C.METRIC_SNRBEST] = float(snr.max())
+    v[C.METRIC_SNRWORST] = float(snr.min())
     if have_labels:
         sig = float(grp.sum())
         v[C.METRIC_SNRMG] = _snr(sig, total - sig)

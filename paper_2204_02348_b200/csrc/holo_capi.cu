@@ -1,6 +1,7 @@
 // C ABI (include/holo_b200.h): plan construction in fp64 on the host, device
 // table upload, workspace sizing and kernel launches.  No exceptions cross the
 // boundary; every entry point returns an hpg_status.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -52,6 +53,8 @@ static int cuda_fail(cudaError_t e, const char* where) {
 
 struct hpg_plan {
   Geometry g;
+  double xi[2][2] = {{0, 0}, {0, 0}};   // fractional beam centre in window pixels (engine.py:147-150)
+  void* tc_dev = nullptr;              // tensor-core DFT matrices (lazy)
   DevTables t;
   FastTables ft{};
   int fill = 0;
@@ -224,13 +227,98 @@ Layout make_layout(const hpg_plan* P, int B, int A, unsigned flags, bool full_pl
 
 }  // namespace
 
+// Tensor-core DFT matrices of a plan (row DFT A1 for holo_fast_tc.cu / holo_tc2.cu, column DFT A2 for
+// holo_tc2.cu), fp16 hi + lo, computed in fp64 on first use so that plans created for the SIMT
+// kernels (e.g. one per AutoAlign evaluation) do not pay for them.
+static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
+  hpg_plan* P = const_cast<hpg_plan*>(Pc);
+  if (P->tc_dev) return cudaSuccess;
+  const Geometry& g = P->g;
+  const double (&xi)[2][2] = P->xi;
+  // tensor-core row DFT (holo_fast_tc.cu): A[n][x], n < 64 -> Re, n >= 64 -> Im of
+  // exp(-2 pi i kx_c x / nx) * px[c] = exp(-2 pi i kx_c (x - xi_x + nx/2) / nx), c = n mod 64,
+  // split into fp16 hi + lo; rows c >= ww are zero.  Only for nx == 128, wavelength 0.
+  std::vector<uint32_t> a_tc;
+  if (g.nx == 128 && g.ww <= 64) {
+    a_tc.assign((size_t)g.P * 2 * 128 * 64, 0u);
+    for (int q = 0; q < g.P; ++q) {
+      const int kx = g.k0[q][0][0];
+      for (int n = 0; n < 128; ++n) {
+        const int c = n & 63;
+        if (c >= g.ww) continue;
+        const double kc = (double)(kx + c - g.ww / 2);
+        for (int x2 = 0; x2 < 64; ++x2) {
+          uint16_t hh[2], ll[2];
+          for (int e = 0; e < 2; ++e) {
+            const int x = 2 * x2 + e;
+            const double ang = -2.0 * kPi * kc * ((double)x - xi[q][0] + g.nx / 2.0) / g.nx;
+            const double v = n < 64 ? std::cos(ang) : std::sin(ang);
+            const __half h = __double2half(v);
+            const __half l = __double2half(v - (double)__half2float(h));
+            hh[e] = __half_as_ushort(h);
+            ll[e] = __half_as_ushort(l);
+          }
+          a_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + x2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + x2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+        }
+      }
+    }
+  }
+  if (a_tc.empty()) a_tc.push_back(0u);
+  // tensor-core column DFT (holo_tc2.cu): rows r < wh -> Cr, rows 64 + r -> Ci of
+  // C[r][y] = exp(-2 pi i ky_r y / ny) * py[r] = exp(-2 pi i ky_r (y - xi_y + ny/2) / ny),
+  // ky_r = k0y + r - wh/2; K = y (0..127), fp16 hi + lo.  ny == 128, wh <= 64, wavelength 0.
+  std::vector<uint32_t> a2_tc;
+  if (g.ny == 128 && g.wh <= 64) {
+    a2_tc.assign((size_t)g.P * 2 * 128 * 64, 0u);
+    for (int q = 0; q < g.P; ++q) {
+      const int ky = g.k0[q][0][1];
+      for (int n = 0; n < 128; ++n) {
+        const int r = n & 63;
+        if (r >= g.wh) continue;
+        const double kr = (double)(ky + r - g.wh / 2);
+        for (int y2 = 0; y2 < 64; ++y2) {
+          uint16_t hh[2], ll[2];
+          for (int e = 0; e < 2; ++e) {
+            const int y = 2 * y2 + e;
+            const double ang = -2.0 * kPi * kr * ((double)y - xi[q][1] + g.ny / 2.0) / g.ny;
+            const double v = n < 64 ? std::cos(ang) : std::sin(ang);
+            const __half h = __double2half(v);
+            const __half l = __double2half(v - (double)__half2float(h));
+            hh[e] = __half_as_ushort(h);
+            ll[e] = __half_as_ushort(l);
+          }
+          a2_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + y2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a2_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + y2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+        }
+      }
+    }
+  }
+  if (a2_tc.empty()) a2_tc.push_back(0u);
+  std::vector<char> blob;
+  const size_t o1 = push(blob, a_tc), o2 = push(blob, a2_tc);
+  cudaError_t e = cudaMalloc(&P->tc_dev, blob.size());
+  if (e != cudaSuccess) { P->tc_dev = nullptr; return e; }
+  e = cudaMemcpy(P->tc_dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  P->ft.a_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o1);
+  P->ft.a2_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o2);
+  return cudaSuccess;
+}
+
 extern "C" {
 
 int hpg_version(void) { return 1; }
 
 const char* hpg_last_error(void) { return g_last_error.c_str(); }
 
+static double now_us() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+static const bool g_plan_timing = getenv("HOLO_PLAN_TIMING") != nullptr;
+
 int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
+  const double t_start = g_plan_timing ? now_us() : 0.0;
   if (!d || !out) return fail(HPG_NULLPOINTER, "null argument");
   *out = nullptr;
   if (d->pol_count < 1 || d->pol_count > 2) return fail(HPG_INVALIDPOLARISATION, "pol_count");
@@ -425,69 +513,10 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
     crange[2 * c] = (int16_t)lo;
     crange[2 * c + 1] = (int16_t)hi;
   }
-  // tensor-core row DFT (holo_fast_tc.cu): A[n][x], n < 64 -> Re, n >= 64 -> Im of
-  // exp(-2 pi i kx_c x / nx) * px[c] = exp(-2 pi i kx_c (x - xi_x + nx/2) / nx), c = n mod 64,
-  // split into fp16 hi + lo; rows c >= ww are zero.  Only for nx == 128, wavelength 0.
-  std::vector<uint32_t> a_tc;
-  if (g.nx == 128 && g.ww <= 64) {
-    a_tc.assign((size_t)g.P * 2 * 128 * 64, 0u);
-    for (int q = 0; q < g.P; ++q) {
-      const int kx = g.k0[q][0][0];
-      for (int n = 0; n < 128; ++n) {
-        const int c = n & 63;
-        if (c >= g.ww) continue;
-        const double kc = (double)(kx + c - g.ww / 2);
-        for (int x2 = 0; x2 < 64; ++x2) {
-          uint16_t hh[2], ll[2];
-          for (int e = 0; e < 2; ++e) {
-            const int x = 2 * x2 + e;
-            const double ang = -2.0 * kPi * kc * ((double)x - xi[q][0] + g.nx / 2.0) / g.nx;
-            const double v = n < 64 ? std::cos(ang) : std::sin(ang);
-            const __half h = __double2half(v);
-            const __half l = __double2half(v - (double)__half2float(h));
-            hh[e] = __half_as_ushort(h);
-            ll[e] = __half_as_ushort(l);
-          }
-          a_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + x2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
-          a_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + x2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
-        }
-      }
-    }
-  }
-  if (a_tc.empty()) a_tc.push_back(0u);
-  // tensor-core column DFT (holo_tc2.cu): rows r < wh -> Cr, rows 64 + r -> Ci of
-  // C[r][y] = exp(-2 pi i ky_r y / ny) * py[r] = exp(-2 pi i ky_r (y - xi_y + ny/2) / ny),
-  // ky_r = k0y + r - wh/2; K = y (0..127), fp16 hi + lo.  ny == 128, wh <= 64, wavelength 0.
-  std::vector<uint32_t> a2_tc;
-  if (g.ny == 128 && g.wh <= 64) {
-    a2_tc.assign((size_t)g.P * 2 * 128 * 64, 0u);
-    for (int q = 0; q < g.P; ++q) {
-      const int ky = g.k0[q][0][1];
-      for (int n = 0; n < 128; ++n) {
-        const int r = n & 63;
-        if (r >= g.wh) continue;
-        const double kr = (double)(ky + r - g.wh / 2);
-        for (int y2 = 0; y2 < 64; ++y2) {
-          uint16_t hh[2], ll[2];
-          for (int e = 0; e < 2; ++e) {
-            const int y = 2 * y2 + e;
-            const double ang = -2.0 * kPi * kr * ((double)y - xi[q][1] + g.ny / 2.0) / g.ny;
-            const double v = n < 64 ? std::cos(ang) : std::sin(ang);
-            const __half h = __double2half(v);
-            const __half l = __double2half(v - (double)__half2float(h));
-            hh[e] = __half_as_ushort(h);
-            ll[e] = __half_as_ushort(l);
-          }
-          a2_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + y2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
-          a2_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + y2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
-        }
-      }
-    }
-  }
-  if (a2_tc.empty()) a2_tc.push_back(0u);
+  for (int q = 0; q < 2; ++q) { P->xi[q][0] = xi[q][0]; P->xi[q][1] = xi[q][1]; }
   P->fill = d->fill_factor;
   std::vector<char> blob;
-  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange), o_atc = push(blob, a_tc), o_a2 = push(blob, a2_tc);
+  const size_t o_px = push(blob, pxv), o_py = push(blob, pyv), o_cr = push(blob, crange), o_unused = 0;
   const size_t o_timg = push(blob, tco_img), o_tinv = push(blob, tco_inv);
   const size_t o_nx = push(blob, tw_nx), o_ny = push(blob, tw_ny), o_gw = push(blob, tw_gw), o_gh = push(blob, tw_gh);
   const size_t o_w = push(blob, wtab), o_rx = push(blob, remx), o_ry = push(blob, remy);
@@ -499,9 +528,11 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   std::vector<double> xad(P->xa.begin(), P->xa.end()), yad(P->ya.begin(), P->ya.end());
   const size_t o_xad = push(blob, xad), o_yad = push(blob, yad);
   const size_t o_mm = push(blob, mm), o_mn = push(blob, mn);
+  const double t_host = g_plan_timing ? now_us() : 0.0;
   cudaGetDevice(&P->device);
   cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
   cudaError_t e = cudaMalloc(&P->dev, blob.size());
+  const double t_alloc = g_plan_timing ? now_us() : 0.0;
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaMalloc(plan tables)"); }
   e = cudaMemcpy(P->dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaMemcpy(plan tables)"); }
@@ -524,12 +555,17 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.px = reinterpret_cast<const float2*>(base + o_px);
   P->ft.py = reinterpret_cast<const float2*>(base + o_py);
   P->ft.crange = reinterpret_cast<const int16_t*>(base + o_cr);
-  P->ft.a_tc = reinterpret_cast<const uint32_t*>(base + o_atc);
-  P->ft.a2_tc = reinterpret_cast<const uint32_t*>(base + o_a2);
+  (void)o_unused;
+  P->ft.a_tc = nullptr;    // tensor-core DFT matrices: built on first use (ensure_tc_tables)
+  P->ft.a2_tc = nullptr;
   P->ft.tco_img = tco_ok ? reinterpret_cast<const uint4*>(base + o_timg) : nullptr;
   P->ft.tco_inv = reinterpret_cast<const float*>(base + o_tinv);
   P->ft.tco_gp = tco_ok ? GP16 : 0;
+  const double t_copy = g_plan_timing ? now_us() : 0.0;
   e = set_smem_limits();
+  if (g_plan_timing)
+    fprintf(stderr, "hpg_plan_create: host %.0f us, malloc %.0f us, copy %.0f us (%zu B), smem limits %.0f us\n",
+            t_host - t_start, t_alloc - t_host, t_copy - t_alloc, blob.size(), now_us() - t_copy);
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaFuncSetAttribute"); }
   *out = P;
   return HPG_SUCCESS;
@@ -538,6 +574,7 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
 int hpg_plan_destroy(hpg_plan* P) {
   if (!P) return fail(HPG_NULLPOINTER, "null plan");
   if (P->dev) cudaFree(P->dev);
+  if (P->tc_dev) cudaFree(P->tc_dev);
   delete P;
   return HPG_SUCCESS;
 }
@@ -668,10 +705,14 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
       tc2_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows)) {
     if (!o->workspace || o->workspace_bytes < tc2_workspace((int64_t)b->batch_count * P->g.P))
       return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
-    e = launch_tc2(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+    e = ensure_tc_tables(P);
+    if (e == cudaSuccess) e = launch_tc2(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
   } else if ((flags & HPG_FLAG_TC) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
       tc_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows))
-    e = launch_fast_tc(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+  {
+    e = ensure_tc_tables(P);
+    if (e == cudaSuccess) e = launch_fast_tc(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+  }
   else if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&
       !b->members)
     e = launch_fast(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));

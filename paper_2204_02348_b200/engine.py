@@ -932,18 +932,23 @@ class Engine:
         else:
             vrows, offs, cnts = rows, None, None
         R = len(vrows)
-        labels = np.array([q * 1000 + mode_group_of_index(i) for q in range(P) for i in range(M)], np.int32)
         dev = self.device
-        t_rows = torch.as_tensor(vrows.astype(np.int32), device=dev)
-        t_off = torch.as_tensor(offs.astype(np.int32), device=dev) if offs is not None else None
-        t_cnt = torch.as_tensor(cnts.astype(np.int32), device=dev) if cnts is not None else None
-        t_lab = torch.as_tensor(labels, device=dev)
-        rp = torch.empty(R, dtype=torch.float64, device=dev)
-        dp = torch.empty(R, dtype=torch.float64, device=dev)
-        gp = torch.empty(R, dtype=torch.float64, device=dev)
+        # device index tables of this row set / layout, cached across AutoAlign evaluations
+        key = (vrows.tobytes(), P, M, pol_ind)
+        cache = self._bufs.get("metric_idx")
+        if cache is None or cache[0] != key:
+            labels = np.array([q * 1000 + mode_group_of_index(i) for q in range(P) for i in range(M)], np.int32)
+            t_rows = torch.as_tensor(vrows.astype(np.int32), device=dev)
+            t_off = torch.as_tensor(offs.astype(np.int32), device=dev) if offs is not None else None
+            t_cnt = torch.as_tensor(cnts.astype(np.int32), device=dev) if cnts is not None else None
+            cache = (key, t_rows, t_off, t_cnt, torch.as_tensor(labels, device=dev))
+            self._bufs["metric_idx"] = cache
+        _, t_rows, t_off, t_cnt, t_lab = cache
         gram_rows = 1 if R <= cols else 0
         n = R if gram_rows else cols
-        gram = torch.empty((n, n), dtype=torch.complex128, device=dev)
+        # one packed fp64 buffer (row | diag | group powers, Gram) -> a single device-to-host copy
+        r3 = (3 * R + 1) & ~1
+        packed = self._buf("metric_out", (r3 + 2 * n * n,), torch.float64)
         a = native.MetricArgs()
         a.coefs = self._coefs.data_ptr()
         a.rows, a.cols, a.ld = R, cols, cols
@@ -952,13 +957,15 @@ class Engine:
         a.col_count = t_cnt.data_ptr() if t_cnt is not None else None
         a.labels = t_lab.data_ptr()
         a.ndiag, a.diag_offset, a.gram_rows = min(R, cols), 0, gram_rows
-        a.row_power, a.diag_power, a.group_power = rp.data_ptr(), dp.data_ptr(), gp.data_ptr()
-        a.gram = gram.data_ptr()
+        base = packed.data_ptr()
+        a.row_power, a.diag_power, a.group_power = base, base + 8 * R, base + 16 * R
+        a.gram = base + 8 * r3
         with torch.cuda.device(dev):
-            native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle()),
+            native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle(dev)),
                          "hpg_metric_partials")
-        return finish_metrics(rp.cpu().numpy(), dp.cpu().numpy(), gp.cpu().numpy(), gram.cpu().numpy(),
-                              R, cols, True)
+        host = packed.cpu().numpy()
+        gram = host[r3:].view(np.complex128).reshape(n, n)
+        return finish_metrics(host[:R], host[R:2 * R], host[2 * R:3 * R], gram, R, cols, True)
 
     def metric(self, metric_idx):
         if self._metrics is None:
