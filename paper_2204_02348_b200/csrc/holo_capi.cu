@@ -29,6 +29,9 @@ cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms
 bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
                    const void* windows);
 size_t tc2_workspace(int64_t items);
+bool lw_supported(const Geometry& g, int A, const void* members, unsigned flags, const void* windows);
+size_t lw_workspace(const Geometry& g, int64_t items);
+cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
 cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
                                  const double* ya, float* params, int slots, float* total, double* pol_total,
@@ -633,6 +636,8 @@ int hpg_workspace_size(const hpg_plan* P, int32_t B, uint32_t flags, size_t* byt
   finish_layout(P, F, (int64_t)P->num_sms * 2, 0);
   *bytes = (size_t)std::max<int64_t>(std::max<int64_t>(fused, F.slab_bytes * F.grid), 256);
   *bytes = std::max(*bytes, tc2_workspace((int64_t)B * P->g.P));   // Fourier windows between the TC2 kernels
+  if (lw_supported(P->g, 1, nullptr, flags, nullptr))                  // large-window path intermediates
+    *bytes = std::max(*bytes, lw_workspace(P->g, (int64_t)B * P->g.P));
   return HPG_SUCCESS;
 }
 
@@ -716,7 +721,11 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
   else if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&
       !b->members)
     e = launch_fast(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
-  else
+  else if (!(flags & HPG_FLAG_GENERIC) && lw_supported(rp.g, A, b->members, flags, o->windows)) {
+    if (!o->workspace || o->workspace_bytes < lw_workspace(rp.g, (int64_t)b->batch_count * P->g.P))
+      return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
+    e = launch_lw(rp, P->num_sms, static_cast<cudaStream_t>(stream));
+  } else
     e = launch_fused(rp, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
   return HPG_SUCCESS;

@@ -294,6 +294,10 @@ HOLO_DEV void stockham_stage_generic(const float2* src, float2* dst, int n, int 
   }
 }
 
+// cos / sin (2 pi e / 41): constant-cache operands of the radix-41 stage (164 = 4 x 41 field grids)
+__constant__ float kCos41[41] = {1.000000000e+00f, 9.882804238e-01f, 9.533963921e-01f, 8.961655570e-01f, 8.179293608e-01f, 7.205215936e-01f, 6.062254110e-01f, 4.777198185e-01f, 3.380168784e-01f, 1.903911092e-01f, 3.830273369e-02f, -1.146834254e-01f, -2.649815022e-01f, -4.090686372e-01f, -5.435675500e-01f, -6.653257002e-01f, -7.714891798e-01f, -8.595696070e-01f, -9.275024511e-01f, -9.736954239e-01f, -9.970658012e-01f, -9.970658012e-01f, -9.736954239e-01f, -9.275024511e-01f, -8.595696070e-01f, -7.714891798e-01f, -6.653257002e-01f, -5.435675500e-01f, -4.090686372e-01f, -2.649815022e-01f, -1.146834254e-01f, 3.830273369e-02f, 1.903911092e-01f, 3.380168784e-01f, 4.777198185e-01f, 6.062254110e-01f, 7.205215936e-01f, 8.179293608e-01f, 8.961655570e-01f, 9.533963921e-01f, 9.882804238e-01f};
+__constant__ float kSin41[41] = {0.000000000e+00f, 1.526492842e-01f, 3.017205986e-01f, 4.437198379e-01f, 5.753186602e-01f, 6.934325008e-01f, 7.952928713e-01f, 8.785122509e-01f, 9.411400480e-01f, 9.817083200e-01f, 9.992661811e-01f, 9.934020898e-01f, 9.642534955e-01f, 9.125036165e-01f, 8.393654261e-01f, 7.465532216e-01f, 6.362424423e-01f, 5.110186794e-01f, 3.738170718e-01f, 2.278535089e-01f, 7.654925284e-02f, -7.654925284e-02f, -2.278535089e-01f, -3.738170718e-01f, -5.110186794e-01f, -6.362424423e-01f, -7.465532216e-01f, -8.393654261e-01f, -9.125036165e-01f, -9.642534955e-01f, -9.934020898e-01f, -9.992661811e-01f, -9.817083200e-01f, -9.411400480e-01f, -8.785122509e-01f, -7.952928713e-01f, -6.934325008e-01f, -5.753186602e-01f, -4.437198379e-01f, -3.017205986e-01f, -1.526492842e-01f};
+
 // Runs every stage of `plan` (block-cooperative, __syncthreads between stages).
 // Ping-pongs between a and b; returns the buffer that holds the result.
 template <bool INV>

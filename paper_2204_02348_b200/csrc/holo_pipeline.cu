@@ -16,6 +16,8 @@
 //                multiply by mask * recentring phase (pipeline.py:72-76,114-127)
 //   IFFT       : wh x ww inverse (pipeline.py:130-149), ifftshift folded into
 //                the separable removal phase (pipeline.py:163-185)
+#include <algorithm>
+
 #include "holo_internal.h"
 
 namespace holo {
@@ -604,6 +606,441 @@ __global__ void refcal_finish_kernel(const float2* a, const float2* b, int64_t n
 cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, float2* out, cudaStream_t s) {
   refcal_finish_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n, out);
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------ large-window path
+// Windows too large for one CTA's shared memory (config 3: 512^2 window, 164^2 field) run as
+// four grid-wide kernels over chunks of items whose intermediates stay resident in L2:
+//   lw_rows   row pairs (y, y + ny/2) -> complex FFT along x -> Hermitian split -> R[c][y]
+//   lw_cols   FFT along y of kept columns -> crop (mask * recentring [/ sinc]) -> IFFT along r -> T[c][y']
+//   lw_field  IFFT along c of field rows -> removal phase, calibrations -> F[y'][x'], per-item peak
+//   lw_pack   int16 packing with scale = float32(32767 / peak) (holopipe/pipeline.py:188-199)
+// Same algebra as row_pass / col_pass / the fused epilogue; every CTA works on one item.
+// 512-point forward FFT by a group of 64 threads, three radix-8 passes (x = t + 64 j in registers
+// -> twiddle W512^(t k) -> S1[k][t]; DFT-8 over t1 of t = t0 + 8 t1 -> twiddle W64^(t0 m1) ->
+// S2[k][m1][t0]; DFT-8 over t0 -> X[k + 8 m1 + 64 m2]).  S1 (8 x 65) also receives the output
+// (natural order, 512); S2 is 64 x 9.  Every pass ends in a CTA barrier (all groups in lockstep).
+HOLO_DEV void fft512_group(float2 (&a)[8], int t, const float2* __restrict__ tw, float2* S1, float2* S2) {
+  dft8<false>(a);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) S1[k * 65 + t] = k ? cmul(a[k], __ldg(&tw[(t * k) & 511])) : a[k];
+  __syncthreads();
+  {
+    const int k = t >> 3, t0 = t & 7;
+    float2 c[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c[j] = S1[k * 65 + t0 + 8 * j];
+    dft8<false>(c);
+#pragma unroll
+    for (int m1 = 0; m1 < 8; ++m1)
+      S2[(k * 8 + m1) * 9 + t0] = m1 ? cmul(c[m1], __ldg(&tw[(8 * t0 * m1) & 511])) : c[m1];
+  }
+  __syncthreads();
+  {
+    const int k = t >> 3, m1 = t & 7;
+    float2 e[8];
+#pragma unroll
+    for (int t0 = 0; t0 < 8; ++t0) e[t0] = S2[(k * 8 + m1) * 9 + t0];
+    dft8<false>(e);
+#pragma unroll
+    for (int m2 = 0; m2 < 8; ++m2) S1[k + 8 * m1 + 64 * m2] = e[m2];   // S1 is free after pass 2
+  }
+  __syncthreads();
+}
+constexpr int kF512Group = 8 * 65 + 64 * 9;   // float2 of scratch per 512-point group
+
+// Row pass for 512-wide windows: 8 row pairs per 512-thread CTA, one 64-thread group each.
+__global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                          float2* __restrict__ R) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int ny = g.ny, ny2 = ny >> 1, ww = g.ww;
+  const int nblk = ny2 / 8;
+  const int item = i0 + blockIdx.x / nblk, y0 = (blockIdx.x % nblk) * 8;
+  if (item >= i1) return;
+  const int b = item / g.P, q = item - b * g.P;
+  const int w = p.wl ? p.wl[b] : 0;
+  const int k0x = g.k0[q][w][0];
+  const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
+  float2* S1 = reinterpret_cast<float2*>(smem) + grp * kF512Group;
+  float2* S2 = S1 + 8 * 65;
+  const int y = y0 + grp;
+  float2 a[8];
+  if (p.fmt == 0) {
+    const float* ra = reinterpret_cast<const float*>(p.frames) + (int64_t)b * g.W * g.H +
+                      (int64_t)(g.row0[q] + y) * g.W + g.col0[q];
+    const float* rb = ra + (int64_t)ny2 * g.W;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = make_float2(__ldg(ra + t + 64 * j), __ldg(rb + t + 64 * j));
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      a[j] = make_float2(load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, g.row0[q] + y, g.col0[q] + t + 64 * j),
+                         load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, g.row0[q] + y + ny2, g.col0[q] + t + 64 * j));
+  }
+  fft512_group(a, t, p.t.tw_nx, S1, S2);
+  // Hermitian split of the kept bins; all 8 row pairs of the CTA write 8 consecutive y per column
+  float2* Ri = R + (size_t)(item - i0) * ww * ny;
+  const float2* X0 = reinterpret_cast<const float2*>(smem);
+  for (int idx = threadIdx.x; idx < 8 * ww; idx += blockDim.x) {
+    const int c = idx >> 3, s = idx & 7;
+    const int kx = pmod(k0x + c - ww / 2, 512);
+    const int km = (512 - kx) & 511;
+    const float2* X = X0 + s * kF512Group;
+    const float2 zk = X[kx], zm = X[km];
+    Ri[(size_t)c * ny + y0 + s] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+    Ri[(size_t)c * ny + y0 + s + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+  }
+}
+
+// Column pass for 512-high windows: 8 columns per 512-thread CTA; FFT along y (512), crop,
+// window table, then the IFFT along r (generic Stockham) -> T[c][y'].
+__global__ void __launch_bounds__(512) lw_cols512_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                          const float2* __restrict__ R, float2* __restrict__ T) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int ny = g.ny, ww = g.ww, wh = g.wh;
+  const int nblk = (ww + 7) / 8;
+  const int item = i0 + blockIdx.x / nblk, c0 = (blockIdx.x % nblk) * 8;
+  if (item >= i1) return;
+  const int b = item / g.P, q = item - b * g.P;
+  const int w = p.wl ? p.wl[b] : 0;
+  const int k0y = g.k0[q][w][1];
+  const int cc = min(8, ww - c0);
+  const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
+  float2* S1 = reinterpret_cast<float2*>(smem) + grp * kF512Group;
+  float2* S2 = S1 + 8 * 65;
+  const float2* Rc = R + (size_t)(item - i0) * ww * ny + (size_t)(c0 + min(grp, cc - 1)) * ny;
+  float2 a[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a[j] = Rc[t + 64 * j];
+  fft512_group(a, t, p.t.tw_ny, S1, S2);
+  // crop + window table -> Wg[c][r] (global, column-major); the IFFT along r runs in lw_ifft_y
+  const float2* wtab = p.t.win_tab + (size_t)(q * g.L + w) * wh * ww;
+  const float2* X0 = reinterpret_cast<const float2*>(smem);
+  float2* Wg = T + (size_t)(item - i0) * ww * wh + (size_t)c0 * wh;
+  for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) {
+    const int j = idx / wh, r = idx - j * wh, c = c0 + j;
+    const int ky = pmod(k0y + r - wh / 2, 512);
+    Wg[idx] = cmul(X0[j * kF512Group + ky], __ldg(&wtab[r * ww + c]));
+  }
+}
+
+// Inverse 164-point transforms (164 = 4 x 41) of `count` sequences (stride 164), S0 -> S0 via S1:
+// the radix-4 Stockham stage, then the radix-41 stage split over (sequence, k, output pair) work
+// items with the conjugate-pair sums staged in `scr` (count * 4 * 20 * 2 float2), so every thread
+// of the CTA has work (one task per thread keeps 20-deep FMA chains on a few threads).
+HOLO_DEV void ifft164(float2* S0, float2* S1, float2* scr, int count, const float2* __restrict__ tw) {
+  constexpr int N = 164, L = 4, P = 41, H = 20;
+  __shared__ float cs41[2][P];   // per-thread (divergent) indices: shared memory, not the constant cache
+  for (int i = threadIdx.x; i < P; i += blockDim.x) {
+    cs41[0][i] = kCos41[i];
+    cs41[1][i] = kSin41[i];
+  }
+  stockham_stage_fixed<4, true>(S0, S1, N, 1, count, N, 1, tw, threadIdx.x, blockDim.x);
+  __syncthreads();
+  float2* SP = scr;
+  float2* SM = scr + count * L * H;
+  for (int i = threadIdx.x; i < count * L * H; i += blockDim.x) {   // (q, k, j)
+    const int qk = i / H, j = i - qk * H + 1, q = qk >> 2, k = qk & 3;
+    const float2* src = S1 + q * N;
+    const float2 a = cmul(src[k * P + j], twid<true>(__ldg(&tw[(j * k) % N])));
+    const float2 b = cmul(src[k * P + P - j], twid<true>(__ldg(&tw[((P - j) * k) % N])));
+    SP[i] = cadd(a, b);
+    SM[i] = csub(a, b);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < count * L * (H + 1); i += blockDim.x) {   // (q, k, t)
+    const int qk = i / (H + 1), t = i - qk * (H + 1), q = qk >> 2, k = qk & 3;
+    const float2 v0 = S1[q * N + k * P];
+    const float2* sp = SP + qk * H;
+    const float2* sm = SM + qk * H;
+    float2* d = S0 + q * N;
+    if (t == 0) {
+      float2 tot = v0;
+#pragma unroll
+      for (int j = 0; j < H; ++j) tot = cadd(tot, sp[j]);
+      d[k] = tot;
+    } else {
+      float2 re = v0, im = make_float2(0.f, 0.f);
+      int e = 0;
+#pragma unroll
+      for (int j = 1; j <= H; ++j) {
+        e += t; if (e >= P) e -= P;
+        const float c = cs41[0][e], sn = cs41[1][e];
+        re.x = fmaf(c, sp[j - 1].x, re.x);
+        re.y = fmaf(c, sp[j - 1].y, re.y);
+        im.x = fmaf(sn, sm[j - 1].x, im.x);
+        im.y = fmaf(sn, sm[j - 1].y, im.y);
+      }
+      const float2 rr = rot90<true>(im);
+      d[k + L * t] = cadd(re, rr);
+      d[k + L * (P - t)] = csub(re, rr);
+    }
+  }
+  __syncthreads();
+}
+
+// IFFT along r of kLwIfft columns per CTA (enough independent tasks for the radix-41 stage)
+constexpr int kLwIfft = 16;
+template <bool F164>
+__global__ void __launch_bounds__(kThreads, 3) lw_ifft_y_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                                 const float2* __restrict__ Wg, float2* __restrict__ T) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int gh = g.gh, ww = g.ww;
+  const int nblk = (ww + kLwIfft - 1) / kLwIfft;
+  const int item = i0 + blockIdx.x / nblk, c0 = (blockIdx.x % nblk) * kLwIfft;
+  if (item >= i1) return;
+  const int cc = min(kLwIfft, ww - c0);
+  float2* S0 = reinterpret_cast<float2*>(smem);
+  float2* S1 = S0 + kLwIfft * gh;
+  const float2* Wi = Wg + (size_t)(item - i0) * ww * gh + (size_t)c0 * gh;
+  for (int i = threadIdx.x; i < cc * gh; i += blockDim.x) S0[i] = Wi[i];
+  __syncthreads();
+  const float2* tr;
+  if constexpr (F164) {
+    ifft164(S0, S1, S1 + kLwIfft * gh, cc, p.t.tw_gh);
+    tr = S0;
+  } else {
+    const FFTPlan pg = make_plan(gh, g.nst_gh, g.radix_gh, p.t.tw_gh);
+    tr = stockham<true>(S0, S1, pg, cc, gh, 1);
+  }
+  float2* Ti = T + (size_t)(item - i0) * ww * gh + (size_t)c0 * gh;
+  for (int i = threadIdx.x; i < cc * gh; i += blockDim.x) Ti[i] = tr[i];
+}
+
+constexpr int kLwRows = 8;    // row pairs per lw_rows CTA
+constexpr int kLwCols = 8;    // columns per lw_cols CTA
+constexpr int kLwFRows = 16;  // field rows per lw_field CTA (tasks for the radix-41 stage)
+
+__global__ void __launch_bounds__(kThreads) lw_rows_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                            float2* __restrict__ R) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int nx = g.nx, ny = g.ny, ny2 = ny >> 1, ww = g.ww;
+  const int nblk = (ny2 + kLwRows - 1) / kLwRows;
+  const int item = i0 + blockIdx.x / nblk, c0 = (blockIdx.x % nblk) * kLwRows;
+  if (item >= i1) return;
+  const int b = item / g.P, q = item - b * g.P;
+  const int w = p.wl ? p.wl[b] : 0;
+  const int k0x = g.k0[q][w][0];
+  const int ch = min(kLwRows, ny2 - c0);
+  float2* S0 = reinterpret_cast<float2*>(smem);
+  float2* S1 = S0 + kLwRows * nx;
+  const int col0 = g.col0[q], row0 = g.row0[q];
+  for (int idx = threadIdx.x; idx < ch * nx; idx += blockDim.x) {
+    const int sr = idx / nx, x = idx - sr * nx, y = c0 + sr;
+    const float a = load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, row0 + y, col0 + x);
+    const float bb = load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, row0 + y + ny2, col0 + x);
+    S0[idx] = make_float2(a, bb);
+  }
+  __syncthreads();
+  const FFTPlan pl = make_plan(nx, g.nst_nx, g.radix_nx, p.t.tw_nx);
+  const float2* Z = stockham<false>(S0, S1, pl, ch, nx, 1);
+  float2* Ri = R + (size_t)(item - i0) * ww * ny;
+  for (int idx = threadIdx.x; idx < ch * ww; idx += blockDim.x) {
+    const int c = idx / ch, sr = idx - c * ch;
+    const int kx = pmod(k0x + c - ww / 2, nx);
+    const int km = kx ? nx - kx : 0;
+    const float2 zk = Z[sr * nx + kx], zm = Z[sr * nx + km];
+    Ri[(size_t)c * ny + c0 + sr] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+    Ri[(size_t)c * ny + c0 + sr + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lw_cols_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                            const float2* __restrict__ R, float2* __restrict__ T) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int ny = g.ny, ww = g.ww, wh = g.wh;
+  const int nblk = (ww + kLwCols - 1) / kLwCols;
+  const int item = i0 + blockIdx.x / nblk, c0 = (blockIdx.x % nblk) * kLwCols;
+  if (item >= i1) return;
+  const int b = item / g.P, q = item - b * g.P;
+  const int w = p.wl ? p.wl[b] : 0;
+  const int k0y = g.k0[q][w][1];
+  const int cc = min(kLwCols, ww - c0);
+  float2* S0 = reinterpret_cast<float2*>(smem);
+  float2* S1 = S0 + kLwCols * ny;
+  const float2* Ri = R + (size_t)(item - i0) * ww * ny + (size_t)c0 * ny;
+  for (int i = threadIdx.x; i < cc * ny; i += blockDim.x) S0[i] = Ri[i];
+  __syncthreads();
+  const FFTPlan pl = make_plan(ny, g.nst_ny, g.radix_ny, p.t.tw_ny);
+  const float2* res = stockham<false>(S0, S1, pl, cc, ny, 1);
+  float2* Wc = res == S0 ? S1 : S0;   // [j][r], column-major window (gh == wh)
+  const float2* wtab = p.t.win_tab + (size_t)(q * g.L + w) * wh * ww;
+  for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) {
+    const int j = idx / wh, r = idx - j * wh, c = c0 + j;
+    const int ky = pmod(k0y + r - wh / 2, ny);
+    Wc[idx] = cmul(res[j * ny + ky], __ldg(&wtab[r * ww + c]));
+  }
+  __syncthreads();
+  // ifftshift and 1/(nx ny) live in the removal vectors (plan tables), so the IDFT is plain
+  const FFTPlan pg = make_plan(g.gh, g.nst_gh, g.radix_gh, p.t.tw_gh);
+  float2* other = Wc == S0 ? S1 : S0;
+  const float2* tr = stockham<true>(Wc, other, pg, cc, wh, 1);
+  float2* Ti = T + (size_t)(item - i0) * ww * g.gh + (size_t)c0 * g.gh;
+  for (int i = threadIdx.x; i < cc * g.gh; i += blockDim.x) Ti[i] = tr[i];
+}
+
+template <bool F164>
+__global__ void __launch_bounds__(kThreads, 3) lw_field_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                                const float2* __restrict__ T, float2* __restrict__ Fo,
+                                                                unsigned* __restrict__ peak) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ float redf[32];
+  const Geometry& g = p.g;
+  const int gh = g.gh, gw = g.gw;
+  const int nblk = (gh + kLwFRows - 1) / kLwFRows;
+  const int item = i0 + blockIdx.x / nblk, y0 = (blockIdx.x % nblk) * kLwFRows;
+  if (item >= i1) return;
+  const int b = item / g.P, q = item - b * g.P;
+  const int w = p.wl ? p.wl[b] : 0;
+  const int rr = min(kLwFRows, gh - y0);
+  float2* S0 = reinterpret_cast<float2*>(smem);
+  float2* S1 = S0 + kLwFRows * gw;
+  const float2* Ti = T + (size_t)(item - i0) * gw * gh;
+  for (int i = threadIdx.x; i < rr * gw; i += blockDim.x) {   // [s][c] <- T[c][y0 + s]
+    const int c = i / rr, sr = i - c * rr;
+    S0[sr * gw + c] = Ti[(size_t)c * gh + y0 + sr];
+  }
+  __syncthreads();
+  const float2* Fr;
+  if constexpr (F164) {
+    ifft164(S0, S1, S1 + kLwFRows * gw, rr, p.t.tw_gw);
+    Fr = S0;
+  } else {
+    const FFTPlan pl = make_plan(gw, g.nst_gw, g.radix_gw, p.t.tw_gw);
+    Fr = stockham<true>(S0, S1, pl, rr, gw, 1);
+  }
+  const float2* ex = p.t.rem_x + (size_t)(q * g.L + w) * gw;
+  const float2* ey = p.t.rem_y + (size_t)(q * g.L + w) * gh;
+  float2 bc = make_float2(1.f, 0.f);
+  if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+  const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * gh * gw : nullptr;
+  float2* Fi = Fo + (size_t)(item - i0) * gh * gw;
+  float lmax = 0.f;
+  for (int i = threadIdx.x; i < rr * gw; i += blockDim.x) {
+    const int sr = i / gw, x = i - sr * gw, y = y0 + sr;
+    float2 v = cmul(cmul(Fr[i], __ldg(&ey[y])), __ldg(&ex[x]));
+    if (p.bcal) v = cmul(v, bc);
+    if (rc) v = cmul(v, rc[(size_t)y * gw + x]);
+    lmax = fmaxf(lmax, fmaxf(fabsf(v.x), fabsf(v.y)));
+    Fi[(size_t)y * gw + x] = v;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  if ((threadIdx.x & 31) == 0) redf[threadIdx.x >> 5] = lmax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < (int)(blockDim.x >> 5); ++j) lmax = fmaxf(lmax, redf[j]);
+    atomicMax(&peak[item - i0], __float_as_uint(lmax));   // non-negative floats order as unsigned
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lw_pack_kernel(const __grid_constant__ RunParams p, int i0, int i1,
+                                                            const float2* __restrict__ Fo,
+                                                            const unsigned* __restrict__ peak) {
+  const Geometry& g = p.g;
+  const int ghw = g.gh * g.gw;
+  const int per = (ghw + 2 * blockDim.x - 1) / (2 * blockDim.x);   // blocks per item
+  const int item = i0 + blockIdx.x / per, part = blockIdx.x % per;
+  if (item >= i1) return;
+  const float lmax = __uint_as_float(peak[item - i0]);
+  const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
+  const float2* Fi = Fo + (size_t)(item - i0) * ghw;
+  int16_t* fro = p.fr + (size_t)item * ghw;
+  int16_t* fio = p.fi + (size_t)item * ghw;
+  for (int i = part * 2 * blockDim.x + threadIdx.x; i < min(ghw, (part + 1) * 2 * (int)blockDim.x); i += blockDim.x) {
+    const float2 v = Fi[i];
+    fro[i] = (int16_t)__float2int_rn(__fmul_rn(v.x, scale));
+    fio[i] = (int16_t)__float2int_rn(__fmul_rn(v.y, scale));
+    if (p.raw) p.raw[(size_t)item * ghw + i] = v;
+  }
+  if (part == 0 && threadIdx.x == 0) p.scale[item] = scale;
+}
+
+bool lw_supported(const Geometry& g, int A, const void* members, unsigned flags, const void* windows) {
+  const size_t cols_smem = 2ull * kLwCols * g.ny * sizeof(float2);
+  const size_t rows_smem = 2ull * kLwRows * g.nx * sizeof(float2);
+  const size_t field_smem = (2ull * g.gw + 160) * kLwFRows * sizeof(float2);
+  const bool coefs_fit = g.G == 0 || ((size_t)g.gh * g.gw + (size_t)g.gh * g.G) * sizeof(float2) <= 200 * 1024;
+  return A == 1 && members == nullptr && g.mode == 1 && g.gh == g.wh && g.gw == g.ww && g.nx >= 256 &&
+         g.ny >= 256 && (flags & 1u) == 0 && windows == nullptr && cols_smem <= 200 * 1024 &&
+         rows_smem <= 200 * 1024 && field_smem <= 200 * 1024 && 2ull * kLwCols * g.gh * sizeof(float2) <= cols_smem &&
+         (2ull * g.gh + 160) * kLwIfft * sizeof(float2) <= 200 * 1024 &&
+         coefs_fit;
+}
+
+int64_t lw_chunk(const Geometry& g) {   // items per chunk: R + T + F of a chunk within ~80 MB of L2
+  const int64_t per = (int64_t)g.ww * g.ny * 8 + 2 * (int64_t)g.gh * g.gw * 8 + 4;
+  return std::max<int64_t>(1, (80ll << 20) / per);
+}
+
+size_t lw_workspace(const Geometry& g, int64_t items) {
+  const int64_t n = std::min<int64_t>(items, lw_chunk(g));
+  return (size_t)n * ((size_t)g.ww * g.ny * 8 + 2 * (size_t)g.gh * g.gw * 8 + 16) + 1024;
+}
+
+cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s);
+
+cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
+  const Geometry& g = p.g;
+  const int items = p.B * g.P;
+  const int64_t chunk = lw_chunk(g);
+  const int64_t n0 = std::min<int64_t>(items, chunk);
+  char* ws = p.work;
+  float2* R = reinterpret_cast<float2*>(ws);
+  float2* T = R + (size_t)n0 * g.ww * g.ny;
+  float2* F = T + (size_t)n0 * g.gh * g.gw;
+  unsigned* peak = reinterpret_cast<unsigned*>(F + (size_t)n0 * g.gh * g.gw);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(lw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_field_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_field_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_rows512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_cols512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_ifft_y_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_ifft_y_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    configured = true;
+  }
+  const int rows_smem = 2 * kLwRows * g.nx * (int)sizeof(float2);
+  const int cols_smem = 2 * kLwCols * g.ny * (int)sizeof(float2);
+  const int field_smem = (2 * g.gw + 160) * kLwFRows * (int)sizeof(float2);
+  for (int i0 = 0; i0 < items; i0 += (int)chunk) {
+    const int i1 = (int)std::min<int64_t>(items, i0 + chunk);
+    const int n = i1 - i0;
+    cudaMemsetAsync(peak, 0, (size_t)n * sizeof(unsigned), s);
+    if (g.nx == 512 && g.ny == 512) {
+      const int f512 = 8 * kF512Group * (int)sizeof(float2);
+      lw_rows512_kernel<<<n * (g.ny / 2 / 8), 512, f512, s>>>(p, i0, i1, R);
+      lw_cols512_kernel<<<n * ((g.ww + 7) / 8), 512, f512, s>>>(p, i0, i1, R, F);   // cropped window -> F (scratch)
+      const int ys = (2 * g.gh + 160) * kLwIfft * (int)sizeof(float2);
+      if (g.gh == 164)
+        lw_ifft_y_kernel<true><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s>>>(p, i0, i1, F, T);
+      else
+        lw_ifft_y_kernel<false><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s>>>(p, i0, i1, F, T);
+    } else {
+      lw_rows_kernel<<<n * ((g.ny / 2 + kLwRows - 1) / kLwRows), kThreads, rows_smem, s>>>(p, i0, i1, R);
+      lw_cols_kernel<<<n * ((g.ww + kLwCols - 1) / kLwCols), kThreads, cols_smem, s>>>(p, i0, i1, R, T);
+    }
+    if (g.gw == 164)
+      lw_field_kernel<true><<<n * ((g.gh + kLwFRows - 1) / kLwFRows), kThreads, field_smem, s>>>(p, i0, i1, T, F, peak);
+    else
+      lw_field_kernel<false><<<n * ((g.gh + kLwFRows - 1) / kLwFRows), kThreads, field_smem, s>>>(p, i0, i1, T, F, peak);
+    const int per = (g.gh * g.gw + 2 * kThreads - 1) / (2 * kThreads);
+    lw_pack_kernel<<<n * per, kThreads, 0, s>>>(p, i0, i1, F, peak);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  if (p.coefs && g.G > 0) {
+    const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms * 4);
+    return launch_coefs(p, grid, s);
+  }
+  return cudaSuccess;
 }
 
 // ---------------------------------------------------------------- launchers

@@ -257,3 +257,17 @@ def test_tensor_core_overlap_matches_simt_overlap(name):
         assert np.array_equal(x, y)
     assert rel_l2_rows(a[3], b[3]) <= 2e-6
     assert rel_l2_rows(a[3], g["coefs"]) <= COEF_TOL
+
+
+@pytest.mark.parametrize("name", ["largeframe", "n256"])
+def test_large_window_path_matches_generic(name):
+    """Chunked large-window kernels (rows / columns / field / pack) == the generic fused kernel."""
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.run_pipeline(0)
+    a = [t.cpu().numpy().copy() for t in eng.fields16_device()]
+    eng.force_generic = True
+    eng.run_pipeline(0)
+    b = [t.cpu().numpy() for t in eng.fields16_device()]
+    assert np.abs(a[0].astype(int) - b[0]).max() <= 2 and np.abs(a[1].astype(int) - b[1]).max() <= 2
+    assert np.allclose(a[2], b[2], rtol=1e-5)
