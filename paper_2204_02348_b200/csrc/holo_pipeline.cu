@@ -616,20 +616,23 @@ cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, fl
 //   lw_field  IFFT along c of field rows -> removal phase, calibrations -> F[y'][x'], per-item peak
 //   lw_pack   int16 packing with scale = float32(32767 / peak) (holopipe/pipeline.py:188-199)
 // Same algebra as row_pass / col_pass / the fused epilogue; every CTA works on one item.
+// output position of bin n in the group's buffer (one pad per 8: conflict-free pass-3 stores)
+HOLO_DEV int f512_pos(int n) { return n + (n >> 3); }
+
 // 512-point forward FFT by a group of 64 threads, three radix-8 passes (x = t + 64 j in registers
 // -> twiddle W512^(t k) -> S1[k][t]; DFT-8 over t1 of t = t0 + 8 t1 -> twiddle W64^(t0 m1) ->
-// S2[k][m1][t0]; DFT-8 over t0 -> X[k + 8 m1 + 64 m2]).  S1 (8 x 65) also receives the output
-// (natural order, 512); S2 is 64 x 9.  Every pass ends in a CTA barrier (all groups in lockstep).
+// S2[k][m1][t0]; DFT-8 over t0 -> X[k + 8 m1 + 64 m2]).  S1 (8 x 72) also receives the output
+// (bin n at f512_pos(n), 576 float2); S2 is 64 x 9.  Every pass ends in a CTA barrier (all groups in lockstep).
 HOLO_DEV void fft512_group(float2 (&a)[8], int t, const float2* __restrict__ tw, float2* S1, float2* S2) {
   dft8<false>(a);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) S1[k * 65 + t] = k ? cmul(a[k], __ldg(&tw[(t * k) & 511])) : a[k];
+  for (int k = 0; k < 8; ++k) S1[k * 72 + t] = k ? cmul(a[k], __ldg(&tw[(t * k) & 511])) : a[k];
   __syncthreads();
   {
     const int k = t >> 3, t0 = t & 7;
     float2 c[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) c[j] = S1[k * 65 + t0 + 8 * j];
+    for (int j = 0; j < 8; ++j) c[j] = S1[k * 72 + t0 + 8 * j];
     dft8<false>(c);
 #pragma unroll
     for (int m1 = 0; m1 < 8; ++m1)
@@ -643,11 +646,11 @@ HOLO_DEV void fft512_group(float2 (&a)[8], int t, const float2* __restrict__ tw,
     for (int t0 = 0; t0 < 8; ++t0) e[t0] = S2[(k * 8 + m1) * 9 + t0];
     dft8<false>(e);
 #pragma unroll
-    for (int m2 = 0; m2 < 8; ++m2) S1[k + 8 * m1 + 64 * m2] = e[m2];   // S1 is free after pass 2
+    for (int m2 = 0; m2 < 8; ++m2) S1[f512_pos(k + 8 * m1 + 64 * m2)] = e[m2];   // S1 is free after pass 2
   }
   __syncthreads();
 }
-constexpr int kF512Group = 8 * 65 + 64 * 9;   // float2 of scratch per 512-point group
+constexpr int kF512Group = 8 * 72 + 64 * 9;   // float2 of scratch per 512-point group
 
 // Row pass for 512-wide windows: 8 row pairs per 512-thread CTA, one 64-thread group each.
 __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__ RunParams p, int i0, int i1,
@@ -663,7 +666,7 @@ __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__
   const int k0x = g.k0[q][w][0];
   const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
   float2* S1 = reinterpret_cast<float2*>(smem) + grp * kF512Group;
-  float2* S2 = S1 + 8 * 65;
+  float2* S2 = S1 + 8 * 72;
   const int y = y0 + grp;
   float2 a[8];
   if (p.fmt == 0) {
@@ -687,7 +690,7 @@ __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__
     const int kx = pmod(k0x + c - ww / 2, 512);
     const int km = (512 - kx) & 511;
     const float2* X = X0 + s * kF512Group;
-    const float2 zk = X[kx], zm = X[km];
+    const float2 zk = X[f512_pos(kx)], zm = X[f512_pos(km)];
     Ri[(size_t)c * ny + y0 + s] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
     Ri[(size_t)c * ny + y0 + s + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
   }
@@ -709,7 +712,7 @@ __global__ void __launch_bounds__(512) lw_cols512_kernel(const __grid_constant__
   const int cc = min(8, ww - c0);
   const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
   float2* S1 = reinterpret_cast<float2*>(smem) + grp * kF512Group;
-  float2* S2 = S1 + 8 * 65;
+  float2* S2 = S1 + 8 * 72;
   const float2* Rc = R + (size_t)(item - i0) * ww * ny + (size_t)(c0 + min(grp, cc - 1)) * ny;
   float2 a[8];
 #pragma unroll
@@ -722,7 +725,7 @@ __global__ void __launch_bounds__(512) lw_cols512_kernel(const __grid_constant__
   for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) {
     const int j = idx / wh, r = idx - j * wh, c = c0 + j;
     const int ky = pmod(k0y + r - wh / 2, 512);
-    Wg[idx] = cmul(X0[j * kF512Group + ky], __ldg(&wtab[r * ww + c]));
+    Wg[idx] = cmul(X0[j * kF512Group + f512_pos(ky)], __ldg(&wtab[r * ww + c]));
   }
 }
 
