@@ -271,3 +271,43 @@ def test_large_window_path_matches_generic(name):
     b = [t.cpu().numpy() for t in eng.fields16_device()]
     assert np.abs(a[0].astype(int) - b[0]).max() <= 2 and np.abs(a[1].astype(int) - b[1]).max() <= 2
     assert np.allclose(a[2], b[2], rtol=1e-5)
+
+
+def test_large_window_path_features_match_generic():
+    """Large-window kernels with dual-pol, two wavelengths, batch calibration and uint16 frames
+    against the generic fused kernel on the same inputs (rows independent, per-row wavelength)."""
+    from paper_2204_02348_b200.engine import Engine
+    from paper_2204_02348_b200.synth import FrameSpec, make_frames
+    PIX = 20e-6
+    frames = make_frames(FrameSpec(width=640, height=256, pol_count=2, batch=4, group_count=6, waist=300e-6,
+                                   tilt=(1.0, 1.1), noise="poisson", seed=31))
+    def make(u16):
+        eng = Engine()
+        c = eng.config
+        c.frameWidth, c.frameHeight, c.polCount, c.batchCount = 640, 256, 2, 4
+        c.fftWindowSizeX = c.fftWindowSizeY = 256
+        c.framePixelSize, c.wavelengthCentre = PIX, 1565e-9
+        c.fourierWindowRadius = 0.32 * np.degrees(1565e-9 / (2 * PIX))
+        c.wavelengths = [1550e-9, 1580e-9]
+        c.tilt = [[1.0, 1.0], [1.1, 1.1]]
+        c.beamCentre = [[-160 * PIX, 160 * PIX], [0.0, 0.0]]
+        c.basisGroupCount, c.basisWaist = 6, [300e-6, 300e-6]
+        cal = np.array([[1.0 + 0.5j, 0.8 - 0.1j], [0.3j + 1, 1.2]], np.complex64)
+        eng.set_batch_calibration(cal.reshape(-1), 2, 2)
+        if u16:
+            eng.source.set_uint16(np.rint(frames).astype(np.uint16))
+        else:
+            eng.source.set_float32(np.rint(frames).astype(np.float32))
+        return eng
+    out = []
+    for u16, generic in ((False, False), (True, False), (False, True)):
+        eng = make(u16)
+        eng.force_generic = generic
+        eng.run_pipeline(0)
+        out.append([t.cpu().numpy().copy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()])
+    lw, lw16, gen = out
+    for x, y in zip(lw[:2], lw16[:2]):
+        assert np.array_equal(x, y)                       # uint16 == float32 of the same integers
+    assert np.abs(lw[0].astype(int) - gen[0]).max() <= 2 and np.abs(lw[1].astype(int) - gen[1]).max() <= 2
+    assert np.allclose(lw[2], gen[2], rtol=1e-5)
+    assert rel_l2_rows(lw[3], gen[3]) <= 2e-5
