@@ -311,3 +311,31 @@ def test_large_window_path_features_match_generic():
     assert np.abs(lw[0].astype(int) - gen[0]).max() <= 2 and np.abs(lw[1].astype(int) - gen[1]).max() <= 2
     assert np.allclose(lw[2], gen[2], rtol=1e-5)
     assert rel_l2_rows(lw[3], gen[3]) <= 2e-5
+
+
+@pytest.mark.parametrize("path", ["default", "tc", "tc2", "generic"])
+def test_zero_frames_give_zero_fields_and_unit_scale(path):
+    """peak = 0 -> scale 1, all-zero int16 fields and coefficients (pipeline.py:194-198), every kernel."""
+    case, g, frames = load("dualpol")
+    eng = _engine(case, np.zeros_like(frames))
+    eng.use_tc = path == "tc"
+    eng.use_tc2 = path == "tc2"
+    eng.force_generic = path == "generic"
+    eng.run_pipeline(0)
+    fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
+    assert not fr.any() and not fi.any()
+    assert np.all(sc == 1.0)
+    assert not np.abs(eng.coefs_device().cpu().numpy()).any()
+
+
+def test_single_frame_batch():
+    """B = 1 through the default kernel equals row 0 of the 3-frame batch."""
+    case, g, frames = load("dualpol")
+    a = _engine(case, frames)
+    a.run_pipeline(0)
+    one = dict(case, config=dict(case["config"], batchCount=1))
+    b = _engine(one, frames[:1])
+    b.run_pipeline(0)
+    for x, y in zip(a.fields16_device(), b.fields16_device()):
+        assert np.array_equal(x.cpu().numpy()[:1], y.cpu().numpy())
+    assert np.array_equal(a.coefs_device().cpu().numpy()[:1], b.coefs_device().cpu().numpy())
