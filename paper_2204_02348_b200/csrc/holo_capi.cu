@@ -499,11 +499,23 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
       const int kx = g.k0[q][w][0], ky = g.k0[q][w][1];
       for (int c = 0; c < g.ww; ++c) {
         const double ax = 2.0 * kPi * (double)(kx + c - g.ww / 2) * (xi[q][0] - g.nx / 2.0) / g.nx;
-        pxv[pl * g.ww + c] = make_float2((float)std::cos(ax), (float)std::sin(ax));
+        // fill-factor envelope (pipeline.py:99-103) folded in: sinc(fx) sinc(fy) >= (2/pi)^2 inside
+        // the Nyquist band, so the 1e-3 floor never binds and the envelope is separable
+        double ex = 1.0;
+        if (d->fill_factor) {
+          int txm = (kx + c - g.ww / 2) % g.nx; if (txm < 0) txm += g.nx;
+          ex = sinc((double)(txm <= g.nx / 2 ? txm : g.nx - txm) / g.nx);
+        }
+        pxv[pl * g.ww + c] = make_float2((float)(std::cos(ax) / ex), (float)(std::sin(ax) / ex));
       }
       for (int r = 0; r < g.wh; ++r) {
         const double ay = 2.0 * kPi * (double)(ky + r - g.wh / 2) * (xi[q][1] - g.ny / 2.0) / g.ny;
-        pyv[pl * g.wh + r] = make_float2((float)std::cos(ay), (float)std::sin(ay));
+        double ey = 1.0;
+        if (d->fill_factor) {
+          int tym = (ky + r - g.wh / 2) % g.ny; if (tym < 0) tym += g.ny;
+          ey = sinc((double)(tym > g.ny / 2 ? tym - g.ny : tym) / g.ny);
+        }
+        pyv[pl * g.wh + r] = make_float2((float)(std::cos(ay) / ey), (float)(std::sin(ay) / ey));
       }
     }
   for (int c = 0; c < g.ww; ++c) {

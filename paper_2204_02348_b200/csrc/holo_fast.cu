@@ -364,7 +364,8 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
-    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc);
+    const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * WH * WW : nullptr;
+    float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc, 1.f, -1, -1, rc);
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
     if ((tid & 31) == 0) redf[tid >> 5] = lmax;
@@ -494,8 +495,10 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
 
 bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal,
                     unsigned flags, const void* windows) {
+  (void)fill;   // the fill-factor envelope is folded into the separable recentring tables
+  (void)rcal;   // the reference calibration is applied in the final IFFT stage
   return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
-         g.G <= FastLayout<42, 42>::GMAX && !(fmt == 1 && transpose) && !fill && rcal == nullptr &&
+         g.G <= FastLayout<42, 42>::GMAX && !(fmt == 1 && transpose) &&
          (flags & 1u) == 0 && windows == nullptr;
 }
 

@@ -54,7 +54,7 @@ HOLO_DEV void ct_stage(const float2* __restrict__ src, float2* __restrict__ dst,
 template <int P, int N, int L, int COUNT>
 HOLO_DEV float ct_stage_final_rows(const float2* __restrict__ src, float2* __restrict__ dst, const float2* tw,
                                    const float2* ey, const float2* ex, bool use_bc, float2 bc, float osc = 1.f,
-                                   int tid0 = -1, int nthr = -1) {
+                                   int tid0 = -1, int nthr = -1, const float2* __restrict__ rc = nullptr) {
   constexpr int m_in = N / L, mp = m_in / P, per = N / P, total = COUNT * per;
   static_assert(mp == 1, "final stage");
   float lmax = 0.f;
@@ -74,6 +74,7 @@ HOLO_DEV float ct_stage_final_rows(const float2* __restrict__ src, float2* __res
       const int x = k + L * t;
       float2 o = cmul(cmul(v[t], eyq), ex[x]);
       if (use_bc) o = cmul(o, bc);
+      if (rc) o = cmul(o, __ldg(&rc[y * N + x]));   // reference calibration (engine.py:250-255)
       lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
       dst[y * N + x] = o;
     }

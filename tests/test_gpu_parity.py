@@ -339,3 +339,19 @@ def test_single_frame_batch():
     for x, y in zip(a.fields16_device(), b.fields16_device()):
         assert np.array_equal(x.cpu().numpy()[:1], y.cpu().numpy())
     assert np.array_equal(a.coefs_device().cpu().numpy()[:1], b.coefs_device().cpu().numpy())
+
+
+@pytest.mark.parametrize("name", ["pr1", "dualpol"])
+def test_fill_factor_in_the_fast_kernel_matches_generic(name):
+    """Fill-factor envelope folded into the separable recentring tables == the generic window table."""
+    case, g, frames = load(name)
+    case = dict(case, config=dict(case["config"], fillFactorCorrectionEnabled=1))
+    eng = _engine(case, frames)
+    eng.run_pipeline(0)
+    a = [t.cpu().numpy().copy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy().copy()]
+    eng.force_generic = True
+    eng.run_pipeline(0)
+    b = [t.cpu().numpy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()]
+    assert np.abs(a[0].astype(int) - b[0]).max() <= 2 and np.abs(a[1].astype(int) - b[1]).max() <= 2
+    assert np.allclose(a[2], b[2], rtol=1e-5)
+    assert rel_l2_rows(a[3], b[3]) <= 2e-5
