@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
   extern __shared__ __align__(16) char smem[];
   __shared__ float redf[8];
   __shared__ int slot[128];
+  __shared__ int slot_both;
   int slot_kxs = -1;
   float2* zs = reinterpret_cast<float2*>(smem + LY::zs);
   float2* xbuf = reinterpret_cast<float2*>(smem + LY::xbuf);
@@ -248,15 +249,22 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
       s_py[i] = ft.py[pl * WH + i];
       s_ey[i] = p.t.rem_y[pl * WH + i];
     }
-    if (kxs != slot_kxs) {   // FFT bin -> zs slots (packed int16 pair, -1 = not in the window)
+    if (kxs != slot_kxs) {   // FFT bin -> zs slots: primary | secondary << 16 (-1 = none)
+      if (tid == 0) slot_both = 0;
+      __syncthreads();
       for (int kk = tid; kk < 128; kk += blockDim.x) {
         const int cp = (kk - kxs) & 127, cm = (128 - kk - kxs) & 127;
         const int sp = cp < WW ? zs_pos<WW>(cp) : -1, sn = cm < WW ? zs_neg<WW>(cm) : -1;
-        slot[kk] = (sp & 0xffff) | (sn << 16);
+        // a bin is normally in the +kx window or the mirrored -kx one; both only when the window
+        // reaches kx = 0 or nx/2 -- then the secondary slot is used (flag checked per item)
+        const int pri = sp >= 0 ? sp : sn, sec = sp >= 0 ? sn : -1;
+        slot[kk] = (pri & 0xffff) | (sec << 16);
+        if (sec >= 0) slot_both = 1;
       }
       slot_kxs = kxs;
       __syncthreads();
     }
+    const bool both = slot_both != 0;
 
     // ------------------------------------------------------------ row pass
     const int W = g.W, H = g.H;
@@ -284,10 +292,13 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
         fft128_stage2(z, h, xg, t, v);
 #pragma unroll
         for (int k2 = 0; k2 < 8; ++k2) {
-          const int sl = slot[t + 8 * h + 16 * k2];   // zs slots of bin kk as +kx_c and as -kx_c
-          const int sp = (short)(sl & 0xffff), sn = sl >> 16;
+          const int sl = slot[t + 8 * h + 16 * k2];   // zs slot(s) of bin kk: +kx_c and/or -kx_c
+          const int sp = (short)(sl & 0xffff);
           if (sp >= 0) zrow[sp] = v[k2];
-          if (sn >= 0) zrow[sn] = v[k2];
+          if (both) {
+            const int sn = sl >> 16;
+            if (sn >= 0) zrow[sn] = v[k2];
+          }
         }
       }
     }
