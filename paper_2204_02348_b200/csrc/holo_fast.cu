@@ -1,9 +1,10 @@
 // Fused kernel for the hot geometry class: 128 x 128 FFT window, a WH x WW
 // (42 x 42 for BASELINE) Fourier window, IFFT resolution mode 1, no
-// averaging, no fill-factor correction.  Same algorithm and numerical
-// conventions as the generic kernel (holo_pipeline.cu) with every size a
-// compile-time constant.  One (frame, pol) item per 256-thread CTA at a time,
-// three CTAs per SM (64 KB shared memory, <= 85 registers):
+// averaging (fill-factor envelope and reference calibration are folded in).
+// Same algorithm and numerical conventions as the generic kernel
+// (holo_pipeline.cu) with every size a compile-time constant.  One (frame, pol)
+// item per 256-thread CTA at a time, three CTAs per SM (64 KB shared memory,
+// <= 85 registers); TCO = true moves the HG overlap onto tcgen05 (G > 16):
 //
 //   row pass    8 threads per (row y, row y+64) pair, 16 points per thread:
 //               DFT-16 in registers -> twiddle W128^(t k1) -> two 8x8

@@ -17,11 +17,12 @@
 //   f  (window, per item)   shared memory, canonical K-major layout, two K chunks
 //   D  (accumulator)        TMEM columns [128,256), drained to shared memory
 //
-// One elected thread issues 24 tcgen05.mma per window and commits to an
-// mbarrier.  Everything after the row pass -- column FFTs, 42x42 IFFT,
-// removal phase, int16 packing, HG overlap -- is the SIMT code of holo_fast.cu
-// (shared helpers in holo_fast_common.cuh).  Two 384-thread CTAs per SM
-// (256 TMEM columns each).
+// Warp-specialised (one 512-thread CTA per SM, all 512 TMEM columns): warps 0-3
+// stage windows and issue the 24 tcgen05.mma per window into one of two TMEM
+// accumulators; warps 4-15 drain them and run everything after the row pass --
+// column FFTs, 42x42 IFFT, removal phase, int16 packing, HG overlap -- with the
+// SIMT code of holo_fast.cu (shared helpers in holo_fast_common.cuh).  Opt-in
+// (HPG_FLAG_TC): the SIMT tail on 12 warps is slower than fast128_kernel.
 #include <cuda_fp16.h>
 
 #include <algorithm>
