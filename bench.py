@@ -321,6 +321,9 @@ def main():
         kernel_name = "holo::fast128tc_kernel<42,42>"
     elif nx == 128 and ny == 128 and gh == 42 and gw == 42:
         kernel_name = "holo::fast128_kernel<42,42>"
+    elif nx == 512 and ny == 512:
+        # one hpg_run = the five L2-chunked large-window kernels; the roofline is taken over all of them
+        kernel_name = "holo::lw_rows512+lw_cols512+lw_ifft_y+lw_field+lw_pack (large-window path)"
     else:
         kernel_name = "holo::fused_kernel"
     traffic = args.traffic_bytes

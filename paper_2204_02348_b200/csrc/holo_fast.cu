@@ -34,14 +34,15 @@
 
 namespace holo {
 
-template <int WH, int WW>
+template <int WH, int WW, int NT = 256>
 struct FastLayout {
   static constexpr int ZS = 2 * WW + 2;            // zs row pitch (float2)
   static constexpr int XG = 72;                    // 8x8 exchange tile per 8-thread group (float2)
+  static constexpr int NG = NT / 8;                // 8-thread FFT groups per CTA
   static constexpr int GMAX = 48;                  // max basis orders on this path
   static constexpr size_t zs = 0;                                          // [64][ZS]
-  static constexpr size_t xbuf = zs + 64 * ZS * sizeof(float2);            // [32][XG]
-  static constexpr size_t tw128 = xbuf + 32 * XG * sizeof(float2);         // [128]
+  static constexpr size_t xbuf = zs + 64 * ZS * sizeof(float2);            // [NG][XG]
+  static constexpr size_t tw128 = xbuf + NG * XG * sizeof(float2);         // [128]
   static constexpr size_t twh = tw128 + 128 * sizeof(float2);              // [WH]
   static constexpr size_t tww = twh + WH * sizeof(float2);                 // [WW]
   static constexpr size_t ph = tww + WW * sizeof(float2);                  // px[WW] py[WH] ex[WW] ey[WH]
@@ -191,13 +192,16 @@ HOLO_DEV void tco_overlap(const RunParams& p, const FastTables& ft, int item, in
   tc_fence_before();
 }
 
-template <int WH, int WW, bool TCO>
-__global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__ RunParams p,
-                                                        const __grid_constant__ FastTables ft) {
-  using LY = FastLayout<WH, WW>;
-  constexpr int ZS = LY::ZS;
+// NT = 256: the throughput configuration (3 CTAs/SM).  NT = 512: one window per SM with every phase in a
+// single round, for batches smaller than the SM count (latency-bound, e.g. PR1's 16 windows).
+template <int WH, int WW, bool TCO, int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __grid_constant__ RunParams p,
+                                                                       const __grid_constant__ FastTables ft) {
+  using LY = FastLayout<WH, WW, NT>;
+  constexpr int ZS = LY::ZS, NG = LY::NG, NW = NT / 32;
+  static_assert(!TCO || NT == 256, "the TMEM drain assumes 8 warps");
   extern __shared__ __align__(16) char smem[];
-  __shared__ float redf[8];
+  __shared__ float redf[NW];
   __shared__ int slot[128];
   __shared__ int slot_both;
   int slot_kxs = -1;
@@ -270,8 +274,7 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
     // ------------------------------------------------------------ row pass
     const int W = g.W, H = g.H;
 #pragma unroll 1
-    for (int rnd = 0; rnd < 2; ++rnd) {
-      const int pr = rnd * 32 + grp;
+    for (int pr = grp; pr < 64; pr += NG) {   // warp-uniform trip count
       float2 z[16];
       if (p.fmt == 0) {
         const float* fa = reinterpret_cast<const float*>(p.frames) + (int64_t)b * W * H +
@@ -323,8 +326,8 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
 
     // --------------------------------------------------------- column pass
 #pragma unroll 1
-    for (int rnd = 0; rnd < 2; ++rnd) {
-      const int c = rnd * 32 + grp;
+    for (int rnd = 0; rnd < (WW + NG - 1) / NG; ++rnd) {
+      const int c = rnd * NG + grp;
       const bool active = c < WW;
       float2 z[16];
       if (active) {
@@ -384,7 +387,7 @@ __global__ void __launch_bounds__(256, 3) fast128_kernel(const __grid_constant__
     __syncthreads();
     lmax = redf[0];
 #pragma unroll
-    for (int j = 1; j < 8; ++j) lmax = fmaxf(lmax, redf[j]);
+    for (int j = 1; j < NW; ++j) lmax = fmaxf(lmax, redf[j]);
     if (p.raw)
       for (int i = tid; i < WH * WW; i += blockDim.x) p.raw[(size_t)item * WH * WW + i] = F[i];
     const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;
@@ -514,36 +517,45 @@ bool fast_supported(const Geometry& g, int A, int fmt, int transpose, int fill, 
          (flags & 1u) == 0 && windows == nullptr;
 }
 
-cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
-  using LY = FastLayout<42, 42>;
+template <int NT>
+static cudaError_t launch_fast_nt(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
+  using LY = FastLayout<42, 42, NT>;
   const int GP = (p.g.G + 3) & ~3;
   const size_t bytes = LY::bytes + ((p.coefs && p.g.G > 0 && GP <= kPersistentBasisGP)
                                         ? (size_t)(42 + 42) * GP * sizeof(float) : 0);
+  // tensor-core overlap pays for large bases (G > 16: config 5 G = 45 +32 %); below that its two MMA
+  // round trips per item cost more than the SIMT overlap they replace (dual-pol G = 14: -10 %)
+  const bool tco = NT == 256 && ft.tco_gp >= 32 && p.coefs && p.g.G > 0 && !(p.flags & kFlagNoTco);
+  auto kt = fast128_kernel<42, 42, true, 256>;
+  auto kf = fast128_kernel<42, 42, false, NT>;
   static size_t configured = 0;
   if (bytes > configured) {
-    cudaError_t e = cudaFuncSetAttribute(fast128_kernel<42, 42, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fast128_kernel<42, 42, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
+    e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     configured = bytes;
   }
   int per_sm = 0;
-  // tensor-core overlap pays for large bases (G > 16: config 5 G = 45 +32 %); below that its two MMA
-  // round trips per item cost more than the SIMT overlap they replace (dual-pol G = 14: -10 %)
-  const bool tco = ft.tco_gp >= 32 && p.coefs && p.g.G > 0 && !(p.flags & kFlagNoTco);
   // same registers / shared memory for both variants; the occupancy API reports 1 CTA/SM for kernels that
   // allocate tensor memory, but 3 x 128 TMEM columns fit the SM's 512
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fast128_kernel<42, 42, false>, 256, bytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, NT, bytes);
   if (tco) per_sm = std::min(per_sm, 4);
   const int items = p.B * p.g.P;
   const int grid = std::max(1, std::min(items, num_sms * std::max(per_sm, 1)));
   if (tco)
-    fast128_kernel<42, 42, true><<<grid, 256, bytes, s>>>(p, ft);
+    kt<<<grid, 256, bytes, s>>>(p, ft);
   else
-    fast128_kernel<42, 42, false><<<grid, 256, bytes, s>>>(p, ft);
+    kf<<<grid, NT, bytes, s>>>(p, ft);
   return cudaGetLastError();
+}
+
+cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
+  // fewer windows than SMs: nothing to overlap across CTAs, so give each window the whole SM
+  const char* e = getenv("HOLO_FAST_NT");
+  const int items = p.B * p.g.P;
+  const bool wide = e ? atoi(e) == 512 : items <= num_sms;
+  return wide ? launch_fast_nt<512>(p, ft, num_sms, s) : launch_fast_nt<256>(p, ft, num_sms, s);
 }
 
 }  // namespace holo
