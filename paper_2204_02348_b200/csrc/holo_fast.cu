@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __
   const int items = p.B * g.P;
   int staged_q = -1;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int b = item / g.P, q = item - b * g.P;
+    const int b = g.P == 1 ? item : (g.P == 2 ? item >> 1 : item / g.P), q = item - b * g.P;
     const int w = p.wl ? p.wl[b] : 0;
     const int pl = q * g.L + w;
     const int kxs = (g.k0[q][w][0] - WW / 2) & 127, kys = (g.k0[q][w][1] - WH / 2) & 127;
@@ -316,10 +316,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __
         const int es = p.fmt == 0 ? 4 : 2;
         const char* base = reinterpret_cast<const char*>(p.frames) +
                            ((int64_t)nb * W * H + (int64_t)g.row0[nq] * W + g.col0[nq]) * es;
-        for (int i = tid; i < 128 * 5; i += blockDim.x) {
-          const int row = i / 5, part = i - row * 5;
-          const int off = min(part * 128, 128 * es - 1);
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (int64_t)row * W * es + off));
+        if (tid < 128) {   // one bulk prefetch per window row: the 16-byte aligned span inside the row
+          const uintptr_t a = reinterpret_cast<uintptr_t>(base + (int64_t)tid * W * es);
+          const uintptr_t a0 = (a + 15) & ~uintptr_t(15), a1 = (a + 128 * es) & ~uintptr_t(15);
+          if (a1 > a0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"((uint32_t)(a1 - a0)) : "memory");
         }
       }
     }
@@ -329,6 +330,8 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __
     for (int rnd = 0; rnd < (WW + NG - 1) / NG; ++rnd) {
       const int c = rnd * NG + grp;
       const bool active = c < WW;
+      // warps whose four groups are all past the last column skip the round (the exchange is warp-local)
+      if (rnd > 0 && rnd * NG + ((tid >> 5) << 2) >= WW) continue;
       float2 z[16];
       if (active) {
         const int sp = zs_pos<WW>(c), sn = zs_neg<WW>(c);
