@@ -301,6 +301,7 @@ def main():
             ends[i].record()
         torch.cuda.synchronize()
     barrier(world)
+    launches_per_step = int(native.lib().hpg_last_launch_count())   # kernels the last hpg_run launched
     per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_local = float(np.mean(per_step))
     ms = max_over_ranks(ms_local, world)
@@ -395,7 +396,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
         }
         if autoalign is not None:

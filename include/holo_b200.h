@@ -141,6 +141,9 @@ int hpg_plan_get_basis(const hpg_plan* plan, float* hx, float* hy);
 int hpg_workspace_size(const hpg_plan* plan, int32_t batch_count, uint32_t flags, size_t* bytes);
 int hpg_run(const hpg_plan* plan, const hpg_batch* batch, const hpg_outputs* out,
             uint32_t flags, void* stream);
+/* Number of kernels the calling thread's last hpg_run launched (0 after an error); the bench
+ * reports it as gpu_launches.  No reference counterpart (instrumentation). */
+int hpg_last_launch_count(void);
 /* Aggregate slot (index B of field_params) and total intensity [gh][gw] from the
  * partials hpg_run(HPG_FLAG_SUMMARY) left in the workspace. */
 int hpg_finalize_summary(const hpg_plan* plan, const hpg_batch* batch, const hpg_outputs* out,

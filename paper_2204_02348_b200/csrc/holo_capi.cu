@@ -31,6 +31,8 @@ bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, c
 size_t tc2_workspace(int64_t items);
 bool lw_supported(const Geometry& g, int A, const void* members, unsigned flags, const void* windows);
 size_t lw_workspace(const Geometry& g, int64_t items);
+int64_t lw_chunk(const Geometry& g);
+int64_t tc2_chunk();
 cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
 cudaError_t launch_plane_summary(const float2* data, int64_t count, int P, int h, int w, const double* xa,
@@ -44,6 +46,7 @@ cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, fl
 using namespace holo;
 
 static thread_local std::string g_last_error;
+static thread_local int g_last_launches = 0;   // kernels the last hpg_run on this thread launched
 
 static int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -693,7 +696,10 @@ static int fill_params(const hpg_plan* P, const hpg_batch* b, const hpg_outputs*
   return HPG_SUCCESS;
 }
 
+int hpg_last_launch_count(void) { return g_last_launches; }
+
 int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_t flags, void* stream) {
+  g_last_launches = 0;
   if (!P || !b || !o) return fail(HPG_NULLPOINTER, "null argument");
   if (!b->frames || !o->field_r || !o->field_i || !o->field_scale) return fail(HPG_NULLPOINTER, "null buffer");
   if (b->batch_count < 1) return fail(HPG_INVALIDDIMENSION, "batch_count");
@@ -718,27 +724,37 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
   if ((rp.lay.slab_bytes > 0 || (flags & HPG_FLAG_SUMMARY)) && (!o->workspace || (int64_t)o->workspace_bytes < need))
     return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
   cudaError_t e;
+  const int64_t items = (int64_t)b->batch_count * P->g.P;
   if ((flags & HPG_FLAG_TC2) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
       tc2_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows)) {
     if (!o->workspace || o->workspace_bytes < tc2_workspace((int64_t)b->batch_count * P->g.P))
       return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
     e = ensure_tc_tables(P);
     if (e == cudaSuccess) e = launch_tc2(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+    g_last_launches = 2 * (int)((items + tc2_chunk() - 1) / tc2_chunk());
   } else if ((flags & HPG_FLAG_TC) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
       tc_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows))
   {
     e = ensure_tc_tables(P);
     if (e == cudaSuccess) e = launch_fast_tc(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+    g_last_launches = 1;
   }
   else if (!(flags & HPG_FLAG_GENERIC) && fast_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows) &&
-      !b->members)
+      !b->members) {
     e = launch_fast(rp, P->ft, P->num_sms, static_cast<cudaStream_t>(stream));
+    g_last_launches = 1;
+  }
   else if (!(flags & HPG_FLAG_GENERIC) && lw_supported(rp.g, A, b->members, flags, o->windows)) {
     if (!o->workspace || o->workspace_bytes < lw_workspace(rp.g, (int64_t)b->batch_count * P->g.P))
       return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
     e = launch_lw(rp, P->num_sms, static_cast<cudaStream_t>(stream));
-  } else
+    const int per_chunk = (rp.g.nx == 512 && rp.g.ny == 512) ? 5 : 4;   // rows, cols, [ifft_y,] field, pack
+    g_last_launches = per_chunk * (int)((items + lw_chunk(rp.g) - 1) / lw_chunk(rp.g)) +
+                      ((rp.coefs && rp.g.G > 0) ? 1 : 0);
+  } else {
     e = launch_fused(rp, static_cast<cudaStream_t>(stream));
+    g_last_launches = 1;
+  }
   if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
   return HPG_SUCCESS;
 }

@@ -608,6 +608,8 @@ bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, c
          (flags & 1u) == 0 && windows == nullptr && aligned;
 }
 
+int64_t tc2_chunk() { return kTc2Chunk; }
+
 size_t tc2_workspace(int64_t items) {
   return (size_t)std::min<int64_t>(items, kTc2Chunk) * 42 * 42 * sizeof(float2);
 }

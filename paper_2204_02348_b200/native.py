@@ -33,6 +33,7 @@ EXPORTS = [
     "hpg_plan_get_basis", "hpg_workspace_size", "hpg_run", "hpg_finalize_summary",
     "hpg_fourier_full", "hpg_extract_coefs", "hpg_ref_calibration_finish", "hpg_metric_partials", "hpg_plane_summary",
     "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_upload_windows", "hpg_last_error",
+    "hpg_last_launch_count",
 ]
 
 
@@ -104,6 +105,7 @@ def lib():
     L = ctypes.CDLL(LIB_PATH)
     P = ctypes.POINTER
     L.hpg_version.restype = c_int32
+    L.hpg_last_launch_count.restype = c_int32
     L.hpg_last_error.restype = ctypes.c_char_p
     L.hpg_plan_create.argtypes = [P(PlanDesc), P(c_void_p)]
     L.hpg_plan_destroy.argtypes = [c_void_p]
