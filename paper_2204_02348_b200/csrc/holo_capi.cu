@@ -8,6 +8,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <mutex>
+#include <tuple>
 
 #include <cuda_fp16.h>
 
@@ -46,6 +48,34 @@ cudaError_t launch_refcal_finish(const float2* a, const float2* b, int64_t n, fl
 using namespace holo;
 
 static thread_local std::string g_last_error;
+
+// Device blocks of destroyed plans, handed to later plans of the same size on the same device.
+// AutoAlign builds a plan per evaluation (holopipe/align.py:25-29 re-runs the pipeline with new
+// parameters); cudaMalloc + cudaFree of the table block cost ~0.6 ms per evaluation, several times
+// the evaluation itself.  A block is pooled only after the device is idle (cudaFree semantics).
+static std::mutex g_pool_mu;
+static std::vector<std::tuple<int, size_t, void*>> g_pool;
+constexpr size_t kPoolMax = 64;
+
+static cudaError_t pool_alloc(int device, size_t bytes, void** p) {
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    for (size_t i = 0; i < g_pool.size(); ++i)
+      if (std::get<0>(g_pool[i]) == device && std::get<1>(g_pool[i]) == bytes) {
+        *p = std::get<2>(g_pool[i]);
+        g_pool.erase(g_pool.begin() + (std::ptrdiff_t)i);
+        return cudaSuccess;
+      }
+  }
+  return cudaMalloc(p, bytes);
+}
+
+static void pool_free(int device, size_t bytes, void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (g_pool.size() < kPoolMax) g_pool.emplace_back(device, bytes, p);
+  else cudaFree(p);
+}
 static thread_local int g_last_launches = 0;   // kernels the last hpg_run on this thread launched
 
 static int fail(int code, const std::string& msg) {
@@ -65,6 +95,7 @@ struct hpg_plan {
   FastTables ft{};
   int fill = 0;
   void* dev = nullptr;         // one allocation for every table
+  size_t dev_bytes = 0, tc_bytes = 0;
   std::vector<float> xa, ya;   // host copies of the axes
   std::vector<float> hx, hy;   // host copies of the dequantised basis
   int device = 0;
@@ -303,8 +334,9 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
   if (a2_tc.empty()) a2_tc.push_back(0u);
   std::vector<char> blob;
   const size_t o1 = push(blob, a_tc), o2 = push(blob, a2_tc);
-  cudaError_t e = cudaMalloc(&P->tc_dev, blob.size());
+  cudaError_t e = pool_alloc(P->device, blob.size(), &P->tc_dev);
   if (e != cudaSuccess) { P->tc_dev = nullptr; return e; }
+  P->tc_bytes = blob.size();
   e = cudaMemcpy(P->tc_dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) return e;
   P->ft.a_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o1);
@@ -549,9 +581,10 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   const double t_host = g_plan_timing ? now_us() : 0.0;
   cudaGetDevice(&P->device);
   cudaDeviceGetAttribute(&P->num_sms, cudaDevAttrMultiProcessorCount, P->device);
-  cudaError_t e = cudaMalloc(&P->dev, blob.size());
+  cudaError_t e = pool_alloc(P->device, blob.size(), &P->dev);
   const double t_alloc = g_plan_timing ? now_us() : 0.0;
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "cudaMalloc(plan tables)"); }
+  P->dev_bytes = blob.size();
   e = cudaMemcpy(P->dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { cudaFree(P->dev); delete P; return cuda_fail(e, "cudaMemcpy(plan tables)"); }
   char* base = static_cast<char*>(P->dev);
@@ -591,8 +624,16 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
 
 int hpg_plan_destroy(hpg_plan* P) {
   if (!P) return fail(HPG_NULLPOINTER, "null plan");
-  if (P->dev) cudaFree(P->dev);
-  if (P->tc_dev) cudaFree(P->tc_dev);
+  if (P->dev || P->tc_dev) {
+    // kernels still in flight may read the tables: wait for the plan's device like cudaFree would
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (cur != P->device) cudaSetDevice(P->device);
+    cudaDeviceSynchronize();
+    if (cur != P->device && cur >= 0) cudaSetDevice(cur);
+    pool_free(P->device, P->dev_bytes, P->dev);
+    pool_free(P->device, P->tc_bytes, P->tc_dev);
+  }
   delete P;
   return HPG_SUCCESS;
 }
