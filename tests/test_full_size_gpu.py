@@ -1,0 +1,99 @@
+"""GPU tests at BASELINE.json's full sizes, through size-independent properties.
+
+The oracle finishes only small batches in seconds, so at full size the checks are:
+  * batch independence -- every row of the full batch is bit-equal to the same frame run in a
+    small batch (rows are independent in the reference: holopipe/engine.py:135-385 loops or
+    vectorises over rows with no cross-row term);
+  * tiling -- config 5's 65,536-frame batch is 1,024 distinct frames repeated 64 times; every
+    repetition must reproduce the first bit for bit (no row-position dependence anywhere in
+    the grid-stride kernel, the largest batch the path sees);
+  * a handful of rows against the oracle, within the BASELINE tolerance (1e-4 relative L2).
+"""
+
+import numpy as np
+import pytest
+
+import bench
+from oracle import holo_oracle as O
+from paper_2204_02348_b200.synth import FrameSpec, make_frames
+from tests.golden_util import dequant, rel_l2_rows
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def _run(cfg, frames_dev, B):
+    from paper_2204_02348_b200.engine import Engine
+    eng = Engine()
+    for k, v in cfg.items():
+        setattr(eng.config, k, v)
+    eng.config.batchCount = B
+    eng.source.set_float32(frames_dev)
+    eng.run_pipeline(0)
+    fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
+    co = eng.coefs_device()
+    return fr, fi, sc, (None if co is None or co.numel() == 0 else co.cpu().numpy())
+
+
+def _check_oracle(cfg, frames_host, rows, out):
+    fr, fi, sc, co = out
+    ref = O.run_chain(O.Cfg(**dict(cfg, batchCount=len(rows))), frames_host[rows])
+    P = cfg["polCount"]
+    got = dequant(fr[rows], fi[rows], sc[rows]).reshape(len(rows) * P, -1)
+    exp = dequant(ref["fr"], ref["fi"], ref["scale"]).reshape(len(rows) * P, -1)
+    assert rel_l2_rows(got, exp) <= TOL
+    if co is not None:
+        assert rel_l2_rows(co[rows], ref["coefs"]) <= TOL
+
+
+def _same(a, b, rows_a, rows_b):
+    for x in range(3):
+        assert np.array_equal(a[x][rows_a], b[x][rows_b])
+    if a[3] is not None:
+        assert np.array_equal(a[3][rows_a], b[3][rows_b])
+
+
+@pytest.mark.parametrize("name", ["dualpol", "largeframe"])
+def test_full_batch_rows_equal_small_batches_and_oracle(name):
+    """Config 2 (1,000 dual-pol frames) and config 3 (256 frames of 1024 x 1024) at full size."""
+    import torch
+    fspec, cfg = bench.config_for(name)
+    B = fspec["batch"]
+    frames = make_frames(FrameSpec(**fspec))
+    dev = torch.device("cuda", 0)
+    full = _run(cfg, torch.from_numpy(frames).to(dev), B)
+    for lo in (0, B // 2, B - 8):   # first, middle and last rows of the batch, run alone
+        part = _run(cfg, torch.from_numpy(frames[lo:lo + 8].copy()).to(dev), 8)
+        _same(full, part, slice(lo, lo + 8), slice(0, 8))
+    _check_oracle(cfg, frames, np.array([0, B // 2, B - 1]), full)
+
+
+def test_large_basis_65536_frames_tiled():
+    """Config 5 at its full 65,536-frame batch on one GPU (1,035 HG modes)."""
+    import torch
+    fspec, cfg = bench.config_for("largebasis", batch=1024)
+    frames = make_frames(FrameSpec(**fspec))
+    dev = torch.device("cuda", 0)
+    reps = 64
+    tiled = torch.from_numpy(frames).to(dev).repeat(reps, 1, 1)   # 21.5 GB of float32 frames
+    full = _run(cfg, tiled, 1024 * reps)
+    del tiled
+    torch.cuda.empty_cache()
+    for r in range(1, reps):
+        _same(full, full, slice(r * 1024, (r + 1) * 1024), slice(0, 1024))
+    _check_oracle(cfg, frames, np.array([0, 511, 1023]), full)
+
+
+def test_launch_count_reported():
+    """hpg_last_launch_count: one fused launch on the 128-window path, per-chunk kernels on the
+    large-window path (bench.py reports it as gpu_launches)."""
+    import torch
+    from paper_2204_02348_b200 import native
+    fspec, cfg = bench.config_for("pr1")
+    frames = make_frames(FrameSpec(**fspec))
+    _run(cfg, torch.from_numpy(frames).cuda(), fspec["batch"])
+    assert native.lib().hpg_last_launch_count() == 1
+    fspec, cfg = bench.config_for("largeframe", batch=4)
+    frames = make_frames(FrameSpec(**fspec))
+    _run(cfg, torch.from_numpy(frames).cuda(), 4)
+    assert native.lib().hpg_last_launch_count() == 5   # rows, cols, IFFT along y, field, pack
