@@ -45,15 +45,36 @@ class MetricsReport:
         self.wavelength_count = int(wavelength_count)
         self.values = np.full((C.METRIC_COUNT, self.wavelength_count + 1), C.METRIC_UNSET,
                               dtype=np.float32)
+        self._mdl_pending = None   # [(slot, gram, nd)]: MDL eigenvalues computed on first read
+
+    def defer_mdl(self, pending):
+        """MDL needs the eigenvalues of each wavelength's Gram matrix (~0.1-0.2 ms of LAPACK for 45 modes);
+        AutoAlign reads only its goal metric per evaluation, so the decomposition runs on the first read
+        of METRIC_MDL instead of inside every calc_metrics."""
+        self._mdl_pending = list(pending) or None
+
+    def _resolve(self, idx):
+        if idx != C.METRIC_MDL or self._mdl_pending is None:
+            return
+        L = self.wavelength_count
+        row = np.full(L, C.METRIC_UNSET, np.float64)
+        for w, gram, nd in self._mdl_pending:
+            row[w] = mdl_db(gram, nd)
+            self.values[C.METRIC_MDL, w] = np.float32(row[w])
+        self._mdl_pending = None
+        ok = row[row > C.METRIC_UNSET / 2]
+        self.values[C.METRIC_MDL, L] = np.float32(ok.mean()) if ok.size else C.METRIC_UNSET
 
     def get(self, idx):
         if not (0 <= idx < C.METRIC_COUNT):
             return 0.0
+        self._resolve(idx)
         return float(self.values[idx, self.wavelength_count])
 
     def get_all(self, idx):
         if not (0 <= idx < C.METRIC_COUNT):
             return None
+        self._resolve(idx)
         return self.values[idx].copy()
 
 
@@ -69,7 +90,16 @@ def _snr(sig, noise):
     return min(10.0 * math.log10(sig / noise), SNR_CAP_DB)
 
 
-def finish_metrics(row_power, diag_power, group_power, gram, rows, cols, have_labels=True):
+def mdl_db(gram, nd):
+    """MDL = 10 log10(lambda_max / lambda_min) over the top min(rows, cols) eigenvalues of the Gram matrix
+    (the squared singular values; holopipe/analysis.py:158-162 takes an SVD of the matrix itself)."""
+    ev = np.linalg.eigvalsh(np.asarray(gram, np.complex128))
+    top = ev[-nd:]
+    lo, hi = float(top.min()), float(top.max())
+    return 10.0 * math.log10(hi / lo) if lo > 0 else C.METRIC_UNSET
+
+
+def finish_metrics(row_power, diag_power, group_power, gram, rows, cols, have_labels=True, defer_mdl=False):
     """Nine metrics from fp64 partials of one transfer matrix (analysis.py:143-188).
 
     row_power/diag_power/group_power are per virtual row (diag entries < 0 mark
@@ -87,23 +117,19 @@ def finish_metrics(row_power, diag_power, group_power, gram, rows, cols, have_la
     rowd = row_power[has][:nd]
     total = float(row_power.sum())
     v[C.METRIC_IL] = _db(float(row_power.mean()))
-    if total > 0 and gram is not None:
-        ev = np.linalg.eigvalsh(np.asarray(gram, np.complex128))
-        top = ev[-nd:]
-        lo, hi = float(top.min()), float(top.max())
-        if lo > 0:
-            v[C.METRIC_MDL] = 10.0 * math.log10(hi / lo)
+    if total > 0 and gram is not None and not defer_mdl:
+        v[C.METRIC_MDL] = mdl_db(gram, nd)
     dt = float(d.sum())
     v[C.METRIC_DIAG] = _db(dt / nd)
     v[C.METRIC_SNRAVG] = _snr(dt, total - dt)
-    with np.errstate(divide="ignore"):
-        ddb = np.where(d > 0, 10.0 * np.log10(np.maximum(d, 1e-300)), _NEG)
+    pos = d > 0
+    ddb = np.where(pos, 10.0 * np.log10(np.maximum(d, 1e-300)), _NEG)   # no zero reaches log10
     v[C.METRIC_DIAGBEST] = float(ddb.max())
     v[C.METRIC_DIAGWORST] = float(ddb.min())
     noise = rowd - d
-    with np.errstate(divide="ignore", invalid="ignore"):
-        snr = np.minimum(10.0 * np.log10(d / np.where(noise > 0, noise, 1.0)), SNR_CAP_DB)
-    snr = np.where(d <= 0, _NEG, np.where(noise <= 0, SNR_CAP_DB, snr))   # _snr per row, vectorised
+    npos = noise > 0
+    snr = np.minimum(10.0 * np.log10(np.maximum(d, 1e-300) / np.where(npos, noise, 1.0)), SNR_CAP_DB)
+    snr = np.where(pos, np.where(npos, snr, SNR_CAP_DB), _NEG)   # _snr per row, vectorised
     v[C.METRIC_SNRBEST] = float(snr.max())
     v[C.METRIC_SNRWORST] = float(snr.min())
     if have_labels:
@@ -137,6 +163,10 @@ def average_slot(per_wl):
     L = per_wl.shape[1]
     rep = MetricsReport(L)
     rep.values[:, :L] = per_wl.astype(np.float32)
+    if L == 1:   # the average of one valid value is the value
+        ok = per_wl[:, 0] > C.METRIC_UNSET / 2
+        rep.values[ok, 1] = per_wl[ok, 0].astype(np.float32)
+        return rep
     for m in range(C.METRIC_COUNT):
         ok = per_wl[m][per_wl[m] > C.METRIC_UNSET / 2]
         if ok.size:

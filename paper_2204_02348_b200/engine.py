@@ -22,6 +22,7 @@ There is no CPU path: every numeric product comes from libholo_b200.so.
 from __future__ import annotations
 
 import collections
+import math
 import ctypes
 
 import numpy as np
@@ -116,7 +117,7 @@ class Engine:
     def _buf(self, name, shape, dtype):
         torch = _torch()
         t = self._bufs.get(name)
-        n = int(np.prod(shape))
+        n = math.prod(shape)
         if t is None or t.numel() < n or t.dtype != dtype:
             t = torch.empty(max(n, 1), dtype=dtype, device=self.device)
             self._bufs[name] = t
@@ -323,8 +324,11 @@ class Engine:
         else:
             b.frame_count = frames.numel() // (self._st0["W"] * self._st0["H"])
 
-    def process_ifft(self):
-        """Stage 1: carrier bins, window, IFFT grid (engine.py:170-220)."""
+    def process_ifft(self, _next_plan=False):
+        """Stage 1: carrier bins, window, IFFT grid (engine.py:170-220).
+
+        ``_next_plan`` (run_pipeline): take the stage-1 products from the plan the fused launch that
+        follows will use (same k0, window and axes), so a restart builds one plan instead of two."""
         if self._st0 is None:
             raise HoloError(ErrorCode.NULLPOINTER, "FFT stage has not run")
         cfg = self.config
@@ -337,7 +341,14 @@ class Engine:
         self._field_r = self._field_i = self._field_scale = None
         self._summary_field = None
         self._coefs = None
-        plan = self._native_plan(self._plan_key(0, (1.0, 1.0)))
+        if _next_plan:
+            self._st2 = self._stage2_snapshot()
+            G = max(cfg.basisGroupCount, 0)
+            key = self._plan_key(G, self._effective()[2]) if G >= 1 else self._plan_key(0, (1.0, 1.0))
+            self._st2 = None
+        else:
+            key = self._plan_key(0, (1.0, 1.0))
+        plan = self._native_plan(key)
         self._field_axes = plan.axes()
         k0 = np.zeros((self._plan["batch"], self._st0["P"], 2), np.int64)
         for q in range(self._st0["P"]):
@@ -589,7 +600,7 @@ class Engine:
         if from_stage <= 0 or self._st0 is None:
             self.process_fft()
         if from_stage <= 1 or self._st1 is None:
-            self.process_ifft()
+            self.process_ifft(_next_plan=True)
         if from_stage <= 2 or self._field_r is None:
             self._st2 = self._stage2_snapshot()
             self._summary_field = None
@@ -902,15 +913,17 @@ class Engine:
         L = len(plan["lambdas"])
         wl = plan["wl_of_batch"]
         per = np.full((C.METRIC_COUNT, L), C.METRIC_UNSET)
+        pending = []
         for w in range(L):
             rows = np.nonzero(wl == w)[0]
             if rows.size == 0:
                 continue
-            per[:, w] = self._metrics_rows(rows)
+            per[:, w] = self._metrics_rows(rows, pending, w)
         self._metrics = average_slot(per)
+        self._metrics.defer_mdl(pending)
         return ErrorCode.SUCCESS
 
-    def _metrics_rows(self, rows):
+    def _metrics_rows(self, rows, pending=None, slot=0):
         torch = _torch()
         cfg = self.config
         P, M = self._st0["P"], self._mode_count
@@ -965,7 +978,11 @@ class Engine:
                          "hpg_metric_partials")
         host = packed.cpu().numpy()
         gram = host[r3:].view(np.complex128).reshape(n, n)
-        return finish_metrics(host[:R], host[R:2 * R], host[2 * R:3 * R], gram, R, cols, True)
+        v = finish_metrics(host[:R], host[R:2 * R], host[2 * R:3 * R], gram, R, cols, True,
+                           defer_mdl=pending is not None)
+        if pending is not None and host[:R].sum() > 0:
+            pending.append((slot, gram.copy(), min(R, cols)))
+        return v
 
     def metric(self, metric_idx):
         if self._metrics is None:
