@@ -441,17 +441,24 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
       const int kx = g.k0[q][w][0], ky = g.k0[q][w][1];
       const double lam = d->wavelengths[w];
       float2* T = &wtab[((size_t)q * g.L + w) * whw];
+      // the recentring phase is separable: one cos / sin per column and per row (same fp64 values)
+      std::vector<double> cxr(g.ww), cxi(g.ww);
+      for (int c = 0; c < g.ww; ++c) {
+        const double tx = (double)(kx + c - g.ww / 2);
+        const double ax = 2.0 * kPi * tx * (xi[q][0] - g.nx / 2.0) / g.nx;
+        cxr[c] = std::cos(ax);
+        cxi[c] = std::sin(ax);
+      }
       for (int r = 0; r < g.wh; ++r) {
         const double dfy = (double)(r - g.wh / 2) / (g.ny * p);
         const double ty = (double)(ky + r - g.wh / 2);
         const double ay = 2.0 * kPi * ty * (xi[q][1] - g.ny / 2.0) / g.ny;
+        const double pyr = std::cos(ay), pyi = std::sin(ay);
         for (int c = 0; c < g.ww; ++c) {
           const double dfx = (double)(c - g.ww / 2) / (g.nx * p);
           const bool in = dfy * dfy + dfx * dfx <= fr * fr + 1e-30;
-          const double tx = (double)(kx + c - g.ww / 2);
-          const double ax = 2.0 * kPi * tx * (xi[q][0] - g.nx / 2.0) / g.nx;
           // product of the two separable phases in complex128 (pipeline.py:125-127)
-          const double pxr = std::cos(ax), pxi = std::sin(ax), pyr = std::cos(ay), pyi = std::sin(ay);
+          const double pxr = cxr[c], pxi = cxi[c];
           const double re = pyr * pxr - pyi * pxi;
           const double im = pyr * pxi + pyi * pxr;
           // complex64 cast, then the mask (bool * c64)

@@ -16,4 +16,4 @@ def run():
 run()
 print("plain", run())
 pr = cProfile.Profile(); pr.enable(); run(); pr.disable()
-pstats.Stats(pr).sort_stats('cumulative').print_stats(45)
+pstats.Stats(pr).sort_stats("tottime").print_stats(30)
