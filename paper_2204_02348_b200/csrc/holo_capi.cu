@@ -619,6 +619,21 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.tco_img = tco_ok ? reinterpret_cast<const uint4*>(base + o_timg) : nullptr;
   P->ft.tco_inv = reinterpret_cast<const float*>(base + o_tinv);
   P->ft.tco_gp = tco_ok ? GP16 : 0;
+  // HG parity on the symmetric part of the field axes (pipeline.py:152-160 puts the origin at index w / 2),
+  // verified bit for bit on the quantised profiles: the fast kernel then folds each +-d pair of the overlap
+  P->ft.hsym = 0;
+  for (int q = 0; q < g.P && G > 0; ++q) {
+    for (int ax = 0; ax < 2; ++ax) {
+      const int n = ax == 0 ? g.gw : g.gh;
+      const float* h = ax == 0 ? &P->hx[(size_t)q * G * n] : &P->hy[(size_t)q * G * n];
+      const int c = n / 2;
+      bool sym = true;
+      for (int m = 0; m < G && sym; ++m)
+        for (int dd = 1; c + dd < n && sym; ++dd)
+          sym = h[(size_t)m * n + c - dd] == ((m & 1) ? -h[(size_t)m * n + c + dd] : h[(size_t)m * n + c + dd]);
+      if (sym) P->ft.hsym |= 1 << (2 * q + ax);
+    }
+  }
   const double t_copy = g_plan_timing ? now_us() : 0.0;
   e = set_smem_limits();
   if (g_plan_timing)

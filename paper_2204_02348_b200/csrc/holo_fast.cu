@@ -467,18 +467,45 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __
       }
       __syncthreads();
       const int GQ = GP >> 2;
+      // HG parity (ft.hsym, checked on the quantised profiles at plan time): h_m(c - d) = (-1)^m h_m(c + d)
+      // around the axis origin c = W / 2, so each +-d pair of samples enters as F(c + d) +- F(c - d)
+      constexpr int CX = WW / 2, NPX = WW - 1 - CX, CY = WH / 2, NPY = WH - 1 - CY;
+      const bool xsym = (ft.hsym >> (2 * q)) & 1, ysym = (ft.hsym >> (2 * q + 1)) & 1;
       for (int idx = tid; idx < WH * GQ; idx += blockDim.x) {
         const int y = idx / GQ, mq = idx - y * GQ;
         const float2* row = F + y * WW;
         float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
+        if (xsym) {   // 4 mq is even: orders 4mq, 4mq + 2 take the sums, 4mq + 1, 4mq + 3 the differences
+#pragma unroll 5
+          for (int dd = 1; dd <= NPX; ++dd) {
+            const float2 vp = row[CX + dd], vm = row[CX - dd];
+            const float2 sv = make_float2(vp.x + vm.x, vp.y + vm.y), dv = make_float2(vp.x - vm.x, vp.y - vm.y);
+            const float4 h = *reinterpret_cast<const float4*>(&hxT[(CX + dd) * GP + 4 * mq]);
+            ar.x = fmaf(sv.x, h.x, ar.x); ai.x = fmaf(sv.y, h.x, ai.x);
+            ar.y = fmaf(dv.x, h.y, ar.y); ai.y = fmaf(dv.y, h.y, ai.y);
+            ar.z = fmaf(sv.x, h.z, ar.z); ai.z = fmaf(sv.y, h.z, ai.z);
+            ar.w = fmaf(dv.x, h.w, ar.w); ai.w = fmaf(dv.y, h.w, ai.w);
+          }
+#pragma unroll
+          for (int k = 0; k < 1 + (CX - NPX); ++k) {   // the origin, and x = 0 when W is even
+            const int x = k == 0 ? CX : 0;
+            const float2 v = row[x];
+            const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+            ar.x = fmaf(v.x, h.x, ar.x); ai.x = fmaf(v.y, h.x, ai.x);
+            ar.y = fmaf(v.x, h.y, ar.y); ai.y = fmaf(v.y, h.y, ai.y);
+            ar.z = fmaf(v.x, h.z, ar.z); ai.z = fmaf(v.y, h.z, ai.z);
+            ar.w = fmaf(v.x, h.w, ar.w); ai.w = fmaf(v.y, h.w, ai.w);
+          }
+        } else {
 #pragma unroll 6
-        for (int x = 0; x < WW; ++x) {
-          const float2 v = row[x];
-          const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
-          ar.x = fmaf(v.x, h.x, ar.x); ai.x = fmaf(v.y, h.x, ai.x);
-          ar.y = fmaf(v.x, h.y, ar.y); ai.y = fmaf(v.y, h.y, ai.y);
-          ar.z = fmaf(v.x, h.z, ar.z); ai.z = fmaf(v.y, h.z, ai.z);
-          ar.w = fmaf(v.x, h.w, ar.w); ai.w = fmaf(v.y, h.w, ai.w);
+          for (int x = 0; x < WW; ++x) {
+            const float2 v = row[x];
+            const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+            ar.x = fmaf(v.x, h.x, ar.x); ai.x = fmaf(v.y, h.x, ai.x);
+            ar.y = fmaf(v.x, h.y, ar.y); ai.y = fmaf(v.y, h.y, ai.y);
+            ar.z = fmaf(v.x, h.z, ar.z); ai.z = fmaf(v.y, h.z, ai.z);
+            ar.w = fmaf(v.x, h.w, ar.w); ai.w = fmaf(v.y, h.w, ai.w);
+          }
         }
         float2* u = U + y * GP + 4 * mq;
         u[0] = make_float2(ar.x, ai.x);
@@ -489,17 +516,41 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __
       __syncthreads();
       const float d = __fdiv_rn(g.dxdy[q], scale);
       float2* out = p.coefs + (size_t)item * g.M;
-      for (int i = tid; i < g.M; i += blockDim.x) {
-        const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+      // two lanes per coefficient (adjacent lanes split the y pairs), combined with one shuffle
+      for (int t0 = 0; t0 < 2 * g.M; t0 += blockDim.x) {
+        const int tt = t0 + tid, i = tt >> 1, half = tt & 1;
         float ax = 0.f, ay = 0.f;
-#pragma unroll 6
-        for (int y = 0; y < WH; ++y) {
-          const float2 v = U[y * GP + m];
-          const float hv = hyT[y * GP + n];
-          ax = fmaf(v.x, hv, ax);
-          ay = fmaf(v.y, hv, ay);
+        if (i < g.M) {
+          const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+          if (ysym) {
+            const float sg = (n & 1) ? -1.f : 1.f;
+#pragma unroll 5
+            for (int dd = 1 + half; dd <= NPY; dd += 2) {
+              const float2 vp = U[(CY + dd) * GP + m], vm = U[(CY - dd) * GP + m];
+              const float hv = hyT[(CY + dd) * GP + n];
+              ax = fmaf(fmaf(sg, vm.x, vp.x), hv, ax);
+              ay = fmaf(fmaf(sg, vm.y, vp.y), hv, ay);
+            }
+            if (half == 0 || CY > NPY) {   // the origin (lane 0) and y = 0 when H is even (lane 1)
+              const int y = half == 0 ? CY : 0;
+              const float2 v = U[y * GP + m];
+              const float hv = hyT[y * GP + n];
+              ax = fmaf(v.x, hv, ax);
+              ay = fmaf(v.y, hv, ay);
+            }
+          } else {
+#pragma unroll 7
+            for (int y = half; y < WH; y += 2) {
+              const float2 v = U[y * GP + m];
+              const float hv = hyT[y * GP + n];
+              ax = fmaf(v.x, hv, ax);
+              ay = fmaf(v.y, hv, ay);
+            }
+          }
         }
-        out[i] = make_float2(ax * d, ay * d);
+        ax += __shfl_xor_sync(0xffffffffu, ax, 1);
+        ay += __shfl_xor_sync(0xffffffffu, ay, 1);
+        if (i < g.M && half == 0) out[i] = make_float2(ax * d, ay * d);
       }
     }
   }
