@@ -1,3 +1,4 @@
+"""cProfile of api-level AutoAlign (config 4 start, device-resident frames): where the host time goes."""
 import cProfile, pstats, sys, copy, time
 sys.path.insert(0,'.')
 import numpy as np, torch
