@@ -648,6 +648,7 @@ class Engine:
         dev = self.device
         lib = native.lib()
         bounds = np.linspace(0, B, self._PIPE_CHUNKS + 1).astype(int)
+        arrived = []   # (r0, r1, event): coefficient rows of a chunk are in host_out
         with torch.cuda.device(dev):
             comp = torch.cuda.current_stream(dev)
             copy, back = self._bufs.get("copy_stream"), self._bufs.get("back_stream")
@@ -702,6 +703,9 @@ class Engine:
                 back.wait_event(done)   # readback on its own stream: uploads keep streaming
                 with torch.cuda.stream(back):
                     host_out[r0 * P * M:r1 * P * M].copy_(L.coefs.view(-1)[r0 * P * M:r1 * P * M], non_blocking=True)
+                got = torch.cuda.Event()
+                got.record(back)
+                arrived.append((r0, r1, got))
             fin = torch.cuda.Event()
             fin.record(back)
             comp.wait_stream(copy)
@@ -711,10 +715,15 @@ class Engine:
         self._field_axes = L.plan.axes()
         self._st3 = {"G": L.G, "waist": tuple(L.waist)}
         self._finish_coefs(L.coefs, M, P)
+        # copy-out (engine.py:416) chunk by chunk as each readback lands, while later chunks still stream
+        staged = host_out[:B * P * M].numpy().reshape(B, P * M)
+        coefs = np.empty((B, P * M), np.complex64)
+        for r0, r1, got in arrived:
+            got.synchronize()
+            coefs[r0:r1] = staged[r0:r1]
         fin.synchronize()
-        coefs = host_out[:B * P * M].numpy().reshape(B, P * M)
         perm = self.output_permutation()
-        return (coefs.copy() if perm is None else coefs[perm]), B, self._mode_count, P
+        return (coefs if perm is None else coefs[perm]), B, self._mode_count, P
 
     def coef_view(self):
         plan = self._plan
