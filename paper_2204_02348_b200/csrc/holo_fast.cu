@@ -606,9 +606,9 @@ static cudaError_t launch_fast_nt(const RunParams& p, const FastTables& ft, int 
 
 cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
   // fewer windows than SMs: nothing to overlap across CTAs, so give each window the whole SM
-  const char* e = getenv("HOLO_FAST_NT");
+  static const int forced_nt = getenv("HOLO_FAST_NT") ? atoi(getenv("HOLO_FAST_NT")) : 0;   // diagnostic override
   const int items = p.B * p.g.P;
-  const bool wide = e ? atoi(e) == 512 : items <= num_sms;
+  const bool wide = forced_nt ? forced_nt == 512 : items <= num_sms;
   return wide ? launch_fast_nt<512>(p, ft, num_sms, s) : launch_fast_nt<256>(p, ft, num_sms, s);
 }
 
