@@ -102,6 +102,7 @@ class Engine:
         self._deferred = None           # host upload postponed by the pipelined process_batch
         self._plans = collections.OrderedDict()
         self._bufs = {}
+        self._views = {}
         self._clear_products()
 
     # ------------------------------------------------------------ plumbing
@@ -115,13 +116,21 @@ class Engine:
         return self._device
 
     def _buf(self, name, shape, dtype):
+        """Device scratch `name` viewed as `shape` (grown on demand; views cached per shape)."""
+        views = self._views.setdefault(name, {})
+        v = views.get((shape, dtype))
+        if v is not None:
+            return v
         torch = _torch()
         t = self._bufs.get(name)
         n = math.prod(shape)
         if t is None or t.numel() < n or t.dtype != dtype:
             t = torch.empty(max(n, 1), dtype=dtype, device=self.device)
             self._bufs[name] = t
-        return t[:n].view(*shape) if shape else t[:1]
+            views.clear()   # views of the previous allocation
+        v = t[:n].view(*shape) if shape else t[:1]
+        views[(shape, dtype)] = v
+        return v
 
     def _clear_products(self):
         self._st0 = None

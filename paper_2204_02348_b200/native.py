@@ -175,11 +175,13 @@ class Plan:
 
     def axes(self):
         import numpy as np
-        x = np.empty(self.gw, np.float32)
-        y = np.empty(self.gh, np.float32)
-        check(self._lib.hpg_plan_get_axes(self.handle, x.ctypes.data_as(c_void_p),
-                                          y.ctypes.data_as(c_void_p)))
-        return x, y
+        if getattr(self, "_axes", None) is None:   # constant per plan: read once, hand out copies
+            x = np.empty(self.gw, np.float32)
+            y = np.empty(self.gh, np.float32)
+            check(self._lib.hpg_plan_get_axes(self.handle, x.ctypes.data_as(c_void_p),
+                                              y.ctypes.data_as(c_void_p)))
+            self._axes = (x, y)
+        return self._axes[0].copy(), self._axes[1].copy()
 
     def basis(self, pol_count, group_count):
         import numpy as np
