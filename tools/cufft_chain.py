@@ -32,9 +32,9 @@ def tables(eng, cfg):
     fr = math.sin(math.radians(cfg["fourierWindowRadius"])) / lam
     xa, ya = plan.axes()
     G = cfg["basisGroupCount"]
-    hx, hy = plan.basis(P, G)
+    hx, hy = plan.basis(P, G) if G > 0 else (np.zeros((P, 0, info.gw)), np.zeros((P, 0, info.gh)))
     dev = torch.device("cuda", 0)
-    T = {"origins": [], "rows": [], "cols": [], "conj": [], "win": [], "rem": [], "wh": wh, "ww": ww,
+    T = {"origins": [], "rows": [], "cols": [], "conj": [], "win": [], "rem": [], "wh": wh, "ww": ww, "G": G,
          "hx": torch.as_tensor(hx, dtype=torch.complex64, device=dev),
          "hy": torch.as_tensor(hy, dtype=torch.complex64, device=dev)}
     fx = (np.arange(ww) - ww // 2) / (nx * p)
@@ -88,9 +88,12 @@ def chain(frames, T, nx, ny):
         scale = torch.where(peak > 0, (32767.0 / peak.double()).float(), torch.ones_like(peak))
         fr = torch.round(field.real * scale[:, None, None]).to(torch.int16)
         fi = torch.round(field.imag * scale[:, None, None]).to(torch.int16)
-        deq = torch.complex(fr.float(), fi.float()) / scale[:, None, None]
-        t = torch.matmul(torch.matmul(T["hy"][q], deq), T["hx"][q].transpose(0, 1)) * T["dxdy"]   # (B, G, G)
-        coefs = t[:, T["ni"], T["mi"]]
+        if T["G"] > 0:
+            deq = torch.complex(fr.float(), fi.float()) / scale[:, None, None]
+            t = torch.matmul(torch.matmul(T["hy"][q], deq), T["hx"][q].transpose(0, 1)) * T["dxdy"]   # (B, G, G)
+            coefs = t[:, T["ni"], T["mi"]]
+        else:
+            coefs = fr.new_zeros((fr.shape[0], 0), dtype=torch.complex64)
         outs.append((fr, fi, scale, coefs))
     fr = torch.stack([o[0] for o in outs], 1)
     fi = torch.stack([o[1] for o in outs], 1)
@@ -135,12 +138,13 @@ def main():
     nx, ny = cfg["fftWindowSizeX"], cfg["fftWindowSizeY"]
     lib = chain(frames, T, nx, ny)
     fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
-    co = eng.coefs_device().cpu().numpy()
+    co = eng.coefs_device().cpu().numpy() if T["G"] > 0 else None
     lfr, lfi, lsc, lco = (t.cpu().numpy() for t in lib)
     dq = lambda r, i, s: (r.astype(np.float32) + 1j * i.astype(np.float32)) / s[..., None, None]   # noqa: E731
-    a, b = dq(fr, fi, sc).reshape(B * T["hx"].shape[0], -1), dq(lfr, lfi, lsc).reshape(B * T["hx"].shape[0], -1)
+    P = len(T["origins"])
+    a, b = dq(fr, fi, sc).reshape(B * P, -1), dq(lfr, lfi, lsc).reshape(B * P, -1)
     field_err = float(np.max(np.linalg.norm(a - b, axis=1) / np.linalg.norm(b, axis=1)))
-    coef_err = float(np.max(np.linalg.norm(co - lco, axis=1) / np.linalg.norm(lco, axis=1)))
+    coef_err = float(np.max(np.linalg.norm(co - lco, axis=1) / np.linalg.norm(lco, axis=1))) if co is not None else None
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     launch = eng.prepare_launch()
     t_fused = timed(lambda: launch.launch(), args.steps, args.warmup, flush)
