@@ -34,6 +34,7 @@ size_t tc2_workspace(int64_t items);
 bool lw_supported(const Geometry& g, int A, const void* members, unsigned flags, const void* windows);
 size_t lw_workspace(const Geometry& g, int64_t items);
 int64_t lw_chunk(const Geometry& g);
+int64_t lw_slot_items(const Geometry& g, int64_t items);
 int64_t tc2_chunk();
 cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s);
 cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s);
@@ -812,7 +813,8 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
       return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
     e = launch_lw(rp, P->num_sms, static_cast<cudaStream_t>(stream));
     const int per_chunk = (rp.g.nx == 512 && rp.g.ny == 512) ? 5 : 4;   // rows, cols, [ifft_y,] field, pack
-    g_last_launches = per_chunk * (int)((items + lw_chunk(rp.g) - 1) / lw_chunk(rp.g)) +
+    const int64_t slot = lw_slot_items(rp.g, items);
+    g_last_launches = per_chunk * (int)((items + slot - 1) / slot) +
                       ((rp.coefs && rp.g.G > 0) ? 1 : 0);
   } else {
     e = launch_fused(rp, static_cast<cudaStream_t>(stream));

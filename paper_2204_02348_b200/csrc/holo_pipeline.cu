@@ -981,23 +981,27 @@ int64_t lw_chunk(const Geometry& g) {   // items per chunk: R + T + F of a chunk
   return std::max<int64_t>(1, (80ll << 20) / per);
 }
 
-size_t lw_workspace(const Geometry& g, int64_t items) {
-  const int64_t n = std::min<int64_t>(items, lw_chunk(g));
-  return (size_t)n * ((size_t)g.ww * g.ny * 8 + 2 * (size_t)g.gh * g.gw * 8 + 16) + 1024;
+// Two slots of half an L2 chunk each, processed on two internal streams so that one slot's kernels fill the
+// tail waves of the other's.
+int64_t lw_slot_items(const Geometry& g, int64_t items) {
+  const int64_t half = std::max<int64_t>(1, (lw_chunk(g) + 1) / 2);
+  return std::max<int64_t>(1, std::min<int64_t>(items, half));
 }
+static size_t lw_slot_bytes(const Geometry& g, int64_t items) {
+  const size_t b = (size_t)lw_slot_items(g, items) * ((size_t)g.ww * g.ny * 8 + 2 * (size_t)g.gh * g.gw * 8 + 16);
+  return (b + 255) & ~size_t(255);
+}
+
+size_t lw_workspace(const Geometry& g, int64_t items) { return 2 * lw_slot_bytes(g, items) + 1024; }
 
 cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s);
 
 cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
   const Geometry& g = p.g;
   const int items = p.B * g.P;
-  const int64_t chunk = lw_chunk(g);
-  const int64_t n0 = std::min<int64_t>(items, chunk);
-  char* ws = p.work;
-  float2* R = reinterpret_cast<float2*>(ws);
-  float2* T = R + (size_t)n0 * g.ww * g.ny;
-  float2* F = T + (size_t)n0 * g.gh * g.gw;
-  unsigned* peak = reinterpret_cast<unsigned*>(F + (size_t)n0 * g.gh * g.gw);
+  const int64_t chunk = lw_slot_items(g, items);
+  const int64_t n0 = chunk;
+  const size_t slot_bytes = lw_slot_bytes(g, items);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(lw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -1013,31 +1017,63 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
   const int rows_smem = 2 * kLwRows * g.nx * (int)sizeof(float2);
   const int cols_smem = 2 * kLwCols * g.ny * (int)sizeof(float2);
   const int field_smem = (2 * g.gw + 160) * kLwFRows * (int)sizeof(float2);
-  for (int i0 = 0; i0 < items; i0 += (int)chunk) {
+  // fork onto two internal streams (one per workspace slot) and join back onto s: stream-ordered for the caller
+  static cudaStream_t lanes[2] = {nullptr, nullptr};
+  static cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+  static int lanes_dev = -1;
+  const bool two = items > chunk;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (two && lanes_dev != dev) {
+    for (int k = 0; k < 2; ++k) {
+      cudaStreamCreateWithFlags(&lanes[k], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&join_ev[k], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+    lanes_dev = dev;
+  }
+  if (two) {
+    cudaEventRecord(fork_ev, s);
+    cudaStreamWaitEvent(lanes[0], fork_ev, 0);
+    cudaStreamWaitEvent(lanes[1], fork_ev, 0);
+  }
+  int slot = 0;
+  for (int i0 = 0; i0 < items; i0 += (int)chunk, slot ^= 1) {
     const int i1 = (int)std::min<int64_t>(items, i0 + chunk);
     const int n = i1 - i0;
-    cudaMemsetAsync(peak, 0, (size_t)n * sizeof(unsigned), s);
+    cudaStream_t s_ = two ? lanes[slot] : s;
+    float2* R = reinterpret_cast<float2*>(p.work + slot * slot_bytes);
+    float2* T = R + (size_t)n0 * g.ww * g.ny;
+    float2* F = T + (size_t)n0 * g.gh * g.gw;
+    unsigned* peak = reinterpret_cast<unsigned*>(F + (size_t)n0 * g.gh * g.gw);
+    cudaMemsetAsync(peak, 0, (size_t)n * sizeof(unsigned), s_);
     if (g.nx == 512 && g.ny == 512) {
       const int f512 = 8 * kF512Group * (int)sizeof(float2);
-      lw_rows512_kernel<<<n * (g.ny / 2 / 8), 512, f512, s>>>(p, i0, i1, R);
-      lw_cols512_kernel<<<n * ((g.ww + 7) / 8), 512, f512, s>>>(p, i0, i1, R, F);   // cropped window -> F (scratch)
+      lw_rows512_kernel<<<n * (g.ny / 2 / 8), 512, f512, s_>>>(p, i0, i1, R);
+      lw_cols512_kernel<<<n * ((g.ww + 7) / 8), 512, f512, s_>>>(p, i0, i1, R, F);   // cropped window -> F (scratch)
       const int ys = (2 * g.gh + 160) * kLwIfft * (int)sizeof(float2);
       if (g.gh == 164)
-        lw_ifft_y_kernel<true><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s>>>(p, i0, i1, F, T);
+        lw_ifft_y_kernel<true><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s_>>>(p, i0, i1, F, T);
       else
-        lw_ifft_y_kernel<false><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s>>>(p, i0, i1, F, T);
+        lw_ifft_y_kernel<false><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s_>>>(p, i0, i1, F, T);
     } else {
-      lw_rows_kernel<<<n * ((g.ny / 2 + kLwRows - 1) / kLwRows), kThreads, rows_smem, s>>>(p, i0, i1, R);
-      lw_cols_kernel<<<n * ((g.ww + kLwCols - 1) / kLwCols), kThreads, cols_smem, s>>>(p, i0, i1, R, T);
+      lw_rows_kernel<<<n * ((g.ny / 2 + kLwRows - 1) / kLwRows), kThreads, rows_smem, s_>>>(p, i0, i1, R);
+      lw_cols_kernel<<<n * ((g.ww + kLwCols - 1) / kLwCols), kThreads, cols_smem, s_>>>(p, i0, i1, R, T);
     }
     if (g.gw == 164)
-      lw_field_kernel<true><<<n * ((g.gh + kLwFRows - 1) / kLwFRows), kThreads, field_smem, s>>>(p, i0, i1, T, F, peak);
+      lw_field_kernel<true><<<n * ((g.gh + kLwFRows - 1) / kLwFRows), kThreads, field_smem, s_>>>(p, i0, i1, T, F, peak);
     else
-      lw_field_kernel<false><<<n * ((g.gh + kLwFRows - 1) / kLwFRows), kThreads, field_smem, s>>>(p, i0, i1, T, F, peak);
+      lw_field_kernel<false><<<n * ((g.gh + kLwFRows - 1) / kLwFRows), kThreads, field_smem, s_>>>(p, i0, i1, T, F, peak);
     const int per = (g.gh * g.gw + 2 * kThreads - 1) / (2 * kThreads);
-    lw_pack_kernel<<<n * per, kThreads, 0, s>>>(p, i0, i1, F, peak);
+    lw_pack_kernel<<<n * per, kThreads, 0, s_>>>(p, i0, i1, F, peak);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+  }
+  if (two) {
+    for (int k = 0; k < 2; ++k) {
+      cudaEventRecord(join_ev[k], lanes[k]);
+      cudaStreamWaitEvent(s, join_ev[k], 0);
+    }
   }
   if (p.coefs && g.G > 0) {
     const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms * 4);
