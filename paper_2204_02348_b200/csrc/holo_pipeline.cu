@@ -981,10 +981,11 @@ int64_t lw_chunk(const Geometry& g) {   // items per chunk: R + T + F of a chunk
   return std::max<int64_t>(1, (80ll << 20) / per);
 }
 
-// Two slots of half an L2 chunk each, processed on two internal streams so that one slot's kernels fill the
-// tail waves of the other's.
+// kLwLanes slots of 1/kLwLanes of an L2 chunk each, processed on as many internal streams so that one slot's
+// kernels fill the tail waves of the others'.
+constexpr int kLwLanes = 3;
 int64_t lw_slot_items(const Geometry& g, int64_t items) {
-  const int64_t half = std::max<int64_t>(1, (lw_chunk(g) + 1) / 2);
+  const int64_t half = std::max<int64_t>(1, (lw_chunk(g) + kLwLanes - 1) / kLwLanes);
   return std::max<int64_t>(1, std::min<int64_t>(items, half));
 }
 static size_t lw_slot_bytes(const Geometry& g, int64_t items) {
@@ -992,7 +993,7 @@ static size_t lw_slot_bytes(const Geometry& g, int64_t items) {
   return (b + 255) & ~size_t(255);
 }
 
-size_t lw_workspace(const Geometry& g, int64_t items) { return 2 * lw_slot_bytes(g, items) + 1024; }
+size_t lw_workspace(const Geometry& g, int64_t items) { return kLwLanes * lw_slot_bytes(g, items) + 1024; }
 
 cudaError_t launch_coefs(const RunParams& p, int grid, cudaStream_t s);
 
@@ -1018,14 +1019,14 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
   const int cols_smem = 2 * kLwCols * g.ny * (int)sizeof(float2);
   const int field_smem = (2 * g.gw + 160) * kLwFRows * (int)sizeof(float2);
   // fork onto two internal streams (one per workspace slot) and join back onto s: stream-ordered for the caller
-  static cudaStream_t lanes[2] = {nullptr, nullptr};
-  static cudaEvent_t fork_ev = nullptr, join_ev[2] = {nullptr, nullptr};
+  static cudaStream_t lanes[kLwLanes] = {};
+  static cudaEvent_t fork_ev = nullptr, join_ev[kLwLanes] = {};
   static int lanes_dev = -1;
   const bool two = items > chunk;
   int dev = 0;
   cudaGetDevice(&dev);
   if (two && lanes_dev != dev) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kLwLanes; ++k) {
       cudaStreamCreateWithFlags(&lanes[k], cudaStreamNonBlocking);
       cudaEventCreateWithFlags(&join_ev[k], cudaEventDisableTiming);
     }
@@ -1034,11 +1035,10 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
   }
   if (two) {
     cudaEventRecord(fork_ev, s);
-    cudaStreamWaitEvent(lanes[0], fork_ev, 0);
-    cudaStreamWaitEvent(lanes[1], fork_ev, 0);
+    for (int k = 0; k < kLwLanes; ++k) cudaStreamWaitEvent(lanes[k], fork_ev, 0);
   }
   int slot = 0;
-  for (int i0 = 0; i0 < items; i0 += (int)chunk, slot ^= 1) {
+  for (int i0 = 0; i0 < items; i0 += (int)chunk, slot = (slot + 1) % kLwLanes) {
     const int i1 = (int)std::min<int64_t>(items, i0 + chunk);
     const int n = i1 - i0;
     cudaStream_t s_ = two ? lanes[slot] : s;
@@ -1070,7 +1070,7 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   if (two) {
-    for (int k = 0; k < 2; ++k) {
+    for (int k = 0; k < kLwLanes; ++k) {
       cudaEventRecord(join_ev[k], lanes[k]);
       cudaStreamWaitEvent(s, join_ev[k], 0);
     }
