@@ -17,6 +17,7 @@
 //   IFFT       : wh x ww inverse (pipeline.py:130-149), ifftshift folded into
 //                the separable removal phase (pipeline.py:163-185)
 #include <algorithm>
+#include <mutex>
 
 #include "holo_internal.h"
 
@@ -1019,20 +1020,29 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
   const int cols_smem = 2 * kLwCols * g.ny * (int)sizeof(float2);
   const int field_smem = (2 * g.gw + 160) * kLwFRows * (int)sizeof(float2);
   // fork onto two internal streams (one per workspace slot) and join back onto s: stream-ordered for the caller
-  static cudaStream_t lanes[kLwLanes] = {};
-  static cudaEvent_t fork_ev = nullptr, join_ev[kLwLanes] = {};
-  static int lanes_dev = -1;
+  constexpr int kMaxDev = 64;
+  static cudaStream_t lanes_of[kMaxDev][kLwLanes] = {};
+  static cudaEvent_t fork_of[kMaxDev] = {}, join_of[kMaxDev][kLwLanes] = {};
+  static std::mutex lanes_mu;
   const bool two = items > chunk;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (two && lanes_dev != dev) {
-    for (int k = 0; k < kLwLanes; ++k) {
-      cudaStreamCreateWithFlags(&lanes[k], cudaStreamNonBlocking);
-      cudaEventCreateWithFlags(&join_ev[k], cudaEventDisableTiming);
+  if (two && (dev < 0 || dev >= kMaxDev)) return cudaErrorInvalidDevice;
+  // the lanes and events of a device are shared: one launch enqueues fork .. join at a time
+  std::unique_lock<std::mutex> lk(lanes_mu, std::defer_lock);
+  if (two) {
+    lk.lock();
+    if (!fork_of[dev]) {   // created once per device, reused by every later launch
+      for (int k = 0; k < kLwLanes; ++k) {
+        cudaStreamCreateWithFlags(&lanes_of[dev][k], cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&join_of[dev][k], cudaEventDisableTiming);
+      }
+      cudaEventCreateWithFlags(&fork_of[dev], cudaEventDisableTiming);
     }
-    cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
-    lanes_dev = dev;
   }
+  cudaStream_t* lanes = two ? lanes_of[dev] : nullptr;
+  cudaEvent_t fork_ev = two ? fork_of[dev] : nullptr;
+  cudaEvent_t* join_ev = two ? join_of[dev] : nullptr;
   if (two) {
     cudaEventRecord(fork_ev, s);
     for (int k = 0; k < kLwLanes; ++k) cudaStreamWaitEvent(lanes[k], fork_ev, 0);
@@ -1067,13 +1077,21 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
     const int per = (g.gh * g.gw + 2 * kThreads - 1) / (2 * kThreads);
     lw_pack_kernel<<<n * per, kThreads, 0, s_>>>(p, i0, i1, F, peak);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+      if (two)   // still join, so the caller's stream never runs ahead of queued work
+        for (int k = 0; k < kLwLanes; ++k) {
+          cudaEventRecord(join_ev[k], lanes[k]);
+          cudaStreamWaitEvent(s, join_ev[k], 0);
+        }
+      return e;
+    }
   }
   if (two) {
     for (int k = 0; k < kLwLanes; ++k) {
       cudaEventRecord(join_ev[k], lanes[k]);
       cudaStreamWaitEvent(s, join_ev[k], 0);
     }
+    lk.unlock();
   }
   if (p.coefs && g.G > 0) {
     const int grid = (int)std::min<int64_t>(items, (int64_t)num_sms * 4);
