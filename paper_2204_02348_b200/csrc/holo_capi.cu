@@ -812,7 +812,9 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
     if (!o->workspace || o->workspace_bytes < lw_workspace(rp.g, (int64_t)b->batch_count * P->g.P))
       return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
     e = launch_lw(rp, P->num_sms, static_cast<cudaStream_t>(stream));
-    const int per_chunk = (rp.g.nx == 512 && rp.g.ny == 512) ? 5 : 4;   // rows, cols, [ifft_y,] field, pack
+    // rows, cols (+ the 164-point IFFT along y when fused), [ifft_y,] field, pack
+    const bool fused164 = rp.g.gh == 164 && rp.g.wh == 164;
+    const int per_chunk = (rp.g.nx == 512 && rp.g.ny == 512 && !fused164) ? 5 : 4;
     const int64_t slot = lw_slot_items(rp.g, items);
     g_last_launches = per_chunk * (int)((items + slot - 1) / slot) +
                       ((rp.coefs && rp.g.G > 0) ? 1 : 0);

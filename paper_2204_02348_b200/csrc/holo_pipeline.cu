@@ -697,8 +697,12 @@ __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__
   }
 }
 
-// Column pass for 512-high windows: 8 columns per 512-thread CTA; FFT along y (512), crop,
-// window table, then the IFFT along r (generic Stockham) -> T[c][y'].
+HOLO_DEV void ifft164(float2* S0, float2* S1, float2* scr, int count, const float2* __restrict__ tw);
+
+// Column pass for 512-high windows: 8 columns per 512-thread CTA; FFT along y (512), crop, window table
+// -> W[c][r] in T.  FUSE164 (164-row field grids, config 3): the 164-point IFFT along r of the CTA's 8 columns
+// follows in the same CTA (the FFT scratch is reused) and T receives the transformed columns directly.
+template <bool FUSE164>
 __global__ void __launch_bounds__(512) lw_cols512_kernel(const __grid_constant__ RunParams p, int i0, int i1,
                                                           const float2* __restrict__ R, float2* __restrict__ T) {
   extern __shared__ __align__(16) char smem[];
@@ -723,10 +727,35 @@ __global__ void __launch_bounds__(512) lw_cols512_kernel(const __grid_constant__
   const float2* wtab = p.t.win_tab + (size_t)(q * g.L + w) * wh * ww;
   const float2* X0 = reinterpret_cast<const float2*>(smem);
   float2* Wg = T + (size_t)(item - i0) * ww * wh + (size_t)c0 * wh;
-  for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) {
-    const int j = idx / wh, r = idx - j * wh, c = c0 + j;
-    const int ky = pmod(k0y + r - wh / 2, 512);
-    Wg[idx] = cmul(X0[j * kF512Group + f512_pos(ky)], __ldg(&wtab[r * ww + c]));
+  if constexpr (FUSE164) {
+    constexpr int kPer = (164 * 8 + 511) / 512;   // cropped values per thread
+    float2 v[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int idx = threadIdx.x + 512 * u;
+      if (idx < wh * cc) {
+        const int j = idx / wh, r = idx - j * wh, c = c0 + j;
+        const int ky = pmod(k0y + r - wh / 2, 512);
+        v[u] = cmul(X0[j * kF512Group + f512_pos(ky)], __ldg(&wtab[r * ww + c]));
+      }
+    }
+    __syncthreads();   // the FFT scratch is free: S0 | S1 | radix-41 sums
+    float2* S0 = reinterpret_cast<float2*>(smem);
+    float2* S1 = S0 + 8 * 164;
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const int idx = threadIdx.x + 512 * u;
+      if (idx < wh * cc) S0[idx] = v[u];
+    }
+    __syncthreads();
+    ifft164(S0, S1, S1 + 8 * 164, cc, p.t.tw_gh);
+    for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) Wg[idx] = S0[idx];
+  } else {
+    for (int idx = threadIdx.x; idx < wh * cc; idx += blockDim.x) {
+      const int j = idx / wh, r = idx - j * wh, c = c0 + j;
+      const int ky = pmod(k0y + r - wh / 2, 512);
+      Wg[idx] = cmul(X0[j * kF512Group + f512_pos(ky)], __ldg(&wtab[r * ww + c]));
+    }
   }
 }
 
@@ -1011,7 +1040,8 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
     cudaFuncSetAttribute(lw_field_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(lw_field_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(lw_rows512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_cols512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_cols512_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(lw_cols512_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(lw_ifft_y_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(lw_ifft_y_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     configured = true;
@@ -1060,12 +1090,16 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
     if (g.nx == 512 && g.ny == 512) {
       const int f512 = 8 * kF512Group * (int)sizeof(float2);
       lw_rows512_kernel<<<n * (g.ny / 2 / 8), 512, f512, s_>>>(p, i0, i1, R);
-      lw_cols512_kernel<<<n * ((g.ww + 7) / 8), 512, f512, s_>>>(p, i0, i1, R, F);   // cropped window -> F (scratch)
-      const int ys = (2 * g.gh + 160) * kLwIfft * (int)sizeof(float2);
-      if (g.gh == 164)
-        lw_ifft_y_kernel<true><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s_>>>(p, i0, i1, F, T);
-      else
-        lw_ifft_y_kernel<false><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s_>>>(p, i0, i1, F, T);
+      if (g.gh == 164 && g.wh == 164) {   // column FFT, crop and the 164-point IFFT along r in one kernel
+        lw_cols512_kernel<true><<<n * ((g.ww + 7) / 8), 512, f512, s_>>>(p, i0, i1, R, T);
+      } else {
+        lw_cols512_kernel<false><<<n * ((g.ww + 7) / 8), 512, f512, s_>>>(p, i0, i1, R, F);   // window -> F (scratch)
+        const int ys = (2 * g.gh + 160) * kLwIfft * (int)sizeof(float2);
+        if (g.gh == 164)
+          lw_ifft_y_kernel<true><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s_>>>(p, i0, i1, F, T);
+        else
+          lw_ifft_y_kernel<false><<<n * ((g.ww + kLwIfft - 1) / kLwIfft), kThreads, ys, s_>>>(p, i0, i1, F, T);
+      }
     } else {
       lw_rows_kernel<<<n * ((g.ny / 2 + kLwRows - 1) / kLwRows), kThreads, rows_smem, s_>>>(p, i0, i1, R);
       lw_cols_kernel<<<n * ((g.ww + kLwCols - 1) / kLwCols), kThreads, cols_smem, s_>>>(p, i0, i1, R, T);

@@ -96,4 +96,4 @@ def test_launch_count_reported():
     fspec, cfg = bench.config_for("largeframe", batch=4)
     frames = make_frames(FrameSpec(**fspec))
     _run(cfg, torch.from_numpy(frames).cuda(), 4)
-    assert native.lib().hpg_last_launch_count() == 5   # rows, cols, IFFT along y, field, pack
+    assert native.lib().hpg_last_launch_count() == 4   # rows, cols + IFFT along y, field, pack
