@@ -653,14 +653,16 @@ HOLO_DEV void fft512_group(float2 (&a)[8], int t, const float2* __restrict__ tw,
 }
 constexpr int kF512Group = 8 * 72 + 64 * 9;   // float2 of scratch per 512-point group
 
-// Row pass for 512-wide windows: 8 row pairs per 512-thread CTA, one 64-thread group each.
+// Row pass for 512-wide windows: 16 row pairs per 512-thread CTA, two per 64-thread group; both pairs' frame
+// rows are loaded before the first FFT so the second load's latency hides behind it.
+constexpr int kRows512Sets = 2;
 __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__ RunParams p, int i0, int i1,
                                                           float2* __restrict__ R) {
   extern __shared__ __align__(16) char smem[];
   const Geometry& g = p.g;
   const int ny = g.ny, ny2 = ny >> 1, ww = g.ww;
-  const int nblk = ny2 / 8;
-  const int item = i0 + blockIdx.x / nblk, y0 = (blockIdx.x % nblk) * 8;
+  const int nblk = ny2 / (8 * kRows512Sets);
+  const int item = i0 + blockIdx.x / nblk, yb = (blockIdx.x % nblk) * 8 * kRows512Sets;
   if (item >= i1) return;
   const int b = item / g.P, q = item - b * g.P;
   const int w = p.wl ? p.wl[b] : 0;
@@ -668,32 +670,41 @@ __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__
   const int grp = threadIdx.x >> 6, t = threadIdx.x & 63;
   float2* S1 = reinterpret_cast<float2*>(smem) + grp * kF512Group;
   float2* S2 = S1 + 8 * 72;
-  const int y = y0 + grp;
-  float2 a[8];
-  if (p.fmt == 0) {
-    const float* ra = reinterpret_cast<const float*>(p.frames) + (int64_t)b * g.W * g.H +
-                      (int64_t)(g.row0[q] + y) * g.W + g.col0[q];
-    const float* rb = ra + (int64_t)ny2 * g.W;
+  float2 a[kRows512Sets][8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) a[j] = make_float2(__ldg(ra + t + 64 * j), __ldg(rb + t + 64 * j));
-  } else {
+  for (int st = 0; st < kRows512Sets; ++st) {
+    const int y = yb + 8 * st + grp;
+    if (p.fmt == 0) {
+      const float* ra = reinterpret_cast<const float*>(p.frames) + (int64_t)b * g.W * g.H +
+                        (int64_t)(g.row0[q] + y) * g.W + g.col0[q];
+      const float* rb = ra + (int64_t)ny2 * g.W;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      a[j] = make_float2(load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, g.row0[q] + y, g.col0[q] + t + 64 * j),
-                         load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, g.row0[q] + y + ny2, g.col0[q] + t + 64 * j));
+      for (int j = 0; j < 8; ++j) a[st][j] = make_float2(__ldg(ra + t + 64 * j), __ldg(rb + t + 64 * j));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        a[st][j] = make_float2(load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, g.row0[q] + y, g.col0[q] + t + 64 * j),
+                               load_px(p.frames, p.fmt, p.transpose, g.W, g.H, b, g.row0[q] + y + ny2,
+                                       g.col0[q] + t + 64 * j));
+    }
   }
-  fft512_group(a, t, p.t.tw_nx, S1, S2);
-  // Hermitian split of the kept bins; all 8 row pairs of the CTA write 8 consecutive y per column
   float2* Ri = R + (size_t)(item - i0) * ww * ny;
   const float2* X0 = reinterpret_cast<const float2*>(smem);
-  for (int idx = threadIdx.x; idx < 8 * ww; idx += blockDim.x) {
-    const int c = idx >> 3, s = idx & 7;
-    const int kx = pmod(k0x + c - ww / 2, 512);
-    const int km = (512 - kx) & 511;
-    const float2* X = X0 + s * kF512Group;
-    const float2 zk = X[f512_pos(kx)], zm = X[f512_pos(km)];
-    Ri[(size_t)c * ny + y0 + s] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-    Ri[(size_t)c * ny + y0 + s + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+#pragma unroll
+  for (int st = 0; st < kRows512Sets; ++st) {
+    const int y0 = yb + 8 * st;
+    if (st > 0) __syncthreads();   // the previous set's bins are read out
+    fft512_group(a[st], t, p.t.tw_nx, S1, S2);
+    // Hermitian split of the kept bins; the 8 row pairs of the set write 8 consecutive y per column
+    for (int idx = threadIdx.x; idx < 8 * ww; idx += blockDim.x) {
+      const int c = idx >> 3, s = idx & 7;
+      const int kx = pmod(k0x + c - ww / 2, 512);
+      const int km = (512 - kx) & 511;
+      const float2* X = X0 + s * kF512Group;
+      const float2 zk = X[f512_pos(kx)], zm = X[f512_pos(km)];
+      Ri[(size_t)c * ny + y0 + s] = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+      Ri[(size_t)c * ny + y0 + s + ny2] = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    }
   }
 }
 
@@ -1089,7 +1100,7 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
     cudaMemsetAsync(peak, 0, (size_t)n * sizeof(unsigned), s_);
     if (g.nx == 512 && g.ny == 512) {
       const int f512 = 8 * kF512Group * (int)sizeof(float2);
-      lw_rows512_kernel<<<n * (g.ny / 2 / 8), 512, f512, s_>>>(p, i0, i1, R);
+      lw_rows512_kernel<<<n * (g.ny / 2 / (8 * kRows512Sets)), 512, f512, s_>>>(p, i0, i1, R);
       if (g.gh == 164 && g.wh == 164) {   // column FFT, crop and the 164-point IFFT along r in one kernel
         lw_cols512_kernel<true><<<n * ((g.ww + 7) / 8), 512, f512, s_>>>(p, i0, i1, R, T);
       } else {
