@@ -243,6 +243,36 @@ def test_pipelined_process_batch_matches_staged(name):
     assert np.array_equal(cc, ca)
 
 
+@pytest.mark.parametrize("name", ["dualpol", "pr1"])
+def test_pipelined_fields_only_matches_staged(name):
+    """No basis: the pipelined process_batch reads the int16 fields back chunk by chunk; get_fields16 then
+    returns them (once), bit-equal to run_pipeline + get_fields16, and the next call reads the device again."""
+    from paper_2204_02348_b200.engine import Engine
+    case, g, frames = load(name)
+    rows = 48
+    big = np.ascontiguousarray(np.concatenate([frames] * -(-rows // frames.shape[0]))[:rows])
+    def make():
+        eng = Engine()
+        for k, v in case["config"].items():
+            setattr(eng.config, k, v)
+        eng.config.batchCount = rows
+        eng.config.basisGroupCount = 0
+        eng.source.set_float32(big)
+        return eng
+    a = make()
+    assert a._pipeline_ok()
+    assert a.process_batch()[0] is None
+    fa = a.get_fields16()
+    b = make()
+    b.run_pipeline(0)
+    fb = b.get_fields16()
+    for x, y in zip(fa[:3], fb[:3]):
+        assert np.array_equal(x, y)
+    fa2 = a.get_fields16()   # second read comes from the device
+    for x, y in zip(fa2[:3], fb[:3]):
+        assert np.array_equal(x, y)
+
+
 @pytest.mark.parametrize("name", ["largebasis", "dualpol_g24"])
 def test_tensor_core_overlap_matches_simt_overlap(name):
     """HG overlap on tcgen05 (exact int16 splits) vs the SIMT overlap: same fields, coefs within 2e-6."""
