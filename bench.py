@@ -122,8 +122,7 @@ class ClockSampler:
         self._t = None
 
     def _run_nvml(self, nv):
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        h, mx = self._nvml
         bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
         while not self._stop.is_set():
@@ -149,18 +148,24 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def _run(self):
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-        except Exception:
+        if self._nvml is None:
             self._run_smi()
             return
         try:
+            import pynvml as nv
             self._run_nvml(nv)
         except Exception:
             self._run_smi()
 
     def __enter__(self):
+        self._nvml = None
+        try:   # NVML set up before the timed region starts, so sampling begins with it
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml = (h, float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
+        except Exception:
+            self._nvml = None
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
