@@ -90,6 +90,15 @@ def _snr(sig, noise):
     return min(10.0 * math.log10(sig / noise), SNR_CAP_DB)
 
 
+def _snr_of_ratio(r):
+    """Per-row SNR in dB from signal / noise (0: no signal -> unset; inf: no noise -> cap)."""
+    if r <= 0:
+        return _NEG
+    if math.isinf(r):
+        return SNR_CAP_DB
+    return min(float(10.0 * np.log10(r)), SNR_CAP_DB)
+
+
 def mdl_db(gram, nd):
     """MDL = 10 log10(lambda_max / lambda_min) over the top min(rows, cols) eigenvalues of the Gram matrix
     (the squared singular values; holopipe/analysis.py:158-162 takes an SVD of the matrix itself)."""
@@ -122,16 +131,15 @@ def finish_metrics(row_power, diag_power, group_power, gram, rows, cols, have_la
     dt = float(d.sum())
     v[C.METRIC_DIAG] = _db(dt / nd)
     v[C.METRIC_SNRAVG] = _snr(dt, total - dt)
-    pos = d > 0
-    ddb = np.where(pos, 10.0 * np.log10(np.maximum(d, 1e-300)), _NEG)   # no zero reaches log10
-    v[C.METRIC_DIAGBEST] = float(ddb.max())
-    v[C.METRIC_DIAGWORST] = float(ddb.min())
+    # best / worst per-row values: 10 log10 is monotonic, so take the extrema first and convert two scalars
+    # (the per-row rules of analysis.py:165-176: d <= 0 -> unset, no noise -> cap)
+    dmax, dmin = float(d.max()), float(d.min())
+    v[C.METRIC_DIAGBEST] = float(10.0 * np.log10(dmax)) if dmax > 0 else _NEG
+    v[C.METRIC_DIAGWORST] = float(10.0 * np.log10(dmin)) if dmin > 0 else _NEG
     noise = rowd - d
-    npos = noise > 0
-    snr = np.minimum(10.0 * np.log10(np.maximum(d, 1e-300) / np.where(npos, noise, 1.0)), SNR_CAP_DB)
-    snr = np.where(pos, np.where(npos, snr, SNR_CAP_DB), _NEG)   # _snr per row, vectorised
-    v[C.METRIC_SNRBEST] = float(snr.max())
-    v[C.METRIC_SNRWORST] = float(snr.min())
+    ratio = np.where(d > 0, np.where(noise > 0, d / np.where(noise > 0, noise, 1.0), np.inf), 0.0)
+    v[C.METRIC_SNRBEST] = _snr_of_ratio(float(ratio.max()))
+    v[C.METRIC_SNRWORST] = _snr_of_ratio(float(ratio.min()))
     if have_labels:
         sig = float(grp.sum())
         v[C.METRIC_SNRMG] = _snr(sig, total - sig)
