@@ -637,7 +637,18 @@ class Engine:
         self.run_pipeline(0)
         return self.coef_view()
 
-    _PIPE_CHUNKS = int(__import__("os").environ.get("HOLO_PIPE_CHUNKS", "4"))
+    # chunk count: HOLO_PIPE_CHUNKS if set, else one chunk per ~48 MB of window upload, 4..16
+    # (B200 sweep, profiles/r1s3_pipe_chunks.txt: dual-pol 131 MB flat over 2..16 chunks, PCIe-bound;
+    # large basis 537 MB + 68 MB coefficient readback 464 K frames/s at 4 chunks -> 563 K at 12)
+    _PIPE_CHUNKS_ENV = int(__import__("os").environ.get("HOLO_PIPE_CHUNKS", "0"))
+    _PIPE_CHUNKS = _PIPE_CHUNKS_ENV or 4       # minimum used by the eligibility check
+    _PIPE_CHUNK_BYTES = 48 << 20
+
+    def _pipe_chunks(self, B, upload_bytes):
+        if self._PIPE_CHUNKS_ENV:
+            return self._PIPE_CHUNKS_ENV
+        n = -(-upload_bytes // self._PIPE_CHUNK_BYTES)
+        return int(max(self._PIPE_CHUNKS, min(16, n, B // 8)))
 
     def _pipeline_ok(self):
         cfg, src = self.config, self.source
@@ -659,7 +670,8 @@ class Engine:
         packed = self._frames_dev[0]
         dev = self.device
         lib = native.lib()
-        bounds = np.linspace(0, B, self._PIPE_CHUNKS + 1).astype(int)
+        nchunks = self._pipe_chunks(B, B * ny * P * nx * es)
+        bounds = np.linspace(0, B, nchunks + 1).astype(int)
         arrived = []   # (r0, r1, event): coefficient rows of a chunk are in host_out
         with torch.cuda.device(dev):
             comp = torch.cuda.current_stream(dev)
@@ -671,7 +683,7 @@ class Engine:
             back.wait_stream(comp)
             cs = ctypes.c_void_p(copy.cuda_stream)
             ups = []
-            for c in range(self._PIPE_CHUNKS):   # every upload queued first: host work below overlaps them
+            for c in range(nchunks):   # every upload queued first: host work below overlaps them
                 r0, r1 = int(bounds[c]), int(bounds[c + 1])
                 if r1 > r0:
                     native.check(lib.hpg_upload_windows(plan0.handle, ctypes.c_void_p(hptr + r0 * W * H * es), fmt,
@@ -702,7 +714,7 @@ class Engine:
         with torch.cuda.device(dev):
             ks = ctypes.c_void_p(comp.cuda_stream)
             wl = L.batch.wl_of_row
-            for c in range(self._PIPE_CHUNKS):
+            for c in range(nchunks):
                 r0, r1 = int(bounds[c]), int(bounds[c + 1])
                 n = r1 - r0
                 if n == 0:
