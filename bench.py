@@ -2,7 +2,7 @@
 hot path (BASELINE.json metric), one JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config dualpol]
-    python bench.py --impl reference ...      # the reference CPU path (oracle port)
+    python bench.py --impl reference ...      # the reference CPU path (holopipe from baseline/_ref)
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 A step is one pass of the hot path over one batch of synthetic frames already
@@ -114,8 +114,17 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
-    def __init__(self, index):
-        self.index = index
+    def __init__(self, device):
+        """``device``: the CUDA ordinal this rank runs on.  NVML and nvidia-smi number GPUs in PCI order
+        and ignore CUDA_VISIBLE_DEVICES, so the GPU is looked up by the UUID torch reports for it."""
+        import torch
+        self.uuid = None
+        try:
+            u = str(torch.cuda.get_device_properties(device).uuid)
+            self.uuid = u if u.startswith("GPU-") else "GPU-" + u
+        except Exception:
+            pass
+        self.index = self.uuid or str(device)
         self.rows = []      # (sm_mhz, sm_max_mhz, {reason names})
         self.source = "nvml"
         self._stop = threading.Event()
@@ -162,7 +171,8 @@ class ClockSampler:
         try:   # NVML set up before the timed region starts, so sampling begins with it
             import pynvml as nv
             nv.nvmlInit()
-            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            h = (nv.nvmlDeviceGetHandleByUUID(self.uuid) if self.uuid
+                 else nv.nvmlDeviceGetHandleByIndex(int(self.index)))
             self._nvml = (h, float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)))
         except Exception:
             self._nvml = None
@@ -180,7 +190,7 @@ class ClockSampler:
         sm = [r[0] for r in self.rows]
         reasons = sorted(set().union(*(r[2] for r in self.rows)))
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
-                "reasons": reasons, "samples": len(self.rows), "source": self.source}
+                "reasons": reasons, "samples": len(self.rows), "source": self.source, "gpu_uuid": self.uuid}
 
 
 def dist_init(n_gpus):
@@ -221,7 +231,7 @@ def cpu_reference(cfg_dict, frames, min_seconds=10.0, threads=None):
     cfg = O.Cfg(**cfg_dict)
     n = frames.shape[0]
     with scipy.fft.set_workers(threads):
-        O.run_chain(cfg, frames[: min(n, 4)] if False else frames)  # warm-up (plans, caches)
+        O.run_chain(cfg, frames)  # warm-up (plans, caches)
         reps, t0 = 0, time.perf_counter()
         while True:
             O.run_chain(cfg, frames)
@@ -232,37 +242,89 @@ def cpu_reference(cfg_dict, frames, min_seconds=10.0, threads=None):
     return reps * n / el, threads, reps, el
 
 
+def holopipe_api():
+    """The reference itself -- holopipe, installed UNMODIFIED into baseline/_ref --
+    or None when that install is absent (then the oracle port stands in, kind "port")."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "holopipe")):
+        return None
+    if ref not in sys.path:
+        sys.path.append(ref)
+    import holopipe.api as R
+    return R
+
+
+def holopipe_rate(R, cfg, frames, threads, steps, warmup):
+    """Frames/s of the reference's public API on the host: holopipe.api.process_batch (= Engine.run_pipeline(0)
+    + coef_view, holopipe/api.py:854-861) with threadCount = ``threads``; mean over ``steps`` after ``warmup``."""
+    B = frames.shape[0]
+    h = R.create_handle()
+    eng = R.engine(h)
+    for k, v in (cfg | {"batchCount": B}).items():
+        setattr(eng.config, k, v)
+    eng.config.threadCount = threads
+    R.set_batch(h, B, frames)
+    for _ in range(max(warmup, 1)):
+        R.process_batch(h)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        out = R.process_batch(h)
+        times.append(time.perf_counter() - t0)
+        assert out[1] == B, "reference process_batch failed"
+    R.destroy_handle(h)
+    return B / float(np.mean(times)), float(np.mean(times))
+
+
 def run_reference_arm(args):
+    """--impl reference: the reference's own CPU implementation of the path on this box's host cores,
+    same workload / metric / unit as the B200 arm.  Rank 0 only (the other ranks exit without work)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from paper_2204_02348_b200.synth import FrameSpec, make_frames
-    sample = min(args.ref_sample, WORKLOADS[args.config]["frames"]["batch"])
+    B = args.batch or WORKLOADS[args.config]["frames"]["batch"]
+    sample = min(args.ref_sample or 1000, B)
     fspec, cfg = config_for(args.config, batch=sample)
     frames = make_frames(FrameSpec(**fspec))
-    import scipy.fft
-    from oracle import holo_oracle as O
     threads = os.cpu_count() or 1
-    ocfg = O.Cfg(**cfg)
-    with scipy.fft.set_workers(threads):
-        for _ in range(max(args.warmup, 1)):
-            O.run_chain(ocfg, frames)
-        times = []
-        for _ in range(args.steps):
-            t0 = time.perf_counter()
-            O.run_chain(ocfg, frames)
-            times.append(time.perf_counter() - t0)
-    ms = 1e3 * float(np.mean(times))
-    value = sample / (ms / 1e3)
-    desc = f"{sample} frames of the '{args.config}' workload per step (oracle port of holopipe on {threads} threads)"
-    print(json.dumps({
+    R = holopipe_api()
+    if R is not None:
+        value, sec = holopipe_rate(R, cfg, frames, threads, args.steps, args.warmup)
+        kind = "reference"
+        what = "holopipe.api.process_batch (baseline/_ref, unmodified reference)"
+        # the single-thread row BASELINE.md section 4 promises (threadCount = 1), on a bounded sample
+        n1 = min(sample, 64)
+        v1, _ = holopipe_rate(R, cfg, frames[:n1], 1, 2, 1)
+        single = {"value": v1, "unit": "frames/s", "cores": 1, "sample": f"{n1} frames x 2 steps, threadCount=1"}
+    else:
+        import scipy.fft
+        from oracle import holo_oracle as O
+        ocfg = O.Cfg(**cfg)
+        with scipy.fft.set_workers(threads):
+            for _ in range(max(args.warmup, 1)):
+                O.run_chain(ocfg, frames)
+            times = []
+            for _ in range(args.steps):
+                t0 = time.perf_counter()
+                O.run_chain(ocfg, frames)
+                times.append(time.perf_counter() - t0)
+        sec = float(np.mean(times))
+        value, kind, single = sample / sec, "port", None
+        what = "oracle/holo_oracle.py (numpy+scipy restatement of holopipe; baseline/_ref absent)"
+    desc = f"{sample} frames of the '{args.config}' workload per step, {what}, threadCount={threads}"
+    line = {
         "impl": "reference", "metric": "camera frames/sec (FFT->IFFT->HG coefs)", "value": value,
-        "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.config, "frames_per_step": sample, "host_cores": threads},
-        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": "port", "sample": desc},
+        "config": {"workload": args.config, "frames_per_step": sample, "same_config": sample == B,
+                   "host_cores": threads},
+        "cpu_baseline": {"value": value, "unit": "frames/s", "cores": threads, "kind": kind, "sample": desc},
         "e2e": {"value": value, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }
+    if single is not None:
+        line["cpu_baseline"]["threadcount_1"] = single
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -273,7 +335,7 @@ def main():
     ap.add_argument("--config", default="dualpol", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--batch", type=int, default=0, help="override frames per step (per GPU)")
-    ap.add_argument("--ref-sample", type=int, default=64)
+    ap.add_argument("--ref-sample", type=int, default=0, help="reference-arm frames per step (default min(B, 1000))")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -328,7 +390,7 @@ def main():
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     barrier(world)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(torch.cuda.current_device()) as clocks:
         for i in range(args.steps):
             flush.zero_()
             starts[i].record()
@@ -406,11 +468,21 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sample = min(B, 256)
-        v, threads, reps, el = cpu_reference(cfg | {"batchCount": sample}, frames_host[:sample],
-                                             min_seconds=args.cpu_seconds)
-        cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
-               "sample": f"{sample} frames x {reps} reps ({el:.1f} s) of the same workload; "
-                         f"oracle/holo_oracle.py (numpy+scipy restatement of holopipe)"}
+        R = holopipe_api()
+        if R is not None:   # the reference itself, ~cpu_seconds of host work
+            threads = os.cpu_count() or 1
+            v0, sec0 = holopipe_rate(R, cfg, frames_host[:sample], threads, 1, 1)
+            reps = max(1, int(args.cpu_seconds / max(sec0, 1e-3)))
+            v, sec = holopipe_rate(R, cfg, frames_host[:sample], threads, reps, 0)
+            cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "reference",
+                   "sample": f"{sample} frames x {reps} steps ({reps * sec:.1f} s) of the same workload; "
+                             f"holopipe.api.process_batch from baseline/_ref, threadCount={threads}"}
+        else:
+            v, threads, reps, el = cpu_reference(cfg | {"batchCount": sample}, frames_host[:sample],
+                                                 min_seconds=args.cpu_seconds)
+            cpu = {"value": v, "unit": "frames/s", "cores": threads, "kind": "port",
+                   "sample": f"{sample} frames x {reps} reps ({el:.1f} s) of the same workload; "
+                             f"oracle/holo_oracle.py (numpy+scipy restatement of holopipe)"}
 
     autoalign = None
     if rank == 0 and args.config == "autoalign":

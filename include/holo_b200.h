@@ -99,7 +99,9 @@ typedef struct hpg_batch {
   int32_t cal_pols, cal_batch;
   const void* ref_cal;           /* device complex64 [ref_cal_count][P][gh][gw] or NULL */
   int32_t ref_cal_count;
-  int32_t row_offset;            /* global index of row 0 (multi-GPU shards) */
+  int32_t row_offset;            /* global index of row 0 (multi-GPU shards, pipelined chunks):
+                                    batch calibration uses entry (row_offset + row) mod cal_batch,
+                                    as the reference indexes it by the global row (engine.py:247-249) */
   /* Optional frame-buffer layout override (window-packed uploads): when
    * layout_width > 0 the buffer holds [frame_count][layout_height][layout_width]
    * and pol q's FFT window starts at (layout_col0[q], layout_row0[q]). */

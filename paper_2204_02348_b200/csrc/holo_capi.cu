@@ -8,6 +8,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <map>
 #include <mutex>
 #include <tuple>
 
@@ -77,6 +78,22 @@ static void pool_free(int device, size_t bytes, void* p) {
   if (g_pool.size() < kPoolMax) g_pool.emplace_back(device, bytes, p);
   else cudaFree(p);
 }
+namespace holo {
+cudaError_t ensure_smem_optin(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{dev, func}];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+}  // namespace holo
+
 static thread_local int g_last_launches = 0;   // kernels the last hpg_run on this thread launched
 
 static int fail(int code, const std::string& msg) {
@@ -735,6 +752,7 @@ static int fill_params(const hpg_plan* P, const hpg_batch* b, const hpg_outputs*
   rp.bcal = static_cast<const float2*>(b->batch_cal);
   rp.cal_pols = b->cal_pols;
   rp.cal_batch = b->cal_batch;
+  rp.row_offset = b->row_offset;
   rp.rcal = static_cast<const float2*>(b->ref_cal);
   rp.rcal_count = std::max(1, b->ref_cal_count);
   rp.flags = flags;
@@ -778,6 +796,7 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
         return fail(HPG_INVALIDDIMENSION, "layout override does not contain the FFT window");
   }
   if (b->batch_cal && (b->cal_pols < 1 || b->cal_batch < 1)) return fail(HPG_INVALIDARGUMENT, "batch calibration dims");
+  if (b->row_offset < 0) return fail(HPG_INVALIDARGUMENT, "row_offset");
   if ((flags & HPG_FLAG_SUMMARY) && o->field_params && o->param_slots < b->batch_count + 1)
     return fail(HPG_INVALIDDIMENSION, "param_slots");
   RunParams rp;

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 1) fast128_kernel(const __
     __syncthreads();
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
-    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
     const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * WH * WW : nullptr;
     float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc, 1.f, -1, -1, rc);
 #pragma unroll
@@ -582,14 +582,10 @@ static cudaError_t launch_fast_nt(const RunParams& p, const FastTables& ft, int 
   const bool tco = NT == 256 && ft.tco_gp >= 32 && p.coefs && p.g.G > 0 && !(p.flags & kFlagNoTco);
   auto kt = fast128_kernel<42, 42, true, 256>;
   auto kf = fast128_kernel<42, 42, false, NT>;
-  static size_t configured = 0;
-  if (bytes > configured) {
-    cudaError_t e = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    configured = bytes;
-  }
+  cudaError_t e = ensure_smem_optin((const void*)kt, bytes);
+  if (e != cudaSuccess) return e;
+  e = ensure_smem_optin((const void*)kf, bytes);
+  if (e != cudaSuccess) return e;
   int per_sm = 0;
   // same registers / shared memory for both variants; the occupancy API reports 1 CTA/SM for kernels that
   // allocate tensor memory, but 3 x 128 TMEM columns fit the SM's 512
@@ -606,7 +602,8 @@ static cudaError_t launch_fast_nt(const RunParams& p, const FastTables& ft, int 
 
 cudaError_t launch_fast(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s) {
   // fewer windows than SMs: nothing to overlap across CTAs, so give each window the whole SM
-  static const int forced_nt = getenv("HOLO_FAST_NT") ? atoi(getenv("HOLO_FAST_NT")) : 0;   // diagnostic override
+  const char* env = getenv("HOLO_FAST_NT");   // diagnostic override, read per launch
+  const int forced_nt = env ? atoi(env) : 0;
   const int items = p.B * p.g.P;
   const bool wide = forced_nt ? forced_nt == 512 : items <= num_sms;
   return wide ? launch_fast_nt<512>(p, ft, num_sms, s) : launch_fast_nt<256>(p, ft, num_sms, s);

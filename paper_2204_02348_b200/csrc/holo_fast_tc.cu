@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kProd + kCons, 1) fast128tc_kernel(const __gri
     nbar(kBarCons, kCons);
     // ------------------------------------------- removal phase, peak, int16
     float2 bc = make_float2(1.f, 0.f);
-    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
     float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc, 1.f, ct, kCons);
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
@@ -484,13 +484,8 @@ cudaError_t launch_fast_tc(const RunParams& p, const FastTables& ft, int num_sms
                                   ? (size_t)p.g.P * (42 + 42) * GP * sizeof(float) : 0) + 64;
   // one CTA per SM: it owns all 512 TMEM columns
   bytes = std::max(bytes, (size_t)120 * 1024);
-  static size_t configured = 0;
-  if (bytes > configured) {
-    cudaError_t e = cudaFuncSetAttribute(fast128tc_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
-    if (e != cudaSuccess) return e;
-    configured = bytes;
-  }
+  cudaError_t e = ensure_smem_optin((const void*)fast128tc_kernel<42, 42>, bytes);
+  if (e != cudaSuccess) return e;
   const int items = p.B * p.g.P;
   const int grid = std::max(1, std::min(items, num_sms));
   fast128tc_kernel<42, 42><<<grid, kProd + kCons, bytes, s>>>(p, ft);

@@ -75,6 +75,12 @@ struct Layout {
   int64_t agg_per_cta;    // bytes of one CTA's aggregate images
 };
 
+// Raise `func`'s dynamic shared-memory limit to at least `bytes` on the CURRENT device.
+// cudaFuncSetAttribute is per device, so the configured size is tracked per
+// (device, kernel) under a mutex: a process driving several GPUs (or several host
+// threads) opts every kernel in on every device it launches on (holo_capi.cu).
+cudaError_t ensure_smem_optin(const void* func, size_t bytes);
+
 struct RunParams {
   Geometry g;
   DevTables t;
@@ -86,6 +92,7 @@ struct RunParams {
   const int32_t* wl;
   const float2* bcal;
   int cal_pols, cal_batch;
+  int row_offset;          // global index of row 0: batch calibration is indexed by the global row (engine.py:247-249)
   const float2* rcal;
   int rcal_count;
   int16_t* fr;

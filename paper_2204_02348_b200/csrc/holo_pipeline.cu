@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(NT) fused_kernel(const __grid_constant__ RunPa
     const float2* ex = p.t.rem_x + (size_t)(q * g.L + w) * g.gw;
     const float2* ey = p.t.rem_y + (size_t)(q * g.L + w) * g.gh;
     float2 bc = make_float2(1.f, 0.f);
-    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
     const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * ghw : nullptr;
     float lmax = 0.f, amax = -1.f;
     int aidx = 0x7fffffff;
@@ -961,7 +961,7 @@ __global__ void __launch_bounds__(kThreads, 3) lw_field_kernel(const __grid_cons
   const float2* ex = p.t.rem_x + (size_t)(q * g.L + w) * gw;
   const float2* ey = p.t.rem_y + (size_t)(q * g.L + w) * gh;
   float2 bc = make_float2(1.f, 0.f);
-  if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+  if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
   const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * gh * gw : nullptr;
   float2* Fi = Fo + (size_t)(item - i0) * gh * gw;
   float lmax = 0.f;
@@ -1044,18 +1044,12 @@ cudaError_t launch_lw(const RunParams& p, int num_sms, cudaStream_t s) {
   const int64_t chunk = lw_slot_items(g, items);
   const int64_t n0 = chunk;
   const size_t slot_bytes = lw_slot_bytes(g, items);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(lw_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_cols_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_field_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_field_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_rows512_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_cols512_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_cols512_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_ifft_y_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(lw_ifft_y_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    configured = true;
+  for (const void* k : {(const void*)lw_rows_kernel, (const void*)lw_cols_kernel, (const void*)lw_field_kernel<true>,
+                        (const void*)lw_field_kernel<false>, (const void*)lw_rows512_kernel,
+                        (const void*)lw_cols512_kernel<false>, (const void*)lw_cols512_kernel<true>,
+                        (const void*)lw_ifft_y_kernel<true>, (const void*)lw_ifft_y_kernel<false>}) {
+    const cudaError_t e = ensure_smem_optin(k, 200 * 1024);
+    if (e != cudaSuccess) return e;
   }
   const int rows_smem = 2 * kLwRows * g.nx * (int)sizeof(float2);
   const int cols_smem = 2 * kLwCols * g.ny * (int)sizeof(float2);

@@ -23,6 +23,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <utility>
 
 #include "holo_fast_common.cuh"
 #include "holo_internal.h"
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(256, 3)
     ct_stage<6, WW, 1, WH, 1, WH, true>(F, T, tww);
     __syncthreads();
     float2 bc = make_float2(1.f, 0.f);
-    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + (b % p.cal_batch)];
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
     float lmax = ct_stage_final_rows<7, WW, 6, WH>(T, F, tww, s_ey, s_ex, p.bcal != nullptr, bc);
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
@@ -644,18 +645,12 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
   using LY = FieldLayout<42, 42>;
   const int GP = (p.g.G + 3) & ~3;
   const size_t k2_bytes = LY::basis + (size_t)(42 + 42) * std::max(GP, 4) * sizeof(float);
-  static bool configured = false;
-  static int k2_per_sm = 1;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fourier128_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)kK1Bytes);
+  int k2_per_sm = 1;
+  for (const auto& kb : {std::make_pair((const void*)fourier128_tc2_kernel<0>, (size_t)kK1Bytes),
+                         std::make_pair((const void*)fourier128_tc2_kernel<1>, (size_t)kK1Bytes),
+                         std::make_pair((const void*)field128_kernel<42, 42>, LY::basis + 84 * 48 * sizeof(float))}) {
+    const cudaError_t e = ensure_smem_optin(kb.first, kb.second);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(fourier128_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kK1Bytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(field128_kernel<42, 42>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(LY::basis + 84 * 48 * sizeof(float)));
-    if (e != cudaSuccess) return e;
-    configured = true;
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k2_per_sm, field128_kernel<42, 42>, 256, k2_bytes);
   float2* wbuf = reinterpret_cast<float2*>(p.work);

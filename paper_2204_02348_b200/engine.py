@@ -655,7 +655,6 @@ class Engine:
         host = src.host_array() if src._pinned is None else None
         return (host is not None and not (src.format() == 1 and src.transpose)
                 and max(1, cfg.avgCount) == 1 and (cfg.basisGroupCount < 1 or cfg.basisType == C.BASISTYPE_HG)
-                and not (self.batch_cal_enabled and self.batch_cal is not None)
                 and max(1, cfg.batchCount) >= 8 * self._PIPE_CHUNKS
                 and not (self.force_generic or self.force_simt))
 
@@ -693,91 +692,101 @@ class Engine:
                 ev = torch.cuda.Event()
                 ev.record(copy)
                 ups.append(ev)
-        self.process_ifft()
-        self._st2 = self._stage2_snapshot()
-        with_coefs = self.config.basisGroupCount >= 1
-        L = self._prepare_fused(with_coefs=with_coefs)
-        M = L.plan.mode_count if with_coefs else 0
-        hw = L.fr.shape[-1] * L.fr.shape[-2]
-        # the step's result read back chunk by chunk: coefficients, or the int16 fields + scales (no basis)
-        per_row = P * M * 8 if with_coefs else P * (2 * hw * 2 + 4)
-        host_out = self._bufs.get("result_host")
-        if host_out is None or host_out.numel() < B * per_row:
-            host_out = torch.empty(B * per_row, dtype=torch.uint8).pin_memory()
-            self._bufs["result_host"] = host_out
-        if with_coefs:
-            hc = host_out[:B * P * M * 8].view(torch.complex64)
-        else:
-            hfr = host_out[:B * P * hw * 2].view(torch.int16)
-            hfi = host_out[B * P * hw * 2:2 * B * P * hw * 2].view(torch.int16)
-            hsc = host_out[2 * B * P * hw * 2:2 * B * P * hw * 2 + B * P * 4].view(torch.float32)
-        with torch.cuda.device(dev):
-            ks = ctypes.c_void_p(comp.cuda_stream)
-            wl = L.batch.wl_of_row
-            for c in range(nchunks):
-                r0, r1 = int(bounds[c]), int(bounds[c + 1])
-                n = r1 - r0
-                if n == 0:
-                    continue
-                comp.wait_event(ups[c])
-                b = type(L.batch).from_buffer_copy(L.batch)
-                o = type(L.out).from_buffer_copy(L.out)
-                b.frames = packed.data_ptr() + r0 * ny * P * nx * es
-                b.frame_count = b.batch_count = n
-                if wl:
-                    b.wl_of_row = wl + r0 * 4
-                o.field_r = L.fr.data_ptr() + r0 * P * hw * 2
-                o.field_i = L.fi.data_ptr() + r0 * P * hw * 2
-                o.field_scale = L.sc.data_ptr() + r0 * P * 4
-                if with_coefs:
-                    o.coefs = L.coefs.data_ptr() + r0 * P * M * 8
-                native.check(lib.hpg_run(L.plan.handle, ctypes.byref(b), ctypes.byref(o), L.flags, ks), "hpg_run")
-                done = torch.cuda.Event()
-                done.record(comp)
-                back.wait_event(done)   # readback on its own stream: uploads keep streaming
-                with torch.cuda.stream(back):
+        try:
+            self.process_ifft()
+            self._st2 = self._stage2_snapshot()
+            with_coefs = self.config.basisGroupCount >= 1
+            L = self._prepare_fused(with_coefs=with_coefs)
+            M = L.plan.mode_count if with_coefs else 0
+            hw = L.fr.shape[-1] * L.fr.shape[-2]
+            # the step's result read back chunk by chunk: coefficients, or the int16 fields + scales (no basis)
+            per_row = P * M * 8 if with_coefs else P * (2 * hw * 2 + 4)
+            host_out = self._bufs.get("result_host")
+            if host_out is None or host_out.numel() < B * per_row:
+                host_out = torch.empty(B * per_row, dtype=torch.uint8).pin_memory()
+                self._bufs["result_host"] = host_out
+            if with_coefs:
+                hc = host_out[:B * P * M * 8].view(torch.complex64)
+            else:
+                hfr = host_out[:B * P * hw * 2].view(torch.int16)
+                hfi = host_out[B * P * hw * 2:2 * B * P * hw * 2].view(torch.int16)
+                hsc = host_out[2 * B * P * hw * 2:2 * B * P * hw * 2 + B * P * 4].view(torch.float32)
+            with torch.cuda.device(dev):
+                ks = ctypes.c_void_p(comp.cuda_stream)
+                wl = L.batch.wl_of_row
+                for c in range(nchunks):
+                    r0, r1 = int(bounds[c]), int(bounds[c + 1])
+                    n = r1 - r0
+                    if n == 0:
+                        continue
+                    comp.wait_event(ups[c])
+                    b = type(L.batch).from_buffer_copy(L.batch)
+                    o = type(L.out).from_buffer_copy(L.out)
+                    b.frames = packed.data_ptr() + r0 * ny * P * nx * es
+                    b.frame_count = b.batch_count = n
+                    b.row_offset = L.batch.row_offset + r0   # batch calibration follows the global row
+                    if wl:
+                        b.wl_of_row = wl + r0 * 4
+                    o.field_r = L.fr.data_ptr() + r0 * P * hw * 2
+                    o.field_i = L.fi.data_ptr() + r0 * P * hw * 2
+                    o.field_scale = L.sc.data_ptr() + r0 * P * 4
                     if with_coefs:
-                        hc[r0 * P * M:r1 * P * M].copy_(L.coefs.view(-1)[r0 * P * M:r1 * P * M], non_blocking=True)
-                    else:
-                        hfr[r0 * P * hw:r1 * P * hw].copy_(L.fr.view(-1)[r0 * P * hw:r1 * P * hw], non_blocking=True)
-                        hfi[r0 * P * hw:r1 * P * hw].copy_(L.fi.view(-1)[r0 * P * hw:r1 * P * hw], non_blocking=True)
-                        hsc[r0 * P:r1 * P].copy_(L.sc.view(-1)[r0 * P:r1 * P], non_blocking=True)
-                got = torch.cuda.Event()
-                got.record(back)
-                arrived.append((r0, r1, got))
-            fin = torch.cuda.Event()
-            fin.record(back)
-            comp.wait_stream(copy)
-            comp.wait_stream(back)
-        self.last_h2d_bytes = packed.numel() * packed.element_size()
-        self._field_r, self._field_i, self._field_scale = L.fr, L.fi, L.sc
-        self._field_axes = L.plan.axes()
-        if not with_coefs:   # fields-only configuration: the int16 fields are the step's result
-            gh, gw = L.fr.shape[-2:]
-            out_fr = np.empty((B, P, gh, gw), np.int16)
-            out_fi = np.empty((B, P, gh, gw), np.int16)
-            out_sc = np.empty((B, P), np.float32)
-            sfr, sfi = hfr.numpy().reshape(B, P, gh, gw), hfi.numpy().reshape(B, P, gh, gw)
-            ssc = hsc.numpy().reshape(B, P)
-            for r0, r1, got in arrived:   # copy-out chunk by chunk as each readback lands
+                        o.coefs = L.coefs.data_ptr() + r0 * P * M * 8
+                    native.check(lib.hpg_run(L.plan.handle, ctypes.byref(b), ctypes.byref(o), L.flags, ks), "hpg_run")
+                    done = torch.cuda.Event()
+                    done.record(comp)
+                    back.wait_event(done)   # readback on its own stream: uploads keep streaming
+                    with torch.cuda.stream(back):
+                        if with_coefs:
+                            hc[r0 * P * M:r1 * P * M].copy_(L.coefs.view(-1)[r0 * P * M:r1 * P * M], non_blocking=True)
+                        else:
+                            hfr[r0 * P * hw:r1 * P * hw].copy_(L.fr.view(-1)[r0 * P * hw:r1 * P * hw], non_blocking=True)
+                            hfi[r0 * P * hw:r1 * P * hw].copy_(L.fi.view(-1)[r0 * P * hw:r1 * P * hw], non_blocking=True)
+                            hsc[r0 * P:r1 * P].copy_(L.sc.view(-1)[r0 * P:r1 * P], non_blocking=True)
+                    got = torch.cuda.Event()
+                    got.record(back)
+                    arrived.append((r0, r1, got))
+                fin = torch.cuda.Event()
+                fin.record(back)
+                comp.wait_stream(copy)
+                comp.wait_stream(back)
+            self.last_h2d_bytes = packed.numel() * packed.element_size()
+            self._field_r, self._field_i, self._field_scale = L.fr, L.fi, L.sc
+            self._field_axes = L.plan.axes()
+            if not with_coefs:   # fields-only configuration: the int16 fields are the step's result
+                gh, gw = L.fr.shape[-2:]
+                out_fr = np.empty((B, P, gh, gw), np.int16)
+                out_fi = np.empty((B, P, gh, gw), np.int16)
+                out_sc = np.empty((B, P), np.float32)
+                sfr, sfi = hfr.numpy().reshape(B, P, gh, gw), hfi.numpy().reshape(B, P, gh, gw)
+                ssc = hsc.numpy().reshape(B, P)
+                for r0, r1, got in arrived:   # copy-out chunk by chunk as each readback lands
+                    got.synchronize()
+                    out_fr[r0:r1], out_fi[r0:r1], out_sc[r0:r1] = sfr[r0:r1], sfi[r0:r1], ssc[r0:r1]
+                fin.synchronize()
+                self._coefs = None
+                self._mode_count = 0
+                self._host_fields16 = (out_fr, out_fi, out_sc)   # handed out by the next get_fields16
+                return None, B, 0, P
+            self._st3 = {"G": L.G, "waist": tuple(L.waist)}
+            self._finish_coefs(L.coefs, M, P)
+            # copy-out (engine.py:416) chunk by chunk as each readback lands, while later chunks still stream
+            staged = hc.numpy().reshape(B, P * M)
+            coefs = np.empty((B, P * M), np.complex64)
+            for r0, r1, got in arrived:
                 got.synchronize()
-                out_fr[r0:r1], out_fi[r0:r1], out_sc[r0:r1] = sfr[r0:r1], sfi[r0:r1], ssc[r0:r1]
+                coefs[r0:r1] = staged[r0:r1]
             fin.synchronize()
-            self._coefs = None
-            self._mode_count = 0
-            self._host_fields16 = (out_fr, out_fi, out_sc)   # handed out by the next get_fields16
-            return None, B, 0, P
-        self._st3 = {"G": L.G, "waist": tuple(L.waist)}
-        self._finish_coefs(L.coefs, M, P)
-        # copy-out (engine.py:416) chunk by chunk as each readback lands, while later chunks still stream
-        staged = hc.numpy().reshape(B, P * M)
-        coefs = np.empty((B, P * M), np.complex64)
-        for r0, r1, got in arrived:
-            got.synchronize()
-            coefs[r0:r1] = staged[r0:r1]
-        fin.synchronize()
-        perm = self.output_permutation()
-        return (coefs if perm is None else coefs[perm]), B, self._mode_count, P
+            perm = self.output_permutation()
+            return (coefs if perm is None else coefs[perm]), B, self._mode_count, P
+        except BaseException:
+            # a failure after the uploads were queued: the compute stream must not run ahead of
+            # the in-flight copies into `packed`, and no half-made product may survive
+            with torch.cuda.device(dev):
+                comp.wait_stream(copy)
+                comp.wait_stream(back)
+            self._clear_products()
+            raise
 
     def coef_view(self):
         plan = self._plan

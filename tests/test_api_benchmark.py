@@ -1,0 +1,31 @@
+"""api.benchmark: the six BENCHMARK_* stage rates (holopipe/bench.py:30-54, holopipe/api.py:1006-1012)
+and its error contract (never raises; (0.0, None) for an invalid handle)."""
+import numpy as np
+import pytest
+
+from paper_2204_02348_b200 import api
+from paper_2204_02348_b200 import constants as C
+
+
+def test_invalid_handle_returns_sentinel():
+    assert api.benchmark(987654) == (0.0, None)
+    assert api.benchmark(987654, goal_duration=0.2) == (0.0, None)
+    assert api.benchmark_estimate_thread_count_optimal(987654) == 2   # INVALIDHANDLE
+
+
+@pytest.mark.gpu
+def test_stage_rates_positive_and_total_bounded():
+    """Same contract as the reference's tests/test_bench.py:21-27."""
+    from tests.golden_util import load
+    case, _, frames = load("pr1")
+    h = api.create_handle()
+    eng = api.engine(h)
+    for k, v in case["config"].items():
+        setattr(eng.config, k, v)
+    eng.source.set_float32(frames)
+    rate, info = api.benchmark(h, goal_duration=0.6)
+    assert info.shape == (C.BENCHMARK_COUNT,)
+    assert np.all(info > 0), info
+    assert rate == info[C.BENCHMARK_TOTAL]
+    assert info[C.BENCHMARK_TOTAL] <= info.min() * 1.10, info
+    api.destroy_handle(h)

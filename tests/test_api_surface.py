@@ -35,3 +35,31 @@ def test_pipeline_chunk_count_policy():
     assert e._pipe_chunks(65536, 4300 * mb) == 16     # capped
     assert e._pipe_chunks(40, 4300 * mb) == 5         # >= 8 rows per chunk
     assert e._pipe_chunks(32, 1 * mb) == 4            # floor
+
+
+def test_parameter_lists_match_the_reference():
+    """Keyword callers of holopipe.api (e.g. config_set_batch_count(h, batch_count=8)) keep working:
+    every function has the reference's parameter names, order and defaults."""
+    import inspect
+    ref = json.load(open(os.path.join(HERE, "golden", "reference_api_names.json")))["params"]
+    bad = []
+    for name, plist in ref.items():
+        sig = inspect.signature(getattr(api, name))
+        ours = [[p.name] if p.default is inspect.Parameter.empty else [p.name, p.default]
+                for p in sig.parameters.values()]
+        if ours != plist:
+            bad.append((name, plist, ours))
+    assert not bad, bad
+
+
+def test_keyword_setters():
+    h = api.create_handle()
+    assert api.config_set_batch_count(h, batch_count=8) == 0
+    assert api.config_get_batch_count(h) == 8
+    assert api.config_set_tilt(h, axis=0, pol=0, tilt=1.25) == 0
+    assert api.config_get_tilt(h, 0, 0) == 1.25
+    assert api.config_set_fft_window_size_x(h, width=100) == 96
+    assert api.config_set_auto_align_mode(h, align_mode=7) == 8      # INVALIDARGUMENT
+    assert api.config_set_pol_lock_tilt(h, pol_lock=1) == 0
+    assert api.config_set_basis_group_count(123456, group_count=3) == 2
+    api.destroy_handle(h)
