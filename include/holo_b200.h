@@ -19,6 +19,7 @@
  *   hpg_extract_coefs    engine.py:353-385 / hgbasis.py:101-116 (overlap of int16 fields)
  *   hpg_metric_partials  analysis.py:104-188 (transfer-matrix row/diag/group power sums,
  *                        Gram matrix for MDL) -- reduced across ranks by the caller
+ *   hpg_coef_transform   engine.py:371-382 (LG / custom transform of the HG coefficients)
  *
  * Conventions
  *   - Every function returns an hpg_status (same integers as holopipe ErrorCode,
@@ -212,6 +213,16 @@ typedef struct hpg_metric_args {
 } hpg_metric_args;
 
 int hpg_metric_partials(const hpg_metric_args* args, void* stream);
+
+/* LG / custom basis transform of the HG coefficients (holopipe/engine.py:371-382):
+ * out[r][p][o] = sum_{m < use} T[o][m] coefs[r][p][m], accumulated in fp64 like the
+ * reference's complex128 einsum.  coefs complex64 [rows][pols][modes_in], transform
+ * complex128 [modes_out][ld] (row o, column m), out complex64 [rows][pols][modes_out].
+ * block_diagonal != 0 declares T block-diagonal by HG mode group (conj(T_LG),
+ * hgbasis.py:126-152): output o of group g then reads only that group's inputs. */
+int hpg_coef_transform(const void* coefs, int64_t rows, int32_t pols, int32_t modes_in, const void* transform,
+                       int32_t modes_out, int32_t use, int32_t ld, int32_t block_diagonal, void* out,
+                       void* stream);
 
 /* Host -> device upload of only the FFT windows of F frames (the bytes the
  * pipeline reads, holopipe/pipeline.py:47-54): one cudaMemcpy3DAsync per pol

@@ -521,13 +521,14 @@ def ref_calibration(cfg, kind, raw, origins, xis, lams, wh, ww, mask, xa, ya):
     return out
 
 
-def run_chain(cfg, frames, batch_cal=None, stop_after=None, ref_cal=None):
+def run_chain(cfg, frames, batch_cal=None, stop_after=None, ref_cal=None, custom_transform=None):
     """Reference pipeline on host frames; returns a dict of stage products.
 
     Follows holopipe/engine.py:135-385 (process_fft, process_ifft,
     process_remove_tilt, extract_coefs) for float32 frames (B*A, H, W).
     ``ref_cal`` = (kind, raw) enables the reference-wave calibration
     (kind 1 intensity (Lc, H, W) float32, kind 2 field complex64).
+    ``custom_transform`` (out x in complex) is the user matrix of basisType CUSTOM.
     """
     W, H = cfg.frameWidth, cfg.frameHeight
     nx, ny, p = cfg.fftWindowSizeX, cfg.fftWindowSizeY, cfg.framePixelSize
@@ -607,6 +608,15 @@ def run_chain(cfg, frames, batch_cal=None, stop_after=None, ref_cal=None):
         deq = ((f16r[:, q].astype(np.float32) + 1j * f16i[:, q].astype(np.float32))
                / scale[:, q, None, None])
         hg[:, q] = overlap(deq, xa, ya, G, waist[q])
+    transform = None   # engine.py:371-382: LG = conj(T_LG); CUSTOM = the user matrix (None -> HG)
+    if getattr(cfg, "basisType", 0) == 1:
+        transform = np.conj(lg_matrix(G))
+    elif getattr(cfg, "basisType", 0) == 2:
+        transform = custom_transform
+    if transform is not None:
+        use = min(M, transform.shape[1])
+        hg = np.einsum("om,bpm->bpo", transform[:, :use], hg[:, :, :use].astype(np.complex128)).astype(np.complex64)
+        M = hg.shape[-1]
     out["coefs"] = hg.reshape(B, P * M)
     out["coefs_out"] = out["coefs"][output_order(cfg, B, len(lams))]   # engine.py:408-417
     out["mode_count"] = M

@@ -97,7 +97,60 @@ __global__ void gram_kernel(const MArgs a) {
   if (i < n && j < n) a.gram[(size_t)i * n + j] = make_double2(sr, si);
 }
 
+// out[r][p][o] = sum_{m < use} T[o][m] x[r][p][m], fp64 accumulation (the reference's complex128
+// einsum, holopipe/engine.py:375-380).  block != 0: T is block-diagonal by mode group (the HG->LG
+// matrix, hgbasis.py:126-152), so output o of group g only reads inputs [g(g+1)/2, g(g+1)/2 + g].
+__global__ void coef_transform_kernel(const float2* __restrict__ x, int64_t rows, int pols, int m_in,
+                                      const double2* __restrict__ t, int m_out, int use, int ld, int block,
+                                      float2* __restrict__ out) {
+  extern __shared__ double2 xs[];
+  const int64_t rp = blockIdx.x;   // one (row, pol) per CTA
+  const float2* xr = x + rp * m_in;
+  for (int m = threadIdx.x; m < use; m += blockDim.x) {
+    const float2 v = xr[m];
+    xs[m] = make_double2(v.x, v.y);
+  }
+  __syncthreads();
+  for (int o = threadIdx.x; o < m_out; o += blockDim.x) {
+    int lo = 0, hi = use;
+    if (block) {
+      int g = (int)((sqrt(8.0 * o + 1.0) - 1.0) * 0.5);
+      while ((g + 1) * (g + 2) / 2 <= o) ++g;
+      while (g * (g + 1) / 2 > o) --g;
+      lo = g * (g + 1) / 2;
+      hi = min(use, lo + g + 1);
+    }
+    const double2* tr = t + (int64_t)o * ld;
+    double re = 0.0, im = 0.0;
+    for (int m = lo; m < hi; ++m) {
+      const double2 a = __ldg(&tr[m]), b = xs[m];
+      re = fma(a.x, b.x, fma(-a.y, b.y, re));
+      im = fma(a.x, b.y, fma(a.y, b.x, im));
+    }
+    out[rp * m_out + o] = make_float2((float)re, (float)im);
+  }
+}
+
 }  // namespace
+
+extern "C" int hpg_coef_transform(const void* coefs, int64_t rows, int32_t pols, int32_t modes_in,
+                                  const void* transform, int32_t modes_out, int32_t use, int32_t ld,
+                                  int32_t block_diagonal, void* out, void* stream) {
+  if (!coefs || !transform || !out) return HPG_NULLPOINTER;
+  if (rows < 0 || pols < 1 || modes_in < 1 || modes_out < 1 || use < 1 || use > modes_in || ld < use)
+    return HPG_INVALIDDIMENSION;
+  if (rows == 0) return HPG_SUCCESS;
+  const size_t smem = (size_t)use * sizeof(double2);
+  if (smem > 200 * 1024) return HPG_INVALIDDIMENSION;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(coef_transform_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return HPG_ERROR;
+  coef_transform_kernel<<<(unsigned)(rows * pols), 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const float2*>(coefs), rows, pols, modes_in, static_cast<const double2*>(transform), modes_out,
+      use, ld, block_diagonal, static_cast<float2*>(out));
+  return cudaGetLastError() == cudaSuccess ? HPG_SUCCESS : HPG_ERROR;
+}
 
 extern "C" int hpg_metric_partials(const hpg_metric_args* m, void* stream) {
   if (!m || !m->coefs || !m->row_ids || !m->row_power || !m->diag_power || !m->group_power)

@@ -89,55 +89,76 @@ def host_partials(coefs, labels, diag_offset, ndiag):
     return rp, dp, gp, gram
 
 
-def calc_metrics(eng, row_offset=0, group=None):
-    """Transfer-matrix metrics of a batch sharded over the process group.
+def shard_partials(coefs, local_rows, labels, diag_offset, ndiag, dev):
+    """fp64 partial sums of one shard's rows of one wavelength, on the GPU (hpg_metric_partials).
 
-    ``eng`` holds this rank's rows (a contiguous shard starting at global row
-    ``row_offset``); wavelength membership follows the global row index
-    (holopipe/engine.py:102-106).  Returns the MetricsReport, identical on
-    every rank.  Pol-independent / A A^H variants are single-process only.
-    """
+    ``local_rows``: indices into ``coefs`` (this rank's rows of the wavelength, in global order);
+    ``diag_offset``: the global index, among the wavelength's rows, of the first of them -- the
+    transfer-matrix diagonal runs along the GLOBAL row (holopipe/analysis.py:155-176);
+    ``ndiag``: min(global rows of the wavelength, cols).  Returns (row, diag, group power, Gram)."""
     import torch
     from . import native
+    R = len(local_rows)
+    cols = coefs.shape[1]
+    rp = torch.zeros(R, dtype=torch.float64, device=dev)
+    dp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
+    gp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
+    gram = torch.zeros((cols, cols), dtype=torch.complex128, device=dev)
+    if R:
+        ids = torch.as_tensor(np.asarray(local_rows, np.int32), device=dev)
+        a = native.MetricArgs()
+        a.coefs = coefs.data_ptr()
+        a.rows, a.cols, a.ld = R, cols, cols
+        a.row_ids = ids.data_ptr()
+        a.labels = labels.data_ptr()
+        a.ndiag, a.diag_offset, a.gram_rows = ndiag, diag_offset, 0
+        a.row_power, a.diag_power, a.group_power = rp.data_ptr(), dp.data_ptr(), gp.data_ptr()
+        a.gram = gram.data_ptr()
+        with torch.cuda.device(dev):
+            native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle(dev)),
+                         "hpg_metric_partials")
+    return rp, dp, gp, gram
+
+
+def mode_labels(P, M, dev):
+    """(pol, mode group) label of every coefficient column: SNRMG's signal set (analysis.py:180-188)."""
+    import torch
+    return torch.as_tensor(np.array([q * 1000 + mode_group_of_index(i) for q in range(P) for i in range(M)],
+                                    np.int32), device=dev)
+
+
+def wavelength_of_rows(rows, B, cfg):
+    """Wavelength index of global rows (holopipe/engine.py:102-106)."""
+    L = len(cfg.wavelength_list())
+    if cfg.wavelengthOrdering[C.WAVELENGTHORDER_INPUT] == C.WAVELENGTHORDER_FAST or L <= 1:
+        return rows % L
+    return np.minimum(rows * L // B, L - 1)
+
+
+def calc_metrics(eng, group=None):
+    """Transfer-matrix metrics of a batch sharded over the process group.
+
+    ``eng`` holds this rank's rows (a contiguous shard; its global row offset is the
+    sum of the lower ranks' row counts); wavelength membership follows the global
+    row index (holopipe/engine.py:102-106).  Returns the MetricsReport, identical on
+    every rank.  Pol-independent / A A^H variants are single-process only.
+    """
     cfg = eng.config
     dev = eng.device
     coefs = eng.coefs_device()
     B_local = coefs.shape[0]
     P, M = eng._st0["P"], eng._mode_count
     cols = P * M
-    lams = cfg.wavelength_list()
-    L = len(lams)
+    L = len(cfg.wavelength_list())
     start, B = exclusive_prefix(B_local, group, device=dev)
-    rows = np.arange(start, start + B_local)
-    if cfg.wavelengthOrdering[C.WAVELENGTHORDER_INPUT] == C.WAVELENGTHORDER_FAST or L <= 1:
-        wl = rows % L
-    else:
-        wl = np.minimum(rows * L // B, L - 1)
-    labels = torch.as_tensor(np.array([q * 1000 + mode_group_of_index(i) for q in range(P) for i in range(M)],
-                                      np.int32), device=dev)
+    wl = wavelength_of_rows(np.arange(start, start + B_local), B, cfg)
+    labels = mode_labels(P, M, dev)
     per = np.full((C.METRIC_COUNT, L), C.METRIC_UNSET)
     for w in range(L):
         local = np.nonzero(wl == w)[0]
         off, n_w = exclusive_prefix(local.size, group, device=dev)
         if n_w == 0:
             continue
-        R = local.size
-        rp = torch.zeros(R, dtype=torch.float64, device=dev)
-        dp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
-        gp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
-        gram = torch.zeros((cols, cols), dtype=torch.complex128, device=dev)
-        if R:
-            ids = torch.as_tensor(local.astype(np.int32), device=dev)
-            a = native.MetricArgs()
-            a.coefs = coefs.data_ptr()
-            a.rows, a.cols, a.ld = R, cols, cols
-            a.row_ids = ids.data_ptr()
-            a.labels = labels.data_ptr()
-            a.ndiag, a.diag_offset, a.gram_rows = min(n_w, cols), off, 0
-            a.row_power, a.diag_power, a.group_power = rp.data_ptr(), dp.data_ptr(), gp.data_ptr()
-            a.gram = gram.data_ptr()
-            with torch.cuda.device(dev):
-                native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle()),
-                             "hpg_metric_partials")
+        rp, dp, gp, gram = shard_partials(coefs, local, labels, off, min(n_w, cols), dev)
         per[:, w] = reduce_and_finish(rp, dp, gp, gram, n_w, cols, group)
     return average_slot(per)

@@ -490,24 +490,34 @@ class Engine:
         return ErrorCode.SUCCESS
 
     def _finish_coefs(self, hg, M, P):
-        """Optional LG / custom transform (engine.py:371-384)."""
+        """Optional LG / custom transform (engine.py:371-384), on the GPU (hpg_coef_transform, fp64
+        accumulation like the reference's complex128 einsum)."""
         cfg = self.config
         torch = _torch()
         B = hg.shape[0]
-        transform = None
+        transform, block = None, 0
         if cfg.basisType == C.BASISTYPE_LG:
-            from .hgbasis import hg_to_lg_transform
-            transform = np.conj(hg_to_lg_transform(cfg.basisGroupCount))
-        elif cfg.basisType == C.BASISTYPE_CUSTOM:
-            transform = self.custom_transform
+            key = ("lg", cfg.basisGroupCount)
+            cached = self._bufs.get("lg_T")
+            if cached is None or cached[0] != key:
+                from .hgbasis import hg_to_lg_transform
+                T = np.ascontiguousarray(np.conj(hg_to_lg_transform(cfg.basisGroupCount)))
+                cached = (key, torch.as_tensor(T, dtype=torch.complex128, device=self.device))
+                self._bufs["lg_T"] = cached
+            transform, block = cached[1], 1
+        elif cfg.basisType == C.BASISTYPE_CUSTOM and self.custom_transform is not None:
+            transform = torch.as_tensor(np.ascontiguousarray(self.custom_transform), dtype=torch.complex128,
+                                        device=self.device)
         if transform is not None:
-            use = min(M, transform.shape[1])
-            T = torch.as_tensor(np.ascontiguousarray(transform[:, :use]), dtype=torch.complex128,
-                                device=self.device)
-            x = hg.view(B, P, M)[:, :, :use].to(torch.complex128)
-            out = torch.einsum("om,bpm->bpo", T, x).to(torch.complex64)
-            self._mode_count = out.shape[-1]
-            self._coefs = out.reshape(B, P * self._mode_count)
+            m_out, ld = transform.shape
+            use = min(M, ld)
+            out = self._buf("coefs_t", (B, P * m_out), torch.complex64)
+            with torch.cuda.device(self.device):
+                native.check(native.lib().hpg_coef_transform(native.ptr(hg), B, P, M, native.ptr(transform), m_out,
+                                                             use, ld, block, native.ptr(out),
+                                                             native.stream_handle()), "hpg_coef_transform")
+            self._mode_count = m_out
+            self._coefs = out
         else:
             self._mode_count = M
             self._coefs = hg

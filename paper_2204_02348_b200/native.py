@@ -33,7 +33,7 @@ EXPORTS = [
     "hpg_plan_get_basis", "hpg_workspace_size", "hpg_run", "hpg_finalize_summary",
     "hpg_fourier_full", "hpg_extract_coefs", "hpg_ref_calibration_finish", "hpg_metric_partials", "hpg_plane_summary",
     "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_upload_windows", "hpg_last_error",
-    "hpg_last_launch_count",
+    "hpg_last_launch_count", "hpg_coef_transform",
 ]
 
 
@@ -119,6 +119,8 @@ def lib():
     L.hpg_extract_coefs.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_void_p,
                                     c_void_p]
     L.hpg_metric_partials.argtypes = [P(MetricArgs), c_void_p]
+    L.hpg_coef_transform.argtypes = [c_void_p, c_int64, c_int32, c_int32, c_void_p, c_int32, c_int32, c_int32,
+                                     c_int32, c_void_p, c_void_p]
     L.hpg_plane_summary.argtypes = [c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p, c_void_p,
                                     c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]
     L.hpg_field_intensity.argtypes = [c_void_p, c_void_p, c_void_p, c_int32, c_int32, c_int32, c_int32,

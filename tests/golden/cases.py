@@ -126,6 +126,44 @@ CASES = {
                     tilt=[[1.2, 1.2], [0.9, 0.9]], basisGroupCount=24,
                     basisWaist=[200e-6, 180e-6], polLockBasisWaist=0,
                     beamCentre=[[-160 * PIX, 160 * PIX], [0.0, 0.0]])),
+    # LG basis: conj(T_LG) applied after the HG overlap (holopipe/engine.py:371-382, hgbasis.py:126-175)
+    "lg": dict(
+        frames=dict(width=640, height=256, pol_count=2, batch=2, group_count=6,
+                    waist=200e-6, tilt=(1.2, 0.9), noise="poisson", seed=31),
+        config=_cfg(frameWidth=640, frameHeight=256, polCount=2, batchCount=2,
+                    tilt=[[1.2, 1.2], [0.9, 0.9]], basisGroupCount=6, basisType=1,
+                    basisWaist=[200e-6, 200e-6], beamCentre=[[-160 * PIX, 160 * PIX], [0.0, 0.0]])),
+    # user transform (12 out x 10 in) narrower than the 15 HG modes: only the first 10 enter
+    # (holopipe/engine.py:375-380, use = min(hg_count, transform.shape[1]))
+    "custom": dict(
+        frames=dict(width=320, height=256, pol_count=1, batch=3, group_count=5,
+                    waist=200e-6, tilt=(1.0, 1.0), noise="gauss", seed=32),
+        config=_cfg(frameWidth=320, frameHeight=256, polCount=1, batchCount=3,
+                    tilt=[[1.0, 1.0], [1.0, 1.0]], basisGroupCount=5, basisType=2,
+                    basisWaist=[200e-6, 200e-6]),
+        custom=dict(seed=33, out=12, inp=10)),
+    # SEQUENTIALSWEEP averaging over two wavelengths (holopipe/engine.py:111-113)
+    "avg_sweep": dict(
+        frames=dict(width=256, height=256, pol_count=1, batch=8, group_count=4,
+                    waist=200e-6, tilt=(1.0, 1.0), noise="gauss", seed=34),
+        config=_cfg(frameWidth=256, frameHeight=256, polCount=1, batchCount=4, avgCount=2, avgMode=2,
+                    wavelengths=[1550e-9, 1580e-9], tilt=[[1.0, 1.0], [1.0, 1.0]],
+                    basisGroupCount=4, basisWaist=[200e-6, 200e-6])),
+    # process_batch_frequency_sweep_linear (holopipe/engine.py:419-431), output ordering swapped
+    "sweep_linear": dict(
+        frames=dict(width=256, height=256, pol_count=1, batch=6, group_count=4,
+                    waist=200e-6, tilt=(1.0, 1.0), noise="gauss", seed=35),
+        config=_cfg(frameWidth=256, frameHeight=256, polCount=1, batchCount=6, wavelengthOrdering=[0, 1],
+                    tilt=[[1.0, 1.0], [1.0, 1.0]], basisGroupCount=4, basisWaist=[200e-6, 200e-6]),
+        sweep=dict(kind="linear", start=1540e-9, stop=1590e-9, count=3)),
+    # process_batch_wavelength_sweep_arbitrary (holopipe/engine.py:433-442)
+    "sweep_arbitrary": dict(
+        frames=dict(width=320, height=128, pol_count=2, batch=4, group_count=4,
+                    waist=120e-6, tilt=(1.0, 1.0), noise="gauss", seed=36),
+        config=_cfg(frameWidth=320, frameHeight=128, polCount=2, batchCount=4, wavelengthOrdering=[1, 0],
+                    tilt=[[1.0, 1.0], [1.0, 1.0]], basisGroupCount=4, basisWaist=[120e-6, 120e-6],
+                    beamCentre=[[-80 * PIX, 80 * PIX], [0.0, 0.0]]),
+        sweep=dict(kind="arbitrary", wavelengths=[1575e-9, 1555e-9], count=2)),
     # reference-wave calibration, intensity kind (holopipe/engine.py:276-335)
     "refcal_int": dict(
         frames=dict(width=256, height=256, pol_count=1, batch=3, group_count=6,
@@ -176,3 +214,24 @@ def make_ref_cal(case):
             phi = a * (X / w0) + b * (Y / w0) + c * ((X ** 2 + Y ** 2) / w0 ** 2)
             out.append((amp * np.exp(-2j * np.pi * (fx * X + fy * Y) + 1j * phi)).astype(np.complex64))
     return spec["kind"], np.stack(out)
+
+
+def make_custom(case):
+    """Seeded user transform (out x in, complex64) of a case's ``custom`` spec."""
+    import numpy as np
+    spec = case["custom"]
+    rng = np.random.default_rng(spec["seed"])
+    t = rng.standard_normal((spec["out"], spec["inp"])) + 1j * rng.standard_normal((spec["out"], spec["inp"]))
+    return (t / np.sqrt(spec["inp"])).astype(np.complex64)
+
+
+def sweep_wavelengths(case):
+    """The wavelength list a case's ``sweep`` sets (holopipe/engine.py:419-442)."""
+    import numpy as np
+    sw = case["sweep"]
+    if sw["kind"] == "linear":
+        if sw["count"] == 1:
+            return [float(sw["start"])]
+        f0, f1 = 1.0 / sw["start"], 1.0 / sw["stop"]
+        return list(1.0 / (f0 + np.arange(sw["count"]) * (f1 - f0) / (sw["count"] - 1)))
+    return [float(v) for v in sw["wavelengths"][:sw["count"]]]

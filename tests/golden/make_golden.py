@@ -28,7 +28,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, "/root/reference/pkg/src")
 
 from paper_2204_02348_b200.synth import FrameSpec, make_frames, frames_digest  # noqa: E402
-from tests.golden.cases import CASES, make_ref_cal  # noqa: E402
+from tests.golden.cases import CASES, make_custom, make_ref_cal  # noqa: E402
 
 
 def run_reference(case):
@@ -52,7 +52,15 @@ def run_reference(case):
             eng.ref_cal.set_intensity(raw, Lc, Wc, Hc)
         else:
             eng.ref_cal.set_field(raw, Lc, Wc, Hc)
-    eng.run_pipeline(0)
+    if case.get("custom") is not None:
+        eng.custom_transform = make_custom(case)
+    sweep = case.get("sweep")
+    if sweep is None:
+        eng.run_pipeline(0)
+    elif sweep["kind"] == "linear":
+        eng.process_batch_frequency_sweep_linear(sweep["start"], sweep["stop"], sweep["count"])
+    else:
+        eng.process_batch_wavelength_sweep_arbitrary(np.asarray(sweep["wavelengths"]), sweep["count"])
     out = {
         "frames_sha256": np.array(frames_digest(frames)),
         "fr": eng._field_r, "fi": eng._field_i, "scale": eng._field_scale,

@@ -4,7 +4,7 @@ reference's own outputs (golden fixtures) and the oracle on the same frames."""
 import numpy as np
 import pytest
 
-from tests.golden.cases import CASES, make_ref_cal
+from tests.golden.cases import CASES, make_custom, make_ref_cal
 from tests.golden_util import dequant, load, rel_l2_rows
 
 pytestmark = pytest.mark.gpu
@@ -27,14 +27,27 @@ def _engine(case, frames):
         kind, raw = make_ref_cal(case)
         Lc, Hc, Wc = raw.shape
         (eng.ref_cal.set_intensity if kind == 1 else eng.ref_cal.set_field)(raw, Lc, Wc, Hc)
+    if case.get("custom") is not None:
+        eng.custom_transform = make_custom(case)
     return eng
+
+
+def _run(eng, case):
+    """run_pipeline(0), or the case's sweep entry point (holopipe/engine.py:419-442)."""
+    sw = case.get("sweep")
+    if sw is None:
+        eng.run_pipeline(0)
+    elif sw["kind"] == "linear":
+        eng.process_batch_frequency_sweep_linear(sw["start"], sw["stop"], sw["count"])
+    else:
+        eng.process_batch_wavelength_sweep_arbitrary(np.asarray(sw["wavelengths"]), sw["count"])
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_fields_and_coefs_match_reference(name):
     case, g, frames = load(name)
     eng = _engine(case, frames)
-    eng.run_pipeline(0)
+    _run(eng, case)
     fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
     assert fr.shape == g["fr"].shape
     ef = rel_l2_rows(dequant(fr, fi, sc), dequant(g["fr"], g["fi"], g["scale"]))
@@ -65,9 +78,20 @@ def test_field_summary_matches_reference(name):
     for k in (0, 1, 2, 3, 5, 6):
         scale = np.abs(ref[k]).max() + 1e-30
         assert np.allclose(s.parameters[k], ref[k], rtol=2e-4, atol=2e-4 * scale), k
-    # MAXABSIDX: same pixel, or a pixel whose magnitude ties within tolerance
+    # MAXABSIDX (analysis.py:61-64): the same flat pixel, except where the two pixels' magnitudes are a
+    # proven tie -- equal within fp32 rounding in the oracle's unquantised field (aggregate slot: in
+    # sqrt(sum_b |F|^2), analysis.py:88-91)
     same = s.parameters[4].view(np.int32) == ref[4].view(np.int32)
-    assert same.mean() >= 0.9
+    if not same.all():
+        from oracle import holo_oracle as O
+        F = O.run_chain(O.Cfg(**case["config"]), frames, batch_cal=case.get("batch_cal"))["fields"]
+        B = F.shape[0]
+        for q, slot in zip(*np.nonzero(~same)):
+            ig = int(s.parameters[4, q, slot].view(np.int32))
+            ir = int(ref[4, q, slot].view(np.int32))
+            img = (np.abs(F[slot, q]) if slot < B else
+                   np.sqrt((np.abs(F[:, q].astype(np.complex128)) ** 2).sum(0))).ravel()
+            assert abs(float(img[ig]) - float(img[ir])) <= 2e-6 * float(img[ir]), (name, q, slot, ig, ir)
     assert np.allclose(s.total_intensity, g["field_inten"], rtol=2e-4, atol=1e-4 * g["field_inten"].max())
 
 

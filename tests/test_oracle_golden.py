@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 from oracle import holo_oracle as O
-from tests.golden.cases import CASES, make_ref_cal
+from tests.golden.cases import CASES, make_custom, make_ref_cal, sweep_wavelengths
 from tests.golden_util import load, rel_l2_rows
 
 
@@ -12,8 +12,11 @@ from tests.golden_util import load, rel_l2_rows
 def test_oracle_matches_reference_fixture(name):
     case, g, frames = load(name)
     cfg = O.Cfg(**case["config"])
+    if case.get("sweep"):
+        cfg.wavelengths = sweep_wavelengths(case)
     rc = make_ref_cal(case) if case.get("ref_cal") else None
-    out = O.run_chain(cfg, frames, batch_cal=case.get("batch_cal"), ref_cal=rc)
+    ct = make_custom(case) if case.get("custom") else None
+    out = O.run_chain(cfg, frames, batch_cal=case.get("batch_cal"), ref_cal=rc, custom_transform=ct)
     if rc is not None:
         assert np.array_equal(out["ref_applied"], g["ref_applied"])
     # int16 fields, scales and field-plane analysis are bit-exact
