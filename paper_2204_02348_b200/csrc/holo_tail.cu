@@ -1,0 +1,293 @@
+// Field tail of the 128-window / 42 x 42 geometry: W -> 42 x 42 IFFT -> removal phase, calibrations ->
+// int16 packing -> HG overlap (holopipe/pipeline.py:130-199, engine.py:234-272, hgbasis.py:101-116).
+//
+// One WARP per window, no CTA-wide barrier: a warp owns a window buffer in shared memory and walks
+// its window through every step with __syncwarp only, so the SM's warps are all independent and the
+// per-step parallelism (294 / 252 small DFTs per IFFT axis) fills the 32 lanes.
+//
+// The 42-point inverse DFT uses the Good-Thomas prime-factor map (42 = 6 x 7, gcd 1): input n =
+// (7 n1 + 6 n2) mod 42, output k = (7 k1 + 36 k2) mod 42, so
+//     X[k] = sum_n2 e^{2 pi i n2 k2 / 7} sum_n1 e^{2 pi i n1 k1 / 6} x[n]
+// -- a DFT-6 over n1 for each n2, then a DFT-7 over n2 for each k1, NO twiddle factors.  Both passes
+// work in place (a DFT-6 writes k1 where it read n1); natural index k ends at position
+// pos(k) = (7 (k mod 6) + 6 (k mod 7)) mod 42, which the epilogue reads through.
+#include <algorithm>
+
+#include "holo_internal.h"
+
+namespace holo {
+
+namespace {
+
+constexpr int kN = 42;          // field side (wh = ww = 42)
+constexpr int kPC = 43;         // buffer pitch (float2) of one column sequence: odd -> spread banks
+constexpr int kTailWarps = 8;   // windows in flight per CTA (one per warp)
+
+HOLO_DEV int pfa_pos(int k) { return (7 * (k % 6) + 6 * (k % 7)) % kN; }
+HOLO_DEV int pfa_in(int a, int b) { return (7 * a + 6 * b) % kN; }   // position of (n1 | k1 = a, n2 | k2 = b)
+
+}  // namespace
+
+// per-warp shared-memory layout (bytes): F / U [42][43] float2 | Fq [42][42] int16x2
+struct TailLayout {
+  int buf_bytes;    // max(42*43, 42*GP) float2
+  int warp_bytes;   // buf + Fq, 16-byte aligned
+  int basis_off;    // per-CTA basis tables [P][(42 + 42) * GP] float, after the warp regions
+  int total;
+};
+
+inline TailLayout tail_layout(int G, int P) {
+  TailLayout L;
+  const int GP = std::max(4, (G + 3) & ~3);
+  L.buf_bytes = std::max(kN * kPC, kN * GP) * 8;
+  L.warp_bytes = (L.buf_bytes + kN * kN * 4 + 15) & ~15;
+  L.basis_off = kTailWarps * L.warp_bytes;
+  L.total = L.basis_off + (G > 0 ? P * (kN + kN) * GP * 4 : 0);
+  return L;
+}
+
+namespace {
+
+// in-place inverse DFT-6 / DFT-7 passes over the 42 sequences of one axis.  Sequence s, element e is at
+// buf[s * SS + e * ES].
+template <int SS, int ES>
+HOLO_DEV void pfa_pass6(float2* buf, int lane) {
+  for (int t = lane; t < kN * 7; t += 32) {
+    const int s = t / 7, n2 = t - 7 * s;
+    float2* q = buf + s * SS;
+    float2 v[6];
+#pragma unroll
+    for (int n1 = 0; n1 < 6; ++n1) v[n1] = q[pfa_in(n1, n2) * ES];
+    dft6<true>(v);
+#pragma unroll
+    for (int k1 = 0; k1 < 6; ++k1) q[pfa_in(k1, n2) * ES] = v[k1];
+  }
+}
+
+template <int SS, int ES>
+HOLO_DEV void pfa_pass7(float2* buf, int lane) {
+  for (int t = lane; t < kN * 6; t += 32) {
+    const int s = t / 6, k1 = t - 6 * s;
+    float2* q = buf + s * SS;
+    float2 v[7];
+#pragma unroll
+    for (int n2 = 0; n2 < 7; ++n2) v[n2] = q[pfa_in(k1, n2) * ES];
+    dft7<true>(v);
+#pragma unroll
+    for (int k2 = 0; k2 < 7; ++k2) q[pfa_in(k1, k2) * ES] = v[k2];
+  }
+}
+
+}  // namespace
+
+// win: [items][2][42 r][42 c] float (Re plane, Im plane of the masked, recentred window, as K1 writes it)
+__global__ void __launch_bounds__(kTailWarps * 32, 1)
+    tail42_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
+                  const float* __restrict__ win, TailLayout L) {
+  extern __shared__ __align__(16) char smem[];
+  const Geometry& g = p.g;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = (p.coefs && g.G > 0) ? g.G : 0;
+  const int GP = max(4, (g.G + 3) & ~3);
+  float2* buf = reinterpret_cast<float2*>(smem + warp * L.warp_bytes);                  // [c][r] pitch 43
+  uint32_t* fq = reinterpret_cast<uint32_t*>(smem + warp * L.warp_bytes + L.buf_bytes);  // [y][x] int16x2
+  float* basis = reinterpret_cast<float*>(smem + L.basis_off);                           // [P][x|y][GP]
+
+  if (G > 0) {   // basis of every pol, transposed [x][m] / [y][n] (hgbasis.py:95-99 profiles)
+    for (int q = 0; q < g.P; ++q) {
+      const float* hx = p.t.hx + (size_t)q * g.G * kN;
+      const float* hy = p.t.hy + (size_t)q * g.G * kN;
+      float* bq = basis + q * 2 * kN * GP;
+      for (int i = threadIdx.x; i < kN * GP; i += blockDim.x) {
+        const int x = i / GP, m = i - x * GP;
+        bq[i] = m < G ? __ldg(&hx[m * kN + x]) : 0.f;
+        bq[kN * GP + i] = m < G ? __ldg(&hy[m * kN + x]) : 0.f;
+      }
+    }
+  }
+  __syncthreads();
+
+  const int nw = gridDim.x * kTailWarps;
+  for (int item = i0 + blockIdx.x * kTailWarps + warp; item < i1; item += nw) {
+    const int b = item / g.P, q = item - b * g.P;
+    const int w = p.wl ? p.wl[b] : 0;
+    const int pl = q * g.L + w;
+    // ------------------------------------------- load W (planar [Re | Im][r][c]) -> buf[c][r]
+    const float* src = win + (size_t)(item - i0) * 2 * kN * kN;
+#pragma unroll 4
+    for (int i = lane; i < kN * kN; i += 32) {
+      const int r = i / kN, c = i - kN * r;
+      buf[c * kPC + r] = make_float2(__ldg(src + i), __ldg(src + kN * kN + i));
+    }
+    __syncwarp();
+    // ---------------------------------------- inverse DFT along r (y): 42 columns, prime-factor 6 x 7
+    pfa_pass6<kPC, 1>(buf, lane);
+    __syncwarp();
+    pfa_pass7<kPC, 1>(buf, lane);
+    __syncwarp();
+    // ---------------------------------------------- along c (x): 42 rows (positions), then epilogue
+    pfa_pass6<1, kPC>(buf, lane);
+    __syncwarp();
+    float2 bc = make_float2(1.f, 0.f);
+    if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
+    const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * kN * kN : nullptr;
+    const float2* ex = p.t.rem_x + pl * kN;
+    const float2* ey = p.t.rem_y + pl * kN;
+    float lmax = 0.f;
+    for (int t = lane; t < kN * 6; t += 32) {   // last pass: DFT-7 along x with the removal phase fused
+      const int pr = t / 6, k1 = t - 6 * pr;    // pr: position of the row (natural y below)
+      const int y = (7 * (pr % 6) + 36 * ((6 * pr) % 7)) % kN;
+      float2 v[7];
+#pragma unroll
+      for (int n2 = 0; n2 < 7; ++n2) v[n2] = buf[pfa_in(k1, n2) * kPC + pr];
+      dft7<true>(v);
+      const float2 eyq = __ldg(&ey[y]);
+#pragma unroll
+      for (int k2 = 0; k2 < 7; ++k2) {
+        const int x = (7 * k1 + 36 * k2) % kN;
+        float2 o = cmul(cmul(v[k2], eyq), __ldg(&ex[x]));   // same operation order as ct_stage_final_rows
+        if (p.bcal) o = cmul(o, bc);
+        if (rc) o = cmul(o, __ldg(&rc[y * kN + x]));   // reference calibration (engine.py:250-255)
+        lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
+        buf[pfa_in(k1, k2) * kPC + pr] = o;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    __syncwarp();
+    const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;   // pipeline.py:194-198
+    // ----------------------------------------------------------- int16 packing, natural [y][x]
+    uint32_t* fro = reinterpret_cast<uint32_t*>(p.fr + (size_t)item * kN * kN);
+    uint32_t* fio = reinterpret_cast<uint32_t*>(p.fi + (size_t)item * kN * kN);
+    for (int i = lane; i < kN * kN / 2; i += 32) {
+      const int y = i / (kN / 2), x = 2 * (i - y * (kN / 2));
+      const int py = pfa_pos(y);
+      const float2 v0 = buf[pfa_pos(x) * kPC + py], v1 = buf[pfa_pos(x + 1) * kPC + py];
+      if (p.raw) {
+        p.raw[(size_t)item * kN * kN + y * kN + x] = v0;
+        p.raw[(size_t)item * kN * kN + y * kN + x + 1] = v1;
+      }
+      const int r0 = __float2int_rn(__fmul_rn(v0.x, scale)), m0 = __float2int_rn(__fmul_rn(v0.y, scale));
+      const int r1 = __float2int_rn(__fmul_rn(v1.x, scale)), m1 = __float2int_rn(__fmul_rn(v1.y, scale));
+      fro[i] = (uint32_t)(r0 & 0xffff) | ((uint32_t)r1 << 16);
+      fio[i] = (uint32_t)(m0 & 0xffff) | ((uint32_t)m1 << 16);
+      fq[y * kN + x] = (uint32_t)(r0 & 0xffff) | ((uint32_t)m0 << 16);
+      fq[y * kN + x + 1] = (uint32_t)(r1 & 0xffff) | ((uint32_t)m1 << 16);
+    }
+    if (lane == 0) p.scale[item] = scale;
+    if (G == 0) {
+      __syncwarp();
+      continue;
+    }
+    __syncwarp();
+    // --------------------------------------------------------------------- HG overlap (SIMT)
+    // U[y][m] = sum_x Fq[y][x] hx[m][x] on the integer-valued field; the dequantisation 1/scale
+    // (engine.py:367-369) is applied once per coefficient.
+    const float* hxT = basis + q * 2 * kN * GP;   // [x][GP]
+    const float* hyT = hxT + kN * GP;              // [y][GP]
+    float2* U = buf;                                // [y][GP]
+    const int GQ = GP >> 2;
+    constexpr int CX = kN / 2, NPX = kN - 1 - CX;  // parity around the axis origin x = 21
+    const bool xsym = (ft.hsym >> (2 * q)) & 1, ysym = (ft.hsym >> (2 * q + 1)) & 1;
+    for (int t = lane; t < kN * GQ; t += 32) {
+      const int y = t / GQ, mq = t - y * GQ;
+      const uint32_t* row = fq + y * kN;
+      float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
+      if (xsym) {   // h_m(c - d) = (-1)^m h_m(c + d): orders 4mq, 4mq+2 take sums, 4mq+1, 4mq+3 differences
+#pragma unroll 4
+        for (int dd = 1; dd <= NPX; ++dd) {
+          const uint32_t a = row[CX + dd], c = row[CX - dd];
+          const float ar_ = (float)(int16_t)(a & 0xffff), ai_ = (float)(int16_t)(a >> 16);
+          const float cr_ = (float)(int16_t)(c & 0xffff), ci_ = (float)(int16_t)(c >> 16);
+          const float sr = ar_ + cr_, si = ai_ + ci_, dr = ar_ - cr_, di = ai_ - ci_;
+          const float4 h = *reinterpret_cast<const float4*>(&hxT[(CX + dd) * GP + 4 * mq]);
+          ar.x = fmaf(sr, h.x, ar.x); ai.x = fmaf(si, h.x, ai.x);
+          ar.y = fmaf(dr, h.y, ar.y); ai.y = fmaf(di, h.y, ai.y);
+          ar.z = fmaf(sr, h.z, ar.z); ai.z = fmaf(si, h.z, ai.z);
+          ar.w = fmaf(dr, h.w, ar.w); ai.w = fmaf(di, h.w, ai.w);
+        }
+#pragma unroll
+        for (int k = 0; k < 1 + (CX - NPX); ++k) {   // the origin, and x = 0 (even width)
+          const int x = k == 0 ? CX : 0;
+          const uint32_t a = row[x];
+          const float vr = (float)(int16_t)(a & 0xffff), vi = (float)(int16_t)(a >> 16);
+          const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+          ar.x = fmaf(vr, h.x, ar.x); ai.x = fmaf(vi, h.x, ai.x);
+          ar.y = fmaf(vr, h.y, ar.y); ai.y = fmaf(vi, h.y, ai.y);
+          ar.z = fmaf(vr, h.z, ar.z); ai.z = fmaf(vi, h.z, ai.z);
+          ar.w = fmaf(vr, h.w, ar.w); ai.w = fmaf(vi, h.w, ai.w);
+        }
+      } else {
+#pragma unroll 6
+        for (int x = 0; x < kN; ++x) {
+          const uint32_t a = row[x];
+          const float vr = (float)(int16_t)(a & 0xffff), vi = (float)(int16_t)(a >> 16);
+          const float4 h = *reinterpret_cast<const float4*>(&hxT[x * GP + 4 * mq]);
+          ar.x = fmaf(vr, h.x, ar.x); ai.x = fmaf(vi, h.x, ai.x);
+          ar.y = fmaf(vr, h.y, ar.y); ai.y = fmaf(vi, h.y, ai.y);
+          ar.z = fmaf(vr, h.z, ar.z); ai.z = fmaf(vi, h.z, ai.z);
+          ar.w = fmaf(vr, h.w, ar.w); ai.w = fmaf(vi, h.w, ai.w);
+        }
+      }
+      float2* u = U + y * GP + 4 * mq;
+      u[0] = make_float2(ar.x, ai.x);
+      u[1] = make_float2(ar.y, ai.y);
+      u[2] = make_float2(ar.z, ai.z);
+      u[3] = make_float2(ar.w, ai.w);
+    }
+    __syncwarp();
+    const float d = __fdiv_rn(g.dxdy[q], scale);
+    float2* out = p.coefs + (size_t)item * g.M;
+    constexpr int CY = kN / 2, NPY = kN - 1 - CY;
+    for (int i = lane; i < g.M; i += 32) {
+      const int m = p.t.mode_m[i], n = p.t.mode_n[i];
+      float ax = 0.f, ay = 0.f;
+      if (ysym) {
+        const float sg = (n & 1) ? -1.f : 1.f;
+#pragma unroll 4
+        for (int dd = 1; dd <= NPY; ++dd) {
+          const float2 vp = U[(CY + dd) * GP + m], vm = U[(CY - dd) * GP + m];
+          const float hv = hyT[(CY + dd) * GP + n];
+          ax = fmaf(fmaf(sg, vm.x, vp.x), hv, ax);
+          ay = fmaf(fmaf(sg, vm.y, vp.y), hv, ay);
+        }
+#pragma unroll
+        for (int k = 0; k < 1 + (CY - NPY); ++k) {
+          const int y = k == 0 ? CY : 0;
+          const float2 v = U[y * GP + m];
+          const float hv = hyT[y * GP + n];
+          ax = fmaf(v.x, hv, ax);
+          ay = fmaf(v.y, hv, ay);
+        }
+      } else {
+#pragma unroll 6
+        for (int y = 0; y < kN; ++y) {
+          const float2 v = U[y * GP + m];
+          const float hv = hyT[y * GP + n];
+          ax = fmaf(v.x, hv, ax);
+          ay = fmaf(v.y, hv, ay);
+        }
+      }
+      out[i] = make_float2(ax * d, ay * d);
+    }
+    __syncwarp();
+  }
+}
+
+bool tail_supported(const Geometry& g) {
+  return g.wh == kN && g.ww == kN && g.gh == kN && g.gw == kN && g.G <= 48 &&
+         tail_layout(g.G, g.P).total <= 227 * 1024;
+}
+
+cudaError_t launch_tail(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s, int i0, int i1,
+                        const float* win) {
+  const TailLayout L = tail_layout(p.coefs ? p.g.G : 0, p.g.P);
+  cudaError_t e = ensure_smem_optin((const void*)tail42_kernel, (size_t)L.total);
+  if (e != cudaSuccess) return e;
+  const int n = i1 - i0;
+  const int grid = std::max(1, std::min((n + kTailWarps - 1) / kTailWarps, num_sms));
+  tail42_kernel<<<grid, kTailWarps * 32, L.total, s>>>(p, ft, i0, i1, win, L);
+  return cudaGetLastError();
+}
+
+}  // namespace holo

@@ -1,24 +1,25 @@
 // Two-kernel tensor-core path for the 128-window / 42x42 geometry (sm_100a).
 //
-// K1  fourier128_tc2_kernel   frames -> masked, recentred Fourier window W (42 x 42)
+// K1  fourier128_tc2_kernel   frames -> masked, recentred Fourier window W (42 x 42), planar
 //     Both DFTs of the crop are GEMMs on the 5th-generation tensor cores:
-//       row DFT     D1[n][y]   = sum_x A1[n][x] f[y][x]          M=128 N=128 K=128
+//       row DFT     D1[n][y]   = sum_x A1[n][x] f[y][x]          M=128 N=64 (per half) K=128
 //                   A1 = [Re; Im] exp(-2 pi i kx_c (x - xi_x + nx/2)/nx)   (recentring folded in)
-//       column DFT  D2a[m][c]  = sum_y A2[m][y] Re R[y][c]        M=128 N=48  K=128
-//                   D2b[m][c]  = sum_y A2[m][y] Im R[y][c]
-//                   A2 = [Cr; Ci], C[r][y] = exp(-2 pi i ky_r (y - xi_y + ny/2)/ny)
+//       column DFT  D2[m][c']  = sum_y A2[m][y] B2[c'][y]        M=128 N=96 K=128 (two K halves)
+//                   A2 = [Cr; Ci], C[r][y] = exp(-2 pi i ky_r (y - xi_y + ny/2)/ny), B2 = [Re R | Im R]
 //       W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr), masked (holopipe/pipeline.py:72-127)
-//     fp32-class precision from fp16 hi/lo operand splits (3 products, fp32
-//     accumulation) with exact power-of-two scalings.  TMEM (512 columns):
-//       A1 hi|lo [0,128)  A2 hi|lo [128,256)  D1 [256,384)  D2a [384,432)  D2b [432,480)
-//     Warp-specialised: warps 0-3 stream windows (per-row power-of-two scale, fp16
-//     split, double-buffered stage) and issue the row GEMM; warps 4-11 drain D1
-//     into the column GEMM's operand, issue it, and drain D2 into W.
-// K2  field128_kernel         W -> 42x42 IFFT, removal phase, calibrations, int16
-//     packing, HG overlap (the SIMT tail of holo_fast.cu; holopipe/pipeline.py:130-199,
-//     holopipe/hgbasis.py:101-116).
-// W lives in the workspace between the two launches; batches are processed in
-// chunks small enough for W to stay resident in L2.
+//     fp32-class precision from fp16 hi/lo operand splits (3 products, fp32 accumulation) with exact
+//     power-of-two scalings (per-row for the row DFT operand, per-window for the column operand).
+//     TMEM (512 columns): A1 hi|lo [0,128)  A2 hi|lo [128,256)  D1 [256,384)  D2 [384,480).
+//     Warp roles (one CTA per SM, persistent, every CTA owns one pol):
+//       warps 0-7   producers: landed half window -> per-row 2^k scale -> fp16 hi/lo row-DFT operand
+//       warp  8     MMA issuer: S1(k,0) S1(k,1) | S2(k,0) S1(k+1,0) S2(k,1) S1(k+1,1) | ...
+//       warp  9     TMA issuer: half windows into a 3-slot landing ring (two halves ahead)
+//       warps 10-17 consumers: D1 half -> column operand B2 (K-major, scaled to a common exponent);
+//                   D2 -> W through a one-sided exchange, the consumer draining the next window's first
+//                   D1 half while the column GEMM of this window still runs
+// K2  tail (holo_tail.cu, or field128_kernel below): W -> 42x42 IFFT, removal phase, calibrations,
+//     int16 packing, HG overlap.  W lives in the workspace between the two launches; batches are
+//     processed in chunks small enough for W to stay resident in L2.
 #include <cuda.h>
 #include <cuda_fp16.h>
 
@@ -35,34 +36,30 @@ namespace {
 
 constexpr int kProd2 = 256;                 // producer threads (warps 0-7)
 constexpr int kMmaWarp = 8;                 // tcgen05.mma issuer
-constexpr int kCons2 = 256;                 // consumer threads (warps 9-16)
-constexpr int kConsWarp0 = kMmaWarp + 1;
-constexpr int kK1Threads = kProd2 + 32 + kCons2;
+constexpr int kTmaWarp = 9;                 // TMA issuer
+constexpr int kConsWarp0 = 10;              // consumers: warps 10-17
+constexpr int kCons2 = 256;
+constexpr int kK1Threads = kProd2 + 64 + kCons2;
 constexpr int kBarProd2 = 1, kBarCons2 = 2;
 constexpr int kN2 = 48;                     // column-DFT N per real part (42 columns, padded)
 constexpr int kWinW = 42, kWinH = 42;
+constexpr int kSlots = 3;                   // landing ring: half windows
 
 // dynamic shared memory (bytes)
 constexpr uint32_t kBox = 4096;                    // TMA box: 32 rows x 128 B (32 f32 / 64 u16), 128B swizzle
-constexpr uint32_t kLand = 0;                      // [chunk 4][box 4] = one window
-constexpr uint32_t kStage = 16 * kBox;             // [half][hi 16 KB | lo 16 KB]
+constexpr uint32_t kSlot = 8 * kBox;               // one half window: [chunk 2][box 4]
+constexpr uint32_t kLand = 0;                      // [slot 3][half window]
+constexpr uint32_t kStage = kSlots * kSlot;        // [half][hi 16 KB | lo 16 KB]
 constexpr uint32_t kStageHalf = 32768;
-// Data operands are split hi + lo as well: rounding the window samples to fp16 alone (2 products per
-// K-step instead of 3, period 8.1 K -> 6.2 K cycles) leaves field errors of 5.8e-4 relative L2 on the
-// dual-pol fixtures, above the 1e-4 parity bar (HOLO_TC2_DATA_LO=0 builds that variant).
-#ifndef HOLO_TC2_DATA_LO
-#define HOLO_TC2_DATA_LO 1
-#endif
-constexpr bool kDataLo = HOLO_TC2_DATA_LO;
 constexpr uint32_t kB2 = kStage + 2 * kStageHalf;  // B2 hi | B2 lo: rows c (Re R), 48 + c (Im R)
 constexpr uint32_t kB2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
-constexpr uint32_t kXP = 88;                       // drain-2 exchange X[acc][c][rho] pitch (floats)
+constexpr uint32_t kXP = 97;                       // exchange pitch (floats): Ci-row products [r][96]
 constexpr uint32_t kX = kB2 + 2 * kB2Part;
-constexpr uint32_t kFac = kX + 2 * kN2 * kXP * 4;  // fac[2][128] f32
+constexpr uint32_t kFac = (kX + kWinH * kXP * 4 + 15) & ~15u;   // fac[2][128] f32 (16-byte aligned)
 constexpr uint32_t kErow = kFac + 2 * 128 * 4;     // e_row[128] int
 constexpr uint32_t kCr = kErow + 128 * 4;          // crange[42][2] int
-constexpr uint32_t kK1Bytes = kCr + 2 * 64 * 4;
-static_assert(kK1Bytes <= 227 * 1024, "K1 shared memory");
+constexpr uint32_t kK1Bytes = kCr + 2 * 48 * 4;
+static_assert(kK1Bytes <= 227 * 1024 - 512, "K1 shared memory");
 
 // canonical K-major, no-swizzle operand layout: [kstep][row/8][khalf][row%8][8 halves]
 HOLO_DEV uint32_t kmaj_off(int row, int k, int ngroups) {
@@ -74,34 +71,43 @@ HOLO_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
+// frexp exponent of a finite positive float (m = f 2^e, f in [0.5, 1)); -1000 for 0 / subnormal
+HOLO_DEV int exp_of(float m) {
+  const int b = (__float_as_int(m) >> 23) & 0xff;
+  return b == 0 ? -1000 : b - 126;
+}
+HOLO_DEV float pow2f(int e) { return __int_as_float((e + 127) << 23); }   // 2^e, -126 <= e <= 127
+
+// {a, b} -> f16x2 (a in the low half), one F2FP
+HOLO_DEV uint32_t f16x2(float a, float b) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(b), "f"(a));
+  return d;
+}
+// exact split of two floats into fp16 hi + lo: hi keeps the top 11 significant bits (exact in fp16 for
+// |v| in the fp16 normal range, which the power-of-two scalings guarantee for every significant value),
+// lo = v - hi is exact in fp32 and rounded once to fp16 (22 significant bits in hi + lo)
+HOLO_DEV void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const float ha = __uint_as_float(__float_as_uint(a) & 0xffffe000u);
+  const float hb = __uint_as_float(__float_as_uint(b) & 0xffffe000u);
+  hi = f16x2(ha, hb);
+  lo = f16x2(a - ha, b - hb);
+}
+
 }  // namespace
 
 // Phase timestamps of CTA 0 (clock64), for tools/tc2_trace.py (hpg_debug_trace).
-__device__ long long g_tc2_trace[2][64][8];
+__device__ long long g_tc2_trace[3][64][8];
 #define TC2_MARK(role, kk, ev)                                                   \
   do {                                                                           \
     if (blockIdx.x == 0 && (kk) < 64) g_tc2_trace[role][kk][ev] = clock64();     \
   } while (0)
 
-// TMA (tensor map over the frame buffer [F][H][W]) of half h of an item's window:
-// chunks 2h, 2h+1 (32 rows each) x 4 boxes of 128 bytes per row, one thread.
-// W = (CrRr - CiRi) + i (CrRi + CiRr), masked, from the drain-2 exchange; thread -> column wc, rows wr0 + 6t
-HOLO_DEV void write_w(const float* X, float2* wo, int wc, int wr0, int wlo, int whi, float gs) {
-  if (wc >= kWinW) return;
-  wo += wc * kWinH;   // column-major [c][r]
-  const float* xa = X + wc * kXP;
-  const float* xb = X + kN2 * kXP + wc * kXP;
-#pragma unroll
-  for (int t = 0; t < 7; ++t) {
-    const int r = wr0 + 6 * t;
-    float2 w = make_float2(0.f, 0.f);
-    if (r >= wlo && r <= whi) w = make_float2((xa[r] - xb[kWinH + r]) * gs, (xb[r] + xa[kWinH + r]) * gs);
-    wo[r] = w;
-  }
-}
-
+// TMA (tensor map over the frame buffer [F][H][W]) of half h of an item's window into landing slot
+// `slot`: two 32-row chunks x 4 boxes of 128 bytes per row, issued by one thread.
 template <int FMT>
-HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, int h, char* smem, uint64_t* bar) {
+HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, int h, char* smem, int slot,
+                         uint64_t* bar) {
   const Geometry& g = p.g;
   const int b = item / g.P, q = item - b * g.P;
   constexpr int bw = FMT == 0 ? 32 : 64;   // box width in elements (128 bytes)
@@ -111,7 +117,7 @@ HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, 
   for (int jj = 0; jj < 2; ++jj) {
     const int j = 2 * h + jj;
     for (int qx = 0; qx < nbox; ++qx) {
-      const uint32_t dst = smem_u32(smem + kLand + (j * 4 + qx) * kBox);
+      const uint32_t dst = smem_u32(smem + kLand + slot * kSlot + (jj * 4 + qx) * kBox);
       asm volatile(
           "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
           "l"(reinterpret_cast<uint64_t>(tmap)), "r"(g.col0[q] + qx * bw), "r"(g.row0[q] + 32 * j), "r"(b),
@@ -121,17 +127,18 @@ HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, 
   }
 }
 
+// wout: [items][2][42 r][42 c] float (Re plane, Im plane) of the masked window, relative to item i0
 template <int FMT>
 __global__ void __launch_bounds__(kK1Threads, 1)
     fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft,
-                          const __grid_constant__ CUtensorMap tmap, int i0, int i1, float2* __restrict__ wout) {
+                          const __grid_constant__ CUtensorMap tmap, int i0, int i1, float* __restrict__ wout) {
   extern __shared__ __align__(1024) char smem[];
-  // lfull[j]: landing chunk j arrived; staged[h]: stage half h ready; meta[s]: fac[s] ready;
-  // mma1[h]: row GEMM half h done; b2ready[h]: D1 half h drained into B2 (D1 half h free);
-  // stfree[h]: stage half h consumed; full2: column GEMM done; d2free: D2 drained;
-  // facfree[s]: fac[s] consumed
-  __shared__ __align__(8) uint64_t lfull[2], staged[2], meta[2], mma1[2], b2ready[2], stfree[2], full2, d2free,
-      facfree[2];
+  // landfull/landfree[slot]: TMA ring; staged[h]: stage half h written; stfree[h]: row GEMM half h done with
+  // it; meta[s]: fac[s] ready; facfree[s]: fac[s] consumed; d1full[h]: row GEMM half h done; b2ready[h]: D1
+  // half h drained into B2 half h (D1 half h free); b2free[h]: column GEMM K-half h done with B2 half h;
+  // d2full: column GEMM done; d2free: D2 drained
+  __shared__ __align__(8) uint64_t landfull[kSlots], landfree[kSlots], staged[2], stfree[2], meta[2], facfree[2],
+      d1full[2], b2ready[2], b2free[2], d2full, d2free;
   __shared__ uint32_t tbase;
   __shared__ int emaxw[8];
   __shared__ int emaxs[2];
@@ -140,22 +147,29 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   int* crs = reinterpret_cast<int*>(smem + kCr);
   const Geometry& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int first = i0 + blockIdx.x;
+  const int nk = first < i1 ? (i1 - first + gridDim.x - 1) / gridDim.x : 0;   // windows of this CTA
+  const int q = first % g.P;   // gridDim.x and i0 are multiples of P: one pol per CTA
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) mbar_init(&lfull[i], 1);
+    for (int i = 0; i < kSlots; ++i) {
+      mbar_init(&landfull[i], 1);
+      mbar_init(&landfree[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&staged[i], 1);
-      mbar_init(&meta[i], 1);
-      mbar_init(&mma1[i], 1);
-      mbar_init(&b2ready[i], 1);
       mbar_init(&stfree[i], 1);
+      mbar_init(&meta[i], 1);
       mbar_init(&facfree[i], 1);
+      mbar_init(&d1full[i], 1);
+      mbar_init(&b2ready[i], 1);
+      mbar_init(&b2free[i], 1);
     }
-    mbar_init(&full2, 1);
+    mbar_init(&d2full, 1);
     mbar_init(&d2free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -165,62 +179,58 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   tc_fence_after();
   const uint32_t tm = tbase;
   const uint32_t tA1 = tm, tA2 = tm + 128, tD1 = tm + 256, tD2 = tm + 384;
+  {   // constant DFT matrices of this CTA's pol into TMEM: A1 by warps 0-3, A2 by warps 4-7
+    const int part_warp = warp & 3;
+    if (warp < 8 && nk > 0) {
+      const uint32_t* src = (warp < 4 ? ft.a_tc : ft.a2_tc) + ((size_t)q * 2 * 128 + part_warp * 32 + lane) * 64;
+      const uint32_t dst = (warp < 4 ? tA1 : tA2) + ((uint32_t)(part_warp * 32) << 16);
+      uint32_t r[32];
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t* s2 = src + (size_t)part * 128 * 64 + hh * 32;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
+          tmem_st32(dst + part * 64 + hh * 32, r);
+        }
+      }
+      tmem_wait_st();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp < kMmaWarp) {
-    // ================================= producer =================================
+    // ================================= producers =================================
     const int r8 = lane & 7, gq = lane >> 3;   // row within the warp's 8, octet group
-    int loaded_q = -1;
-    if (tid == 0 && i0 + (int)blockIdx.x < i1)
-      for (int h = 0; h < 2; ++h) issue_half<FMT>(p, &tmap, i0 + blockIdx.x, h, smem, &lfull[h]);
-    int k = 0;
-    for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
+    for (int k = 0; k < nk; ++k) {
       const int s = k & 1;
-      const int q = item % g.P;
-      const int nitem = item + gridDim.x;
-      if (tid == 0) TC2_MARK(0, k, 0);
-      if (q != loaded_q) {   // A1 of this pol; the previous window's row GEMM must be done with it
-        if (k >= 1) mbar_wait_warp(&stfree[1], (k - 1) & 1);
-        tc_fence_after();
-        if (warp < 4) {
-          const uint32_t* src = ft.a_tc + ((size_t)q * 2 * 128 + warp * 32 + lane) * 64;
-          uint32_t r[32];
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const uint32_t* s2 = src + (size_t)part * 128 * 64 + hh * 32;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
-              tmem_st32(tA1 + ((uint32_t)(warp * 32) << 16) + part * 64 + hh * 32, r);
-            }
-          }
-          tmem_wait_st();
-        }
-        loaded_q = q;
-      }
       int emax_t = -1000;
-#pragma unroll
+#pragma unroll 1
       for (int h = 0; h < 2; ++h) {   // half h = rows 64h..64h+63; warp w -> rows 64h + 8w + r8
-        if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done
-        if (tid == 0 && h == 0) TC2_MARK(0, k, 1);
-        mbar_wait_warp(&lfull[h], k & 1);
-        if (tid == 0 && h == 0) TC2_MARK(0, k, 6);
-        if (tid == 0 && h == 1) TC2_MARK(0, k, 7);
+        const int jh = 2 * k + h, slot = jh % kSlots;
+        if (tid == 0) TC2_MARK(0, k, 4 * h + 0);
+        if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done with the stage
+        if (tid == 0) TC2_MARK(0, k, 4 * h + 1);
+        mbar_wait_warp(&landfull[slot], (jh / kSlots) & 1);
+        if (tid == 0) TC2_MARK(0, k, 4 * h + 2);
         const int yl = 8 * warp + r8, y = 64 * h + yl;
-        const int j = y >> 5, rb = y & 31;   // chunk, row in box
+        const int jj = yl >> 5, rb = y & 31;   // chunk within the half, row in box
         float v[32];   // octets o = gq + 4 i, i = 0..3
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int o = gq + 4 * i;
           if (FMT == 0) {   // f32: box qx = o / 4, 16-byte chunks 2(o%4), 2(o%4)+1, swizzled by row
-            const char* box = smem + kLand + (j * 4 + (o >> 2)) * kBox + rb * 128;
+            const char* box = smem + kLand + slot * kSlot + (jj * 4 + (o >> 2)) * kBox + rb * 128;
             const int c0 = (2 * (o & 3)) ^ (rb & 7), c1 = (2 * (o & 3) + 1) ^ (rb & 7);
             const float4 a = *reinterpret_cast<const float4*>(box + c0 * 16);
             const float4 c = *reinterpret_cast<const float4*>(box + c1 * 16);
             v[8 * i + 0] = a.x; v[8 * i + 1] = a.y; v[8 * i + 2] = a.z; v[8 * i + 3] = a.w;
             v[8 * i + 4] = c.x; v[8 * i + 5] = c.y; v[8 * i + 6] = c.z; v[8 * i + 7] = c.w;
           } else {            // u16: box qx = o / 8, one 16-byte chunk o%8
-            const char* box = smem + kLand + (j * 4 + (o >> 3)) * kBox + rb * 128;
+            const char* box = smem + kLand + slot * kSlot + (jj * 4 + (o >> 3)) * kBox + rb * 128;
             const uint4 a = *reinterpret_cast<const uint4*>(box + (((o & 7) ^ (rb & 7)) * 16));
             const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
@@ -236,10 +246,8 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
         // exact power-of-two row scale: |f| * sc < 2^14, fh + fl keep 22 bits
-        int e2 = 0;
-        frexpf(m, &e2);
-        const float sc = m > 0.f ? ldexpf(1.f, 14 - e2) : 1.f;
-        const int ey = m > 0.f ? e2 : -1000;
+        const int ey = exp_of(m);
+        const float sc = ey > -1000 ? pow2f(14 - ey) : 1.f;
         if (gq == 0) erow[y] = ey;
         emax_t = max(emax_t, ey);
         char* st = smem + kStage + h * kStageHalf;
@@ -248,26 +256,19 @@ __global__ void __launch_bounds__(kK1Threads, 1)
           const uint32_t off = kmaj_off(yl, 8 * (gq + 4 * i), 8);
           uint32_t hi2[4], lo2[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float a = v[8 * i + 2 * e] * sc, c = v[8 * i + 2 * e + 1] * sc;
-            hi2[e] = pack_h2(a, c);
-            if (kDataLo) {
-              const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi2[e]));
-              lo2[e] = pack_h2(a - back.x, c - back.y);
-            }
-          }
+          for (int e = 0; e < 4; ++e) split2(v[8 * i + 2 * e] * sc, v[8 * i + 2 * e + 1] * sc, hi2[e], lo2[e]);
           *reinterpret_cast<uint4*>(st + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-          if (kDataLo) *reinterpret_cast<uint4*>(st + 16384 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+          *reinterpret_cast<uint4*>(st + 16384 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
         }
         fence_async_smem();
         tc_fence_before();
-        nbar(kBarProd2, kProd2);   // half h consumed: landing free, stage half written
+        nbar(kBarProd2, kProd2);   // half h consumed: landing slot free, stage half written
+        if (tid == 0) TC2_MARK(0, k, 4 * h + 3);
         if (tid == 0) {
           mbar_arrive(&staged[h]);
-          if (nitem < i1) issue_half<FMT>(p, &tmap, nitem, h, smem, &lfull[h]);
+          mbar_arrive(&landfree[slot]);
         }
       }
-      if (tid == 0) TC2_MARK(0, k, 2);
 #pragma unroll
       for (int o = 16; o; o >>= 1) emax_t = max(emax_t, __shfl_xor_sync(0xffffffffu, emax_t, o));
       if (lane == 0) emaxw[warp] = emax_t;
@@ -277,178 +278,170 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         int em = emaxw[0];
 #pragma unroll
         for (int j = 1; j < 8; ++j) em = max(em, emaxw[j]);
-        const int ey = erow[tid];
-        fac[s * 128 + tid] = ey > -1000 ? ldexpf(1.f, ey - em - 6) : 0.f;
+        const int e = erow[tid];
+        fac[s * 128 + tid] = e > -1000 ? pow2f(e - em - 6) : 0.f;
         if (tid == 0) emaxs[s] = em;
       }
       nbar(kBarProd2, kProd2);
-      if (tid == 0) {
-        mbar_arrive(&meta[s]);
-        TC2_MARK(0, k, 3);
+      if (tid == 0) mbar_arrive(&meta[s]);
+    }
+  } else if (warp == kTmaWarp) {
+    // ================================ TMA issuer ================================
+    if (lane == 0) {
+      for (int jh = 0; jh < 2 * nk; ++jh) {
+        const int slot = jh % kSlots;
+        if (jh >= kSlots) mbar_wait(&landfree[slot], ((jh / kSlots) - 1) & 1);
+        issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, slot, &landfull[slot]);
       }
     }
   } else if (warp == kMmaWarp) {
     // ================================ MMA issuer ================================
     const uint32_t idesc1 = idesc_f16(128, 64), idesc2 = idesc_f16(128, 2 * kN2);
-    int k = 0;
-    for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {   // row GEMM, half h: D1[:, 64h .. 64h+63]
-        mbar_wait_warp(&staged[h], k & 1);
-        if (k >= 1) mbar_wait_warp(&b2ready[h], (k - 1) & 1);   // D1 half h drained
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sb = smem_u32(smem + kStage + h * kStageHalf);
+    auto row_gemm = [&](int k, int h) {   // D1[:, 64h .. 64h+63] = A1 * stage half h
+      mbar_wait_warp(&staged[h], k & 1);
+      if (k >= 1) mbar_wait_warp(&b2ready[h], (k - 1) & 1);   // D1 half h of k-1 drained
+      if (lane == 0) TC2_MARK(2, k, 2 * h);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sb = smem_u32(smem + kStage + h * kStageHalf);
 #pragma unroll
-          for (int gk = 0; gk < 8; ++gk) {
-            const uint64_t bh = umma_desc(sb + gk * 2048, 128, 256);
-            const uint64_t bl = umma_desc(sb + 16384 + gk * 2048, 128, 256);
-            mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bh, idesc1, gk != 0);
-            mma_f16_ts(tD1 + 64 * h, tA1 + 64 + gk * 8, bh, idesc1, 1);
-            if (kDataLo) mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bl, idesc1, 1);
-          }
-          tc_commit(&mma1[h]);
-          tc_commit(&stfree[h]);
-          if (h == 1) TC2_MARK(0, k, 4);
+        for (int gk = 0; gk < 8; ++gk) {
+          const uint64_t bh = umma_desc(sb + gk * 2048, 128, 256);
+          const uint64_t bl = umma_desc(sb + 16384 + gk * 2048, 128, 256);
+          mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bh, idesc1, gk != 0);
+          mma_f16_ts(tD1 + 64 * h, tA1 + 64 + gk * 8, bh, idesc1, 1);
+          mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bl, idesc1, 1);
         }
-        __syncwarp();
+        tc_commit(&stfree[h]);
+        tc_commit(&d1full[h]);
+        TC2_MARK(2, k, 2 * h + 1);
       }
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {   // column GEMM, K-half h (y = 64h .. 64h+63), N = 96
-        mbar_wait_warp(&b2ready[h], k & 1);
-        if (h == 0 && k >= 1) mbar_wait_warp(&d2free, (k - 1) & 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t sb = smem_u32(smem + kB2);
+      __syncwarp();
+    };
+    auto col_gemm = [&](int k, int h) {   // D2 (+)= A2[:, K-half h] * B2 half h, N = 96
+      mbar_wait_warp(&b2ready[h], k & 1);
+      if (h == 0 && k >= 1) mbar_wait_warp(&d2free, (k - 1) & 1);
+      if (lane == 0) TC2_MARK(2, k, 4 + 2 * h);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sb = smem_u32(smem + kB2);
 #pragma unroll
-          for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {
-            const uint32_t o = ks * 3072;
-            const uint64_t rh = umma_desc(sb + o, 128, 256), rl = umma_desc(sb + kB2Part + o, 128, 256);
-            mma_f16_ts(tD2, tA2 + ks * 8, rh, idesc2, ks != 0);
-            mma_f16_ts(tD2, tA2 + 64 + ks * 8, rh, idesc2, 1);
-            if (kDataLo) mma_f16_ts(tD2, tA2 + ks * 8, rl, idesc2, 1);
-          }
-          if (h == 1) {
-            tc_commit(&full2);
-            TC2_MARK(0, k, 5);
-          }
+        for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {
+          const uint32_t o = ks * 3072;
+          const uint64_t rh = umma_desc(sb + o, 128, 256), rl = umma_desc(sb + kB2Part + o, 128, 256);
+          mma_f16_ts(tD2, tA2 + ks * 8, rh, idesc2, ks != 0);
+          mma_f16_ts(tD2, tA2 + 64 + ks * 8, rh, idesc2, 1);
+          mma_f16_ts(tD2, tA2 + ks * 8, rl, idesc2, 1);
         }
-        __syncwarp();
+        tc_commit(&b2free[h]);
+        if (h == 1) tc_commit(&d2full);
+        TC2_MARK(2, k, 5 + 2 * h);
       }
+      __syncwarp();
+    };
+    if (nk > 0) {
+      row_gemm(0, 0);
+      row_gemm(0, 1);
+    }
+    for (int k = 0; k < nk; ++k) {
+      col_gemm(k, 0);
+      if (k + 1 < nk) row_gemm(k + 1, 0);
+      col_gemm(k, 1);
+      if (k + 1 < nk) row_gemm(k + 1, 1);
     }
   } else {
-    // ================================= consumer =================================
-    const int ct = tid - kProd2 - 32, cw = warp - kConsWarp0, quarter = warp & 3, sub = cw >> 2;
+    // ================================= consumers =================================
+    const int ct = tid - kConsWarp0 * 32, cw = warp - kConsWarp0, quarter = warp & 3, sub = cw >> 2;
     char* b2 = smem + kB2;
     float* X = reinterpret_cast<float*>(smem + kX);
-    const int wc = ct / 6, wr0 = ct - 6 * wc;   // W pass: 42 columns x 6 row phases
-    const int wlo = wc < kWinW ? crs[2 * wc] : 0, whi = wc < kWinW ? crs[2 * wc + 1] : -1;
-    int loaded_q = -1, prev_item = 0;
-    float gs_prev = 0.f;
-    int k = 0;
-    for (int item = i0 + blockIdx.x; item < i1; item += gridDim.x, ++k) {
+    const int n = quarter * 32 + lane, c = n & 63;
+    const int brow = (n >= 64 ? kN2 : 0) + c;   // B2 row: Re R rows then Im R rows
+    auto drain_d1 = [&](int k, int h) {   // D1 half h of window k -> B2 half h (this warp: 32 of its 64 y)
       const int s = k & 1;
-      const int q = item % g.P;
-      if (q != loaded_q) {   // A2 of this pol (the previous column GEMM completed: waited full2 below)
-        if (sub == 0) {
-          const uint32_t* src = ft.a2_tc + ((size_t)q * 2 * 128 + quarter * 32 + lane) * 64;
-          uint32_t r[32];
-#pragma unroll
-          for (int part = 0; part < 2; ++part) {
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const uint32_t* s2 = src + (size_t)part * 128 * 64 + hh * 32;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
-              tmem_st32(tA2 + ((uint32_t)(quarter * 32) << 16) + part * 64 + hh * 32, r);
-            }
-          }
-          tmem_wait_st();
-        }
-        loaded_q = q;
-      }
-      if (ct == 0) TC2_MARK(1, k, 0);
-      mbar_wait_warp(&meta[s], (k >> 1) & 1);
-      // ------------------------------------------- drain D1 (by halves) -> B2
-      const int n = quarter * 32 + lane, c = n & 63;
-      const int brow = (n >= 64 ? kN2 : 0) + c;   // B2 row: Re R rows then Im R rows
-      const float* fs = fac + s * 128;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mbar_wait_warp(&mma1[h], k & 1);
-        tc_fence_after();
-        if (ct == 0 && h == 0) TC2_MARK(1, k, 1);
-        const int y0 = 64 * h + 32 * sub;
-        uint32_t r[32];
-        tmem_ld16(tD1 + ((uint32_t)(quarter * 32) << 16) + y0, r);
-        tmem_ld16(tD1 + ((uint32_t)(quarter * 32) << 16) + y0 + 16, r + 16);
-        tmem_wait_ld();
-        if (c < kN2) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {   // one 16-byte row chunk: y = y0 + 8j .. +7
-            uint32_t hi2[4], lo2[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f2 = *reinterpret_cast<const float2*>(fs + y0 + 8 * j + 2 * e);
-              const float a = __uint_as_float(r[8 * j + 2 * e]) * f2.x;
-              const float d = __uint_as_float(r[8 * j + 2 * e + 1]) * f2.y;
-              hi2[e] = pack_h2(a, d);
-              if (kDataLo) {
-                const float2 back = __half22float2(*reinterpret_cast<const __half2*>(&hi2[e]));
-                lo2[e] = pack_h2(a - back.x, d - back.y);
-              }
-            }
-            const uint32_t o = kmaj_off(brow, y0 + 8 * j, 2 * kN2 / 8);
-            *reinterpret_cast<uint4*>(b2 + o) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-            if (kDataLo) *reinterpret_cast<uint4*>(b2 + kB2Part + o) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
-          }
-        }
-        fence_async_smem();
-        tc_fence_before();
-        nbar(kBarCons2, kCons2);
-        if (ct == 0) {
-          mbar_arrive(&b2ready[h]);
-          if (h == 1) {
-            mbar_arrive(&facfree[s]);
-            TC2_MARK(1, k, 2);
-          }
-        }
-      }
-      const float gs = ldexpf(1.f, emaxs[s] - 8);
-      // W of the previous window while this window's column GEMM runs (X still holds its partials)
-      if (k >= 1) write_w(X, wout + (size_t)(prev_item - i0) * kWinH * kWinW, wc, wr0, wlo, whi, gs_prev);
-      nbar(kBarCons2, kCons2);   // X free for this window's drain
-      mbar_wait_warp(&full2, k & 1);
+      mbar_wait_warp(&d1full[h], k & 1);
+      if (k >= 1) mbar_wait_warp(&b2free[h], (k - 1) & 1);   // column GEMM of k-1 done with B2 half h
       tc_fence_after();
-      if (ct == 0) TC2_MARK(1, k, 3);
-
-      // ------------------------------------- drain D2 -> exchange X[acc][c][rho]
-      {
-        const int r = n & 63;
-        const uint32_t src = tD2 + (sub ? kN2 : 0) + ((uint32_t)(quarter * 32) << 16);
-        const int rho = n < 64 ? r : kWinH + r;   // compact row: Cr rows then Ci rows
-        float* xr = X + (size_t)sub * kN2 * kXP + rho;
-        uint32_t v[48];
-        tmem_ld16(src, v);
-        tmem_ld16(src + 16, v + 16);
-        tmem_ld16(src + 32, v + 32);
-        tmem_wait_ld();
-        if (r < kWinH) {
+      if (ct == 0) TC2_MARK(1, k, 2 * h);
+      const int y0 = 64 * h + 32 * sub;
+      uint32_t r[32];
+      tmem_ld32(tD1 + ((uint32_t)(quarter * 32) << 16) + y0, r);
+      tmem_wait_ld();
+      if (c < kN2) {
+        const float4* fs = reinterpret_cast<const float4*>(fac + s * 128 + y0);
 #pragma unroll
-          for (int cc = 0; cc < kWinW; ++cc) xr[cc * kXP] = __uint_as_float(v[cc]);
+        for (int j = 0; j < 4; ++j) {   // one 16-byte row chunk: y = y0 + 8j .. +7
+          const float4 fa = fs[2 * j], fb = fs[2 * j + 1];
+          const float f[8] = {fa.x, fa.y, fa.z, fa.w, fb.x, fb.y, fb.z, fb.w};
+          uint32_t hi2[4], lo2[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            split2(__uint_as_float(r[8 * j + 2 * e]) * f[2 * e], __uint_as_float(r[8 * j + 2 * e + 1]) * f[2 * e + 1],
+                   hi2[e], lo2[e]);
+          const uint32_t o = kmaj_off(brow, y0 + 8 * j, 2 * kN2 / 8);
+          *reinterpret_cast<uint4*>(b2 + o) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+          *reinterpret_cast<uint4*>(b2 + kB2Part + o) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
         }
       }
+      fence_async_smem();
       tc_fence_before();
       nbar(kBarCons2, kCons2);
       if (ct == 0) {
-        mbar_arrive(&d2free);
-        TC2_MARK(1, k, 4);
+        mbar_arrive(&b2ready[h]);
+        TC2_MARK(1, k, 2 * h + 1);
       }
-      prev_item = item;
-      gs_prev = gs;
+    };
+    // D2 -> W.  Lane r < 42 holds the Cr rows [Cr Rr | Cr Ri], lane 64 + r the Ci rows [Ci Rr | Ci Ri]
+    // (sub 0: the Re R products, sub 1: the Im R products).  The Ci rows go through X; the Cr-row
+    // threads form Wr = CrRr - CiRi (sub 0) and Wi = CrRi + CiRr (sub 1), mask, scale, store.
+    auto drain_d2 = [&](int k, float gs) {
+      mbar_wait_warp(&d2full, k & 1);
+      tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 5);
+      uint32_t v[48];
+      const uint32_t src = tD2 + (sub ? kN2 : 0) + ((uint32_t)(quarter * 32) << 16);
+      tmem_ld32(src, v);
+      tmem_ld16(src + 32, v + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      const int r = n & 63;
+      if (n >= 64 && r < kWinH) {
+        float* xr = X + r * kXP + sub * kN2;
+#pragma unroll
+        for (int cc = 0; cc < kWinW; ++cc) xr[cc] = __uint_as_float(v[cc]);
+      }
+      nbar(kBarCons2, kCons2);
+      if (ct == 0) mbar_arrive(&d2free);   // D2 is in registers / X: the next column GEMM may start
+      if (n < 64 && r < kWinH) {
+        const float* xr = X + r * kXP + (sub ? 0 : kN2);   // sub 0 needs Ci Ri, sub 1 needs Ci Rr
+        const float sg = sub ? 1.f : -1.f;
+        float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 2 + sub) * (kWinH * kWinW) + r * kWinW;
+#pragma unroll
+        for (int cc = 0; cc < kWinW; ++cc) {
+          const bool in = r >= crs[2 * cc] && r <= crs[2 * cc + 1];
+          wo[cc] = in ? fmaf(sg, xr[cc], __uint_as_float(v[cc])) * gs : 0.f;
+        }
+      }
+      nbar(kBarCons2, kCons2);   // X free for the next window
+      if (ct == 0) TC2_MARK(1, k, 6);
+    };
+    if (nk > 0) {
+      mbar_wait_warp(&meta[0], 0);
+      drain_d1(0, 0);
     }
-    if (k >= 1) write_w(X, wout + (size_t)(prev_item - i0) * kWinH * kWinW, wc, wr0, wlo, whi, gs_prev);
+    float gs = nk > 0 ? pow2f(emaxs[0] - 8) : 1.f;
+    for (int k = 0; k < nk; ++k) {
+      drain_d1(k, 1);   // ends with a consumer barrier: every thread is done with fac[k & 1]
+      if (ct == 0) mbar_arrive(&facfree[k & 1]);
+      float gs_next = 1.f;
+      if (k + 1 < nk) {
+        mbar_wait_warp(&meta[(k + 1) & 1], ((k + 1) >> 1) & 1);
+        if (ct == 0) TC2_MARK(1, k + 1, 4);
+        gs_next = pow2f(emaxs[(k + 1) & 1] - 8);
+        drain_d1(k + 1, 0);
+      }
+      drain_d2(k, gs);
+      gs = gs_next;
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -472,7 +465,7 @@ struct FieldLayout {
 
 template <int WH, int WW>
 __global__ void __launch_bounds__(256, 3)
-    field128_kernel(const __grid_constant__ RunParams p, int i0, int i1, const float2* __restrict__ win) {
+    field128_kernel(const __grid_constant__ RunParams p, int i0, int i1, const float* __restrict__ win) {
   using LY = FieldLayout<WH, WW>;
   extern __shared__ __align__(1024) char smem[];
   __shared__ float redf[8];
@@ -519,9 +512,14 @@ __global__ void __launch_bounds__(256, 3)
       staged_q = q;
     }
     __syncthreads();
-    const float2* Wt = win + (size_t)(item - i0) * WH * WW;   // column-major [c][r]
+    const float* Wp = win + (size_t)(item - i0) * 2 * WH * WW;   // planar [Re | Im][r][c]
+    for (int i = tid; i < WH * WW; i += blockDim.x) {            // -> F, column-major [c][r]
+      const int r = i / WW, c = i - r * WW;
+      F[c * WH + r] = make_float2(__ldg(Wp + i), __ldg(Wp + WH * WW + i));
+    }
+    __syncthreads();
     // IFFT along r (y) first, then along c (x)
-    ct_stage<6, WH, 1, WW, WH, 1, true>(Wt, T, twh);
+    ct_stage<6, WH, 1, WW, WH, 1, true>(F, T, twh);
     __syncthreads();
     ct_stage<7, WH, 6, WW, WH, 1, true>(T, F, twh);
     __syncthreads();
@@ -598,6 +596,10 @@ extern "C" int hpg_debug_trace(long long* out) {   // copies g_tc2_trace (2*64*8
   return cudaMemcpyFromSymbol(out, g_tc2_trace, sizeof(g_tc2_trace)) == cudaSuccess ? 0 : 1;
 }
 
+bool tail_supported(const Geometry& g);
+cudaError_t launch_tail(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s, int i0, int i1,
+                        const float* win);
+
 constexpr int kTc2Chunk = 4096;   // items per K1/K2 pair: W (14 KB each) stays resident in L2
 
 bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
@@ -612,7 +614,7 @@ bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, c
 int64_t tc2_chunk() { return kTc2Chunk; }
 
 size_t tc2_workspace(int64_t items) {
-  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 42 * 42 * sizeof(float2);
+  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 2 * 42 * 42 * sizeof(float);   // planar W
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -653,7 +655,7 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
     if (e != cudaSuccess) return e;
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k2_per_sm, field128_kernel<42, 42>, 256, k2_bytes);
-  float2* wbuf = reinterpret_cast<float2*>(p.work);
+  float* wbuf = reinterpret_cast<float*>(p.work);
   CUtensorMap tmap;
   cudaError_t te = frame_tensor_map(p, &tmap);
   if (te != cudaSuccess) return te;
@@ -661,16 +663,22 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
   for (int i0 = 0; i0 < items; i0 += kTc2Chunk) {
     const int i1 = std::min(items, i0 + kTc2Chunk);
     const int n = i1 - i0;
-    const int g1 = std::max(1, std::min(n, num_sms));
+    // one pol per CTA: the grid (and every chunk start) is a multiple of P
+    const int g1 = std::max(1, std::min(n, num_sms) / p.g.P * p.g.P);
     if (p.fmt == 0)
       fourier128_tc2_kernel<0><<<g1, kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1, wbuf);
     else
       fourier128_tc2_kernel<1><<<g1, kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1, wbuf);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(
-        p, i0, i1, wbuf);
-    e = cudaGetLastError();
+    const char* env = getenv("HOLO_TAIL");   // diagnostic: HOLO_TAIL=0 runs the round-1 CTA-wide tail
+    if (tail_supported(p.g) && !(env && env[0] == '0')) {
+      e = launch_tail(p, ft, num_sms, s, i0, i1, wbuf);
+    } else {
+      field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(
+          p, i0, i1, wbuf);
+      e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -24,26 +24,28 @@ L = eng.prepare_launch()
 for _ in range(3):
     L.launch()
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * (2 * 64 * 8))()
+buf = (ctypes.c_longlong * (3 * 64 * 8))()
 lib = native.lib()
 lib.hpg_debug_trace.argtypes = [ctypes.c_void_p]
 assert lib.hpg_debug_trace(buf) == 0
-t = np.frombuffer(buf, dtype=np.int64).reshape(2, 64, 8).astype(np.float64)
+t = np.frombuffer(buf, dtype=np.int64).reshape(3, 64, 8).astype(np.float64)
 t0 = t[0, 0, 0]
 P = t[0] - t0
 C = t[1] - t0
-names_p = ["start", "-", "converted", "fac ready", "mma1 issued", "mma2 issued"]
-names_c = ["start", "mma1a done", "drained1", "mma2 done", "drained2", "W stored"]
-for k in range(min(14, 64)):
-    print(f"k={k:2d} P: " + " ".join(f"{n}={P[k, i]:8.0f}" for i, n in enumerate(names_p) if n != "-"))
-    print(f"      C: " + " ".join(f"{n}={C[k, i]:8.0f}" for i, n in enumerate(names_c)))
-n = 12
-print("per-window period (consumer W stored):", np.diff(C[2:n, 5]).mean(), " producer:", np.diff(P[2:n, 0]).mean())
-print("producer convert", (P[2:n, 2] - P[2:n, 0]).mean(), " fac", (P[2:n, 3] - P[2:n, 2]).mean())
-print("  stfree0 wait", (P[2:n, 1] - P[2:n, 0]).mean(), " lfull0 wait", (P[2:n, 6] - P[2:n, 1]).mean(),
-      " chunk0-1 convert + lfull2 wait", (P[2:n, 7] - P[2:n, 6]).mean(), " chunks 2-3", (P[2:n, 2] - P[2:n, 7]).mean())
-print("mma1b issued - mma2 issued(prev)", (P[2:n, 4] - P[1:n - 1, 5]).mean(), " mma2 issued - mma1b issued",
-      (P[2:n, 5] - P[2:n, 4]).mean())
-print("consumer wait mma1a:", (C[2:n, 1] - C[2:n, 0]).mean(), " drain1 (both halves):", (C[2:n, 2] - C[2:n, 1]).mean(),
-      " wait mma2:", (C[2:n, 3] - C[2:n, 2]).mean(), " drain2:", (C[2:n, 4] - C[2:n, 3]).mean(),
-      " W:", (C[2:n, 5] - C[2:n, 4]).mean())
+M = t[2] - t0
+# P (producers) per half h: 4h+0 start, 4h+1 stfree passed, 4h+2 landed, 4h+3 converted (after barrier)
+# M (MMA): 0/1 S1h0 ready/issued, 2/3 S1h1, 4/5 S2h0, 6/7 S2h1
+# C (consumers): 0/1 D1h0 ready/drained, 2/3 D1h1 ready/drained, 4 fac ready, 5 D2 ready, 6 W stored
+n = 14
+np.set_printoptions(linewidth=200)
+for k in range(n):
+    print(f"k={k:2d} P " + " ".join(f"{v:7.0f}" for v in P[k]))
+    print(f"     M " + " ".join(f"{v:7.0f}" for v in M[k]))
+    print(f"     C " + " ".join(f"{v:7.0f}" for v in C[k]))
+a, b = 3, n - 1
+d = lambda X, i, j: (X[a:b, j] - X[a:b, i]).mean()
+print("period", np.diff(M[a:b, 3]).mean())
+print("P h0: stfree wait", d(P, 0, 1), "land wait", d(P, 1, 2), "convert", d(P, 2, 3), "| h1: gap", d(P, 3, 4),
+      "stfree wait", d(P, 4, 5), "land wait", d(P, 5, 6), "convert", d(P, 6, 7))
+print("M: S1h0 issue", d(M, 0, 1), "S1h1 issue", d(M, 2, 3), "S2h0 issue", d(M, 4, 5), "S2h1 issue", d(M, 6, 7))
+print("C: D1h0 drain", d(C, 0, 1), "D1h1 drain", d(C, 2, 3), "D2 drain", d(C, 5, 6))
