@@ -434,17 +434,15 @@ def main():
         except (OSError, ValueError, KeyError):
             traffic = None
 
-    # ---------------- e2e through the public API with pinned host frames
-    e2e = None
-    if not args.no_e2e:
-        pinned = torch.from_numpy(frames_host).pin_memory()
-        api.set_batch(h, B, pinned)
+    # ---------------- e2e through the public API with host frames (H2D + kernel + D2H in the timed region)
+    def time_e2e(setter, host, reps):
+        setter(host)
         for _ in range(2):
             api.process_batch(h)
         torch.cuda.synchronize()
         e_ms = []
         barrier(world)
-        for i in range(max(5, min(args.steps, 20))):
+        for i in range(reps):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s.record()
             coefs, b, m, p = api.process_batch(h)       # H2D frames, kernel, D2H coefs
@@ -458,11 +456,34 @@ def main():
             e_ms.append(s.elapsed_time(e))
         barrier(world)
         em = max_over_ranks(float(np.median(e_ms)), world)   # median step (host scheduling jitter)
-        e2e = {"value": B * world / (em / 1e3), "unit": "frames/s",
-               "h2d_bytes_per_step": int(eng.last_h2d_bytes), "d2h_bytes_per_step": d2h,
-               "ms_per_step": em, "steps": len(e_ms), "stat": "median",
-               "path": "api.process_batch on pinned host frames: window-only H2D (hpg_upload_windows), "
-                       "fused kernel, D2H of the coefficients (of the int16 fields when there is no basis)"}
+        return {"value": B * world / (em / 1e3), "unit": "frames/s",
+                "h2d_bytes_per_step": int(eng.last_h2d_bytes), "d2h_bytes_per_step": d2h,
+                "ms_per_step": em, "steps": len(e_ms), "stat": "median"}
+
+    e2e = None
+    e2e_variants = {}
+    if not args.no_e2e:
+        reps = max(5, min(args.steps, 20))
+        pinned = torch.from_numpy(frames_host).pin_memory()
+        e2e = time_e2e(lambda x: api.set_batch(h, B, x), pinned, reps)
+        e2e["path"] = ("api.process_batch on pinned host frames: window-only H2D (hpg_upload_windows), "
+                       "fused kernel, D2H of the coefficients (of the int16 fields when there is no basis)")
+        del pinned
+        # the drop-in caller's buffer: a pageable numpy array, exactly as holopipe.api.set_batch receives it
+        v = time_e2e(lambda x: api.set_batch(h, B, x), frames_host, reps)
+        v["path"] = "api.set_batch(numpy float32, pageable) + api.process_batch"
+        e2e_variants["pageable_numpy_f32"] = v
+        if np.array_equal(frames_host, np.round(frames_host)) and frames_host.min() >= 0 and frames_host.max() < 65536:
+            # camera format (holopipe/frames.py:49-59): the same integer frames as uint16, half the PCIe bytes
+            u16 = torch.from_numpy(frames_host.astype(np.uint16)).pin_memory()
+            v = time_e2e(lambda x: api.set_batch_uint16(h, B, x), u16, reps)
+            v["path"] = "api.set_batch_uint16(pinned uint16 frames) + api.process_batch"
+            e2e_variants["pinned_u16"] = v
+            u16np = frames_host.astype(np.uint16)
+            v = time_e2e(lambda x: api.set_batch_uint16(h, B, x), u16np, reps)
+            v["path"] = "api.set_batch_uint16(numpy uint16, pageable) + api.process_batch"
+            e2e_variants["pageable_numpy_u16"] = v
+            del u16, u16np
         api.set_batch(h, B, frames_dev)
 
     cpu = None
@@ -503,6 +524,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_variants": e2e_variants or None,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks.summary(),
         }

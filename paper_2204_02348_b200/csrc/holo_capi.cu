@@ -290,6 +290,8 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
   if (P->tc_dev) return cudaSuccess;
   const Geometry& g = P->g;
   const double (&xi)[2][2] = P->xi;
+  // Both tables are stored column-major, [pol][hi | lo][column (f16x2)][row n], so that a warp loading its
+  // 32 TMEM lanes reads 32 consecutive words per instruction.
   // tensor-core row DFT (holo_fast_tc.cu): A[n][x], n < 64 -> Re, n >= 64 -> Im of
   // exp(-2 pi i kx_c x / nx) * px[c] = exp(-2 pi i kx_c (x - xi_x + nx/2) / nx), c = n mod 64,
   // split into fp16 hi + lo; rows c >= ww are zero.  Only for nx == 128, wavelength 0.
@@ -313,8 +315,8 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
             hh[e] = __half_as_ushort(h);
             ll[e] = __half_as_ushort(l);
           }
-          a_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + x2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
-          a_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + x2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+          a_tc[(((size_t)q * 2 + 0) * 64 + x2) * 128 + n] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a_tc[(((size_t)q * 2 + 1) * 64 + x2) * 128 + n] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
         }
       }
     }
@@ -343,8 +345,8 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
             hh[e] = __half_as_ushort(h);
             ll[e] = __half_as_ushort(l);
           }
-          a2_tc[(((size_t)q * 2 + 0) * 128 + n) * 64 + y2] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
-          a2_tc[(((size_t)q * 2 + 1) * 128 + n) * 64 + y2] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+          a2_tc[(((size_t)q * 2 + 0) * 64 + y2) * 128 + n] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a2_tc[(((size_t)q * 2 + 1) * 64 + y2) * 128 + n] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
         }
       }
     }

@@ -178,15 +178,15 @@ __global__ void __launch_bounds__(kProd + kCons, 1) fast128tc_kernel(const __gri
         asm volatile("tcgen05.fence::after_thread_sync;");
       }
       if (q != loaded_q) {
-        const uint32_t* src = ft.a_tc + ((size_t)q * 2 * 128 + warp * 32 + lane) * 64;
+        const uint32_t* src = ft.a_tc + (size_t)q * 2 * 64 * 128 + warp * 32 + lane;   // column-major table
         uint32_t r[32];
 #pragma unroll
         for (int part = 0; part < 2; ++part) {
 #pragma unroll
           for (int half = 0; half < 2; ++half) {
-            const uint32_t* s2 = src + (size_t)part * 128 * 64 + half * 32;
+            const uint32_t* s2 = src + ((size_t)part * 64 + half * 32) * 128;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
+            for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
             tmem_st32(tm + ((uint32_t)(warp * 32) << 16) + part * 64 + half * 32, r);
           }
         }

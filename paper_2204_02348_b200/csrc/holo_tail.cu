@@ -49,32 +49,73 @@ inline TailLayout tail_layout(int G, int P) {
 namespace {
 
 // in-place inverse DFT-6 / DFT-7 passes over the 42 sequences of one axis.  Sequence s, element e is at
-// buf[s * SS + e * ES].
+// buf[s * SS + e * ES].  Tasks touch disjoint elements, so each lane loads the inputs of TWO tasks before
+// it stores anything (otherwise every task's loads wait behind the previous task's stores).
 template <int SS, int ES>
 HOLO_DEV void pfa_pass6(float2* buf, int lane) {
-  for (int t = lane; t < kN * 7; t += 32) {
-    const int s = t / 7, n2 = t - 7 * s;
-    float2* q = buf + s * SS;
-    float2 v[6];
+  constexpr int kTasks = kN * 7;
+#pragma unroll 1
+  for (int t0 = lane; t0 < kTasks; t0 += 64) {
+    const int t1 = t0 + 32;
+    const bool two = t1 < kTasks;
+    const int s0 = t0 / 7, a0 = 6 * (t0 - 7 * s0);
+    const int s1 = two ? t1 / 7 : s0, a1 = two ? 6 * (t1 - 7 * s1) : a0;
+    float2* q0 = buf + s0 * SS;
+    float2* q1 = buf + s1 * SS;
+    int p0[6], p1[6];
 #pragma unroll
-    for (int n1 = 0; n1 < 6; ++n1) v[n1] = q[pfa_in(n1, n2) * ES];
+    for (int n1 = 0; n1 < 6; ++n1) {   // (7 n1 + 6 n2) mod 42 with 6 n2 = a < 42
+      p0[n1] = a0 + 7 * n1 >= kN ? a0 + 7 * n1 - kN : a0 + 7 * n1;
+      p1[n1] = a1 + 7 * n1 >= kN ? a1 + 7 * n1 - kN : a1 + 7 * n1;
+    }
+    float2 v[6], w[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      v[j] = q0[p0[j] * ES];
+      w[j] = q1[p1[j] * ES];
+    }
     dft6<true>(v);
+    dft6<true>(w);
 #pragma unroll
-    for (int k1 = 0; k1 < 6; ++k1) q[pfa_in(k1, n2) * ES] = v[k1];
+    for (int j = 0; j < 6; ++j) q0[p0[j] * ES] = v[j];
+    if (two) {
+#pragma unroll
+      for (int j = 0; j < 6; ++j) q1[p1[j] * ES] = w[j];
+    }
   }
 }
 
 template <int SS, int ES>
 HOLO_DEV void pfa_pass7(float2* buf, int lane) {
-  for (int t = lane; t < kN * 6; t += 32) {
-    const int s = t / 6, k1 = t - 6 * s;
-    float2* q = buf + s * SS;
-    float2 v[7];
+  constexpr int kTasks = kN * 6;
+#pragma unroll 1
+  for (int t0 = lane; t0 < kTasks; t0 += 64) {
+    const int t1 = t0 + 32;
+    const bool two = t1 < kTasks;
+    const int s0 = t0 / 6, a0 = 7 * (t0 - 6 * s0);
+    const int s1 = two ? t1 / 6 : s0, a1 = two ? 7 * (t1 - 6 * s1) : a0;
+    float2* q0 = buf + s0 * SS;
+    float2* q1 = buf + s1 * SS;
+    int p0[7], p1[7];
 #pragma unroll
-    for (int n2 = 0; n2 < 7; ++n2) v[n2] = q[pfa_in(k1, n2) * ES];
+    for (int n2 = 0; n2 < 7; ++n2) {   // (7 k1 + 6 n2) mod 42 with 7 k1 = a <= 35
+      p0[n2] = a0 + 6 * n2 >= kN ? a0 + 6 * n2 - kN : a0 + 6 * n2;
+      p1[n2] = a1 + 6 * n2 >= kN ? a1 + 6 * n2 - kN : a1 + 6 * n2;
+    }
+    float2 v[7], w[7];
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+      v[j] = q0[p0[j] * ES];
+      w[j] = q1[p1[j] * ES];
+    }
     dft7<true>(v);
+    dft7<true>(w);
 #pragma unroll
-    for (int k2 = 0; k2 < 7; ++k2) q[pfa_in(k1, k2) * ES] = v[k2];
+    for (int j = 0; j < 7; ++j) q0[p0[j] * ES] = v[j];
+    if (two) {
+#pragma unroll
+      for (int j = 0; j < 7; ++j) q1[p1[j] * ES] = w[j];
+    }
   }
 }
 
@@ -89,8 +130,8 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int G = (p.coefs && g.G > 0) ? g.G : 0;
   const int GP = max(4, (g.G + 3) & ~3);
-  float2* buf = reinterpret_cast<float2*>(smem + warp * L.warp_bytes);                  // [c][r] pitch 43
-  uint32_t* fq = reinterpret_cast<uint32_t*>(smem + warp * L.warp_bytes + L.buf_bytes);  // [y][x] int16x2
+  float2* __restrict__ buf = reinterpret_cast<float2*>(smem + warp * L.warp_bytes);     // [c][r] pitch 43
+  uint32_t* __restrict__ fq = reinterpret_cast<uint32_t*>(smem + warp * L.warp_bytes + L.buf_bytes);  // [y][x]
   float* basis = reinterpret_cast<float*>(smem + L.basis_off);                           // [P][x|y][GP]
 
   if (G > 0) {   // basis of every pol, transposed [x][m] / [y][n] (hgbasis.py:95-99 profiles)
@@ -134,23 +175,30 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
     const float2* ex = p.t.rem_x + pl * kN;
     const float2* ey = p.t.rem_y + pl * kN;
     float lmax = 0.f;
+#pragma unroll 1
     for (int t = lane; t < kN * 6; t += 32) {   // last pass: DFT-7 along x with the removal phase fused
       const int pr = t / 6, k1 = t - 6 * pr;    // pr: position of the row (natural y below)
       const int y = (7 * (pr % 6) + 36 * ((6 * pr) % 7)) % kN;
+      const int a = 7 * k1;
+      int pc[7];
+#pragma unroll
+      for (int n2 = 0; n2 < 7; ++n2) pc[n2] = a + 6 * n2 >= kN ? a + 6 * n2 - kN : a + 6 * n2;
       float2 v[7];
 #pragma unroll
-      for (int n2 = 0; n2 < 7; ++n2) v[n2] = buf[pfa_in(k1, n2) * kPC + pr];
+      for (int n2 = 0; n2 < 7; ++n2) v[n2] = buf[pc[n2] * kPC + pr];
       dft7<true>(v);
       const float2 eyq = __ldg(&ey[y]);
 #pragma unroll
       for (int k2 = 0; k2 < 7; ++k2) {
-        const int x = (7 * k1 + 36 * k2) % kN;
+        const int x = (a + 36 * k2) % kN;
         float2 o = cmul(cmul(v[k2], eyq), __ldg(&ex[x]));   // same operation order as ct_stage_final_rows
         if (p.bcal) o = cmul(o, bc);
         if (rc) o = cmul(o, __ldg(&rc[y * kN + x]));   // reference calibration (engine.py:250-255)
         lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
-        buf[pfa_in(k1, k2) * kPC + pr] = o;
+        v[k2] = o;
       }
+#pragma unroll
+      for (int k2 = 0; k2 < 7; ++k2) buf[pc[k2] * kPC + pr] = v[k2];
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
@@ -183,15 +231,15 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
     // --------------------------------------------------------------------- HG overlap (SIMT)
     // U[y][m] = sum_x Fq[y][x] hx[m][x] on the integer-valued field; the dequantisation 1/scale
     // (engine.py:367-369) is applied once per coefficient.
-    const float* hxT = basis + q * 2 * kN * GP;   // [x][GP]
-    const float* hyT = hxT + kN * GP;              // [y][GP]
-    float2* U = buf;                                // [y][GP]
+    const float* __restrict__ hxT = basis + q * 2 * kN * GP;   // [x][GP]
+    const float* __restrict__ hyT = hxT + kN * GP;              // [y][GP]
+    float2* __restrict__ U = buf;                                // [y][GP]
     const int GQ = GP >> 2;
     constexpr int CX = kN / 2, NPX = kN - 1 - CX;  // parity around the axis origin x = 21
     const bool xsym = (ft.hsym >> (2 * q)) & 1, ysym = (ft.hsym >> (2 * q + 1)) & 1;
     for (int t = lane; t < kN * GQ; t += 32) {
       const int y = t / GQ, mq = t - y * GQ;
-      const uint32_t* row = fq + y * kN;
+      const uint32_t* __restrict__ row = fq + y * kN;
       float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
       if (xsym) {   // h_m(c - d) = (-1)^m h_m(c + d): orders 4mq, 4mq+2 take sums, 4mq+1, 4mq+3 differences
 #pragma unroll 4

@@ -49,7 +49,7 @@ constexpr int kSlots = 3;                   // landing ring: half windows
 constexpr uint32_t kBox = 4096;                    // TMA box: 32 rows x 128 B (32 f32 / 64 u16), 128B swizzle
 constexpr uint32_t kSlot = 8 * kBox;               // one half window: [chunk 2][box 4]
 constexpr uint32_t kLand = 0;                      // [slot 3][half window]
-constexpr uint32_t kStage = kSlots * kSlot;        // [half][hi 16 KB | lo 16 KB]
+constexpr uint32_t kStage = kSlots * kSlot;        // row-DFT operand, N = 128 rows: [hi 32 KB | lo 32 KB]
 constexpr uint32_t kStageHalf = 32768;
 constexpr uint32_t kB2 = kStage + 2 * kStageHalf;  // B2 hi | B2 lo: rows c (Re R), 48 + c (Im R)
 constexpr uint32_t kB2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
@@ -97,7 +97,13 @@ HOLO_DEV void split2(float a, float b, uint32_t& hi, uint32_t& lo) {
 }  // namespace
 
 // Phase timestamps of CTA 0 (clock64), for tools/tc2_trace.py (hpg_debug_trace).
-__device__ long long g_tc2_trace[3][64][8];
+__device__ long long g_tc2_trace[4][64][8];
+__device__ long long g_tc2_span[160][4];   // per CTA: globaltimer start / end (ns), clock64 start / end
+HOLO_DEV long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define TC2_MARK(role, kk, ev)                                                   \
   do {                                                                           \
     if (blockIdx.x == 0 && (kk) < 64) g_tc2_trace[role][kk][ev] = clock64();     \
@@ -151,6 +157,10 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   const int nk = first < i1 ? (i1 - first + gridDim.x - 1) / gridDim.x : 0;   // windows of this CTA
   const int q = first % g.P;   // gridDim.x and i0 are multiples of P: one pol per CTA
 
+  if (tid == 0 && blockIdx.x < 160) {
+    g_tc2_span[blockIdx.x][0] = gtimer();
+    g_tc2_span[blockIdx.x][2] = clock64();
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tbase)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -182,16 +192,16 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   {   // constant DFT matrices of this CTA's pol into TMEM: A1 by warps 0-3, A2 by warps 4-7
     const int part_warp = warp & 3;
     if (warp < 8 && nk > 0) {
-      const uint32_t* src = (warp < 4 ? ft.a_tc : ft.a2_tc) + ((size_t)q * 2 * 128 + part_warp * 32 + lane) * 64;
+      const uint32_t* src = (warp < 4 ? ft.a_tc : ft.a2_tc) + (size_t)q * 2 * 64 * 128 + part_warp * 32 + lane;
       const uint32_t dst = (warp < 4 ? tA1 : tA2) + ((uint32_t)(part_warp * 32) << 16);
       uint32_t r[32];
 #pragma unroll
       for (int part = 0; part < 2; ++part) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t* s2 = src + (size_t)part * 128 * 64 + hh * 32;
+          const uint32_t* s2 = src + ((size_t)part * 64 + hh * 32) * 128;   // column-major: coalesced
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j);
+          for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
           tmem_st32(dst + part * 64 + hh * 32, r);
         }
       }
@@ -250,15 +260,15 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         const float sc = ey > -1000 ? pow2f(14 - ey) : 1.f;
         if (gq == 0) erow[y] = ey;
         emax_t = max(emax_t, ey);
-        char* st = smem + kStage + h * kStageHalf;
+        char* st = smem + kStage;   // one K-major N = 128 operand: hi [0, 32 KB), lo [32 KB, 64 KB)
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t off = kmaj_off(yl, 8 * (gq + 4 * i), 8);
+          const uint32_t off = kmaj_off(y, 8 * (gq + 4 * i), 16);
           uint32_t hi2[4], lo2[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) split2(v[8 * i + 2 * e] * sc, v[8 * i + 2 * e + 1] * sc, hi2[e], lo2[e]);
           *reinterpret_cast<uint4*>(st + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-          *reinterpret_cast<uint4*>(st + 16384 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+          *reinterpret_cast<uint4*>(st + 32768 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
         }
         fence_async_smem();
         tc_fence_before();
@@ -283,38 +293,46 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         if (tid == 0) emaxs[s] = em;
       }
       nbar(kBarProd2, kProd2);
-      if (tid == 0) mbar_arrive(&meta[s]);
+      if (tid == 0) {
+        mbar_arrive(&meta[s]);
+        TC2_MARK(2, k, 2);   // (row_gemm's entry mark is overwritten: slot 2 = meta arrive time)
+      }
     }
   } else if (warp == kTmaWarp) {
     // ================================ TMA issuer ================================
-    if (lane == 0) {
-      for (int jh = 0; jh < 2 * nk; ++jh) {
-        const int slot = jh % kSlots;
-        if (jh >= kSlots) mbar_wait(&landfree[slot], ((jh / kSlots) - 1) & 1);
-        issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, slot, &landfull[slot]);
-      }
+    for (int jh = 0; jh < 2 * nk; ++jh) {   // the whole warp walks the ring (converged), lane 0 issues
+      const int slot = jh % kSlots;
+      if (jh >= kSlots) mbar_wait_warp(&landfree[slot], ((jh / kSlots) - 1) & 1);
+      if (lane == 0) issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, slot, &landfull[slot]);
+      __syncwarp();
     }
   } else if (warp == kMmaWarp) {
     // ================================ MMA issuer ================================
-    const uint32_t idesc1 = idesc_f16(128, 64), idesc2 = idesc_f16(128, 2 * kN2);
-    auto row_gemm = [&](int k, int h) {   // D1[:, 64h .. 64h+63] = A1 * stage half h
-      mbar_wait_warp(&staged[h], k & 1);
-      if (k >= 1) mbar_wait_warp(&b2ready[h], (k - 1) & 1);   // D1 half h of k-1 drained
-      if (lane == 0) TC2_MARK(2, k, 2 * h);
+    const uint32_t idesc1 = idesc_f16(128, 128), idesc2 = idesc_f16(128, 2 * kN2);
+    // row GEMM over the whole window (N = 128: 24 MMAs; two N = 64 halves cost 48 MMAs, each bounded by
+    // its 4 KB TMEM A-operand read rather than by N -- measured 1.4 K cycles per half vs ~1.75 K in one)
+    auto row_gemm = [&](int k) {
+      mbar_wait_warp(&staged[0], k & 1);
+      if (lane == 0) TC2_MARK(2, k, 3);
+      mbar_wait_warp(&staged[1], k & 1);
+      if (k >= 1) mbar_wait_warp(&b2ready[1], (k - 1) & 1);   // D1 of k-1 drained (both halves, in order)
+      if (lane == 0) TC2_MARK(2, k, 0);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t sb = smem_u32(smem + kStage + h * kStageHalf);
+        const uint32_t sb = smem_u32(smem + kStage);
 #pragma unroll
         for (int gk = 0; gk < 8; ++gk) {
-          const uint64_t bh = umma_desc(sb + gk * 2048, 128, 256);
-          const uint64_t bl = umma_desc(sb + 16384 + gk * 2048, 128, 256);
-          mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bh, idesc1, gk != 0);
-          mma_f16_ts(tD1 + 64 * h, tA1 + 64 + gk * 8, bh, idesc1, 1);
-          mma_f16_ts(tD1 + 64 * h, tA1 + gk * 8, bl, idesc1, 1);
+          const uint64_t bh = umma_desc(sb + gk * 4096, 128, 256);
+          const uint64_t bl = umma_desc(sb + 32768 + gk * 4096, 128, 256);
+          mma_f16_ts(tD1, tA1 + gk * 8, bh, idesc1, gk != 0);
+          mma_f16_ts(tD1, tA1 + 64 + gk * 8, bh, idesc1, 1);
+          mma_f16_ts(tD1, tA1 + gk * 8, bl, idesc1, 1);
         }
-        tc_commit(&stfree[h]);
-        tc_commit(&d1full[h]);
-        TC2_MARK(2, k, 2 * h + 1);
+        tc_commit(&stfree[0]);
+        tc_commit(&stfree[1]);
+        tc_commit(&d1full[0]);
+        tc_commit(&d1full[1]);
+        TC2_MARK(2, k, 1);
       }
       __syncwarp();
     };
@@ -339,15 +357,11 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       }
       __syncwarp();
     };
-    if (nk > 0) {
-      row_gemm(0, 0);
-      row_gemm(0, 1);
-    }
+    if (nk > 0) row_gemm(0);
     for (int k = 0; k < nk; ++k) {
       col_gemm(k, 0);
-      if (k + 1 < nk) row_gemm(k + 1, 0);
       col_gemm(k, 1);
-      if (k + 1 < nk) row_gemm(k + 1, 1);
+      if (k + 1 < nk) row_gemm(k + 1);
     }
   } else {
     // ================================= consumers =================================
@@ -356,12 +370,17 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     float* X = reinterpret_cast<float*>(smem + kX);
     const int n = quarter * 32 + lane, c = n & 63;
     const int brow = (n >= 64 ? kN2 : 0) + c;   // B2 row: Re R rows then Im R rows
+
     auto drain_d1 = [&](int k, int h) {   // D1 half h of window k -> B2 half h (this warp: 32 of its 64 y)
       const int s = k & 1;
       mbar_wait_warp(&d1full[h], k & 1);
       if (k >= 1) mbar_wait_warp(&b2free[h], (k - 1) & 1);   // column GEMM of k-1 done with B2 half h
       tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 2 * h);
+      if (h == 0 && k >= 1) {   // the previous window's W bulk copy has finished reading its staging in B2
+        if (ct == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        nbar(kBarCons2, kCons2);
+      }
       const int y0 = 64 * h + 32 * sub;
       uint32_t r[32];
       tmem_ld32(tD1 + ((uint32_t)(quarter * 32) << 16) + y0, r);
@@ -403,50 +422,69 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       tmem_ld16(src + 32, v + 32);
       tmem_wait_ld();
       tc_fence_before();
+      if (ct == 0) TC2_MARK(3, k, 0);
+      // Cr rows -> the planar staging copy in the (now free) B2 buffer, Y[sub][r][c] (sub 0: Cr Rr, 1: Cr Ri);
+      // Ci rows -> X[r][sub * 48 + c]; then every consumer thread combines in place:
+      //   Y[0] = (Cr Rr - Ci Ri) gs,  Y[1] = (Cr Ri + Ci Rr) gs, masked
+      float* Y = reinterpret_cast<float*>(b2);
       const int r = n & 63;
-      if (n >= 64 && r < kWinH) {
-        float* xr = X + r * kXP + sub * kN2;
+      if (r < kWinH) {
+        float* dst = n >= 64 ? X + r * kXP + sub * kN2 : Y + sub * (kWinH * kWinW) + r * kWinW;
 #pragma unroll
-        for (int cc = 0; cc < kWinW; ++cc) xr[cc] = __uint_as_float(v[cc]);
+        for (int cc = 0; cc < kWinW; ++cc) dst[cc] = __uint_as_float(v[cc]);
       }
+      if (ct == 0) TC2_MARK(3, k, 1);
       nbar(kBarCons2, kCons2);
-      if (ct == 0) mbar_arrive(&d2free);   // D2 is in registers / X: the next column GEMM may start
-      if (n < 64 && r < kWinH) {
-        const float* xr = X + r * kXP + (sub ? 0 : kN2);   // sub 0 needs Ci Ri, sub 1 needs Ci Rr
-        const float sg = sub ? 1.f : -1.f;
-        float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 2 + sub) * (kWinH * kWinW) + r * kWinW;
-#pragma unroll
-        for (int cc = 0; cc < kWinW; ++cc) {
-          const bool in = r >= crs[2 * cc] && r <= crs[2 * cc + 1];
-          wo[cc] = in ? fmaf(sg, xr[cc], __uint_as_float(v[cc])) * gs : 0.f;
-        }
+      if (ct == 0) {
+        TC2_MARK(3, k, 2);
+        mbar_arrive(&d2free);   // D2 is in shared memory: the next column GEMM may start
       }
+      if (ct == 64) TC2_MARK(3, k, 6);
+      for (int i = ct; i < kWinH * kWinW; i += kCons2) {
+        const int rr = i / kWinW, cc = i - rr * kWinW;
+        const float crr = Y[i], cri = Y[kWinH * kWinW + i];
+        const float cir = X[rr * kXP + cc], cii = X[rr * kXP + kN2 + cc];
+        const bool in = rr >= crs[2 * cc] && rr <= crs[2 * cc + 1];
+        Y[i] = in ? (crr - cii) * gs : 0.f;
+        Y[kWinH * kWinW + i] = in ? (cri + cir) * gs : 0.f;
+      }
+      if (ct == 64) TC2_MARK(3, k, 7);
+      if (ct == 0) TC2_MARK(3, k, 3);
+      nbar(kBarCons2, kCons2);
+      if (ct == 0) TC2_MARK(3, k, 4);
+      // ... and one bulk async copy (TMA engine, not the LSU) of both planes to the item's W
+      if (ct == 0) {
+        fence_async_smem();
+        float* wo = wout + (size_t)(first + k * gridDim.x - i0) * 2 * (kWinH * kWinW);
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wo), "r"(smem_u32(Y)),
+                     "r"((uint32_t)(2 * kWinH * kWinW * sizeof(float)))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if (ct == 0) TC2_MARK(3, k, 5);
       nbar(kBarCons2, kCons2);   // X free for the next window
       if (ct == 0) TC2_MARK(1, k, 6);
     };
-    if (nk > 0) {
-      mbar_wait_warp(&meta[0], 0);
-      drain_d1(0, 0);
-    }
-    float gs = nk > 0 ? pow2f(emaxs[0] - 8) : 1.f;
     for (int k = 0; k < nk; ++k) {
+      if (ct == 0) TC2_MARK(1, k, 7);
+      mbar_wait_warp(&meta[k & 1], (k >> 1) & 1);
+      if (ct == 0) TC2_MARK(1, k, 4);
+      const float gs = pow2f(emaxs[k & 1] - 8);
+      drain_d1(k, 0);
       drain_d1(k, 1);   // ends with a consumer barrier: every thread is done with fac[k & 1]
       if (ct == 0) mbar_arrive(&facfree[k & 1]);
-      float gs_next = 1.f;
-      if (k + 1 < nk) {
-        mbar_wait_warp(&meta[(k + 1) & 1], ((k + 1) >> 1) & 1);
-        if (ct == 0) TC2_MARK(1, k + 1, 4);
-        gs_next = pow2f(emaxs[(k + 1) & 1] - 8);
-        drain_d1(k + 1, 0);
-      }
       drain_d2(k, gs);
-      gs = gs_next;
     }
   }
+  if (warp >= kConsWarp0 && tid == kConsWarp0 * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tm));
+  if (tid == 0 && blockIdx.x < 160) {
+    g_tc2_span[blockIdx.x][1] = gtimer();
+    g_tc2_span[blockIdx.x][3] = clock64();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -590,6 +628,10 @@ __global__ void __launch_bounds__(256, 3)
       }
     }
   }
+}
+
+extern "C" int hpg_debug_span(long long* out) {   // copies g_tc2_span (160*4 int64) to host
+  return cudaMemcpyFromSymbol(out, g_tc2_span, sizeof(g_tc2_span)) == cudaSuccess ? 0 : 1;
 }
 
 extern "C" int hpg_debug_trace(long long* out) {   // copies g_tc2_trace (2*64*8 int64) to host

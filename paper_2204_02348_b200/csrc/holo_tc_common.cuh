@@ -33,19 +33,17 @@ HOLO_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
-// one lane waits (suspended in hardware up to the hint instead of spinning hot),
-// the rest of the warp waits at the warp barrier
+// every lane of the warp polls the barrier (the warp stays converged: no lane parks at a warp barrier
+// while another spins, which was measured to delay the hand-offs by ~1-5 K cycles)
 HOLO_DEV void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
-  if ((threadIdx.x & 31) == 0) {
-    uint32_t done = 0;
-    while (!done) {
+  uint32_t done = 0;
+  while (!__all_sync(0xffffffffu, done)) {
+    if (!done)
       asm volatile(
-          "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p;}"
+          "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
           : "=r"(done)
-          : "r"(smem_u32(bar)), "r"(phase), "r"(1000000u));
-    }
+          : "r"(smem_u32(bar)), "r"(phase));
   }
-  __syncwarp();
 }
 
 HOLO_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
@@ -71,7 +69,13 @@ HOLO_DEV uint32_t pack_h2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-HOLO_DEV void nbar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// named barrier over n threads; bar.sync is .aligned (every lane of a warp must execute the same
+// instance), so the warp is reconverged first -- a warp arriving split after divergent code was measured
+// to hold the barrier for thousands of cycles
+HOLO_DEV void nbar(int id, int n) {
+  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 HOLO_DEV void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }

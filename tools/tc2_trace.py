@@ -24,15 +24,16 @@ L = eng.prepare_launch()
 for _ in range(3):
     L.launch()
 torch.cuda.synchronize()
-buf = (ctypes.c_longlong * (3 * 64 * 8))()
+buf = (ctypes.c_longlong * (4 * 64 * 8))()
 lib = native.lib()
 lib.hpg_debug_trace.argtypes = [ctypes.c_void_p]
 assert lib.hpg_debug_trace(buf) == 0
-t = np.frombuffer(buf, dtype=np.int64).reshape(3, 64, 8).astype(np.float64)
+t = np.frombuffer(buf, dtype=np.int64).reshape(4, 64, 8).astype(np.float64)
 t0 = t[0, 0, 0]
 P = t[0] - t0
 C = t[1] - t0
 M = t[2] - t0
+D = t[3] - t0
 # P (producers) per half h: 4h+0 start, 4h+1 stfree passed, 4h+2 landed, 4h+3 converted (after barrier)
 # M (MMA): 0/1 S1h0 ready/issued, 2/3 S1h1, 4/5 S2h0, 6/7 S2h1
 # C (consumers): 0/1 D1h0 ready/drained, 2/3 D1h1 ready/drained, 4 fac ready, 5 D2 ready, 6 W stored
@@ -42,6 +43,7 @@ for k in range(n):
     print(f"k={k:2d} P " + " ".join(f"{v:7.0f}" for v in P[k]))
     print(f"     M " + " ".join(f"{v:7.0f}" for v in M[k]))
     print(f"     C " + " ".join(f"{v:7.0f}" for v in C[k]))
+    print(f"     D " + " ".join(f"{v:7.0f}" for v in D[k]))
 a, b = 3, n - 1
 d = lambda X, i, j: (X[a:b, j] - X[a:b, i]).mean()
 print("period", np.diff(M[a:b, 3]).mean())
@@ -49,3 +51,20 @@ print("P h0: stfree wait", d(P, 0, 1), "land wait", d(P, 1, 2), "convert", d(P, 
       "stfree wait", d(P, 4, 5), "land wait", d(P, 5, 6), "convert", d(P, 6, 7))
 print("M: S1h0 issue", d(M, 0, 1), "S1h1 issue", d(M, 2, 3), "S2h0 issue", d(M, 4, 5), "S2h1 issue", d(M, 6, 7))
 print("C: D1h0 drain", d(C, 0, 1), "D1h1 drain", d(C, 2, 3), "D2 drain", d(C, 5, 6))
+
+sp = (ctypes.c_longlong * (160 * 4))()
+lib.hpg_debug_span.argtypes = [ctypes.c_void_p]
+assert lib.hpg_debug_span(sp) == 0
+sp = np.frombuffer(sp, dtype=np.int64).reshape(160, 4).astype(np.float64)
+g = sp[:148]
+t0 = g[:, 0].min()
+print("CTA start (us) min/med/max", (g[:, 0] - t0).min() / 1e3, np.median(g[:, 0] - t0) / 1e3, (g[:, 0] - t0).max() / 1e3)
+print("CTA end   (us) min/med/max", (g[:, 1] - t0).min() / 1e3, np.median(g[:, 1] - t0) / 1e3, (g[:, 1] - t0).max() / 1e3)
+cyc = g[:, 3] - g[:, 2]
+ns = g[:, 1] - g[:, 0]
+print("CTA duration cycles min/med/max", cyc.min(), np.median(cyc), cyc.max(), " -> GHz", np.median(cyc / ns))
+c0 = sp[0, 2]
+last = max(C[k, 6] for k in range(64) if C[k, 6] > 0) + t0_cycles if False else None
+raw = np.frombuffer(buf, dtype=np.int64).reshape(4, 64, 8).astype(np.float64)
+print("CTA0: setup (entry -> first producer mark) cycles", raw[0, 0, 0] - c0,
+      " last W -> exit", sp[0, 3] - raw[1, :, 6].max())
