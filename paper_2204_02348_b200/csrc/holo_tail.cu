@@ -1,9 +1,9 @@
 // Field tail of the 128-window / 42 x 42 geometry: W -> 42 x 42 IFFT -> removal phase, calibrations ->
 // int16 packing -> HG overlap (holopipe/pipeline.py:130-199, engine.py:234-272, hgbasis.py:101-116).
 //
-// One WARP per window, no CTA-wide barrier: a warp owns a window buffer in shared memory and walks
-// its window through every step with __syncwarp only, so the SM's warps are all independent and the
-// per-step parallelism (294 / 252 small DFTs per IFFT axis) fills the 32 lanes.
+// One warp PAIR per window, no CTA-wide barrier: a pair owns a window buffer in shared memory and walks
+// its window through every step with a 64-thread named barrier only, so the windows of an SM are
+// independent and the per-step parallelism (294 / 252 small DFTs per IFFT axis) fills the 64 lanes.
 //
 // The 42-point inverse DFT uses the Good-Thomas prime-factor map (42 = 6 x 7, gcd 1): input n =
 // (7 n1 + 6 n2) mod 42, output k = (7 k1 + 36 k2) mod 42, so
@@ -21,10 +21,15 @@ namespace {
 
 constexpr int kN = 42;          // field side (wh = ww = 42)
 constexpr int kPC = 43;         // buffer pitch (float2) of one column sequence: odd -> spread banks
-constexpr int kTailWarps = 8;   // windows in flight per CTA (one per warp)
+constexpr int kWinPerCta = 8;   // windows in flight per CTA
+constexpr int kWarpsPerWin = 2;  // one warp pair (64 lanes) per window
+constexpr int kTailWarps = kWinPerCta * kWarpsPerWin;
+constexpr int kLanes = 32 * kWarpsPerWin;
 
 HOLO_DEV int pfa_pos(int k) { return (7 * (k % 6) + 6 * (k % 7)) % kN; }
 HOLO_DEV int pfa_in(int a, int b) { return (7 * a + 6 * b) % kN; }   // position of (n1 | k1 = a, n2 | k2 = b)
+// position of output k2 of the DFT-7 task with a = 7 k1 (a + 6 k2 < 42 + 36: one conditional subtract)
+HOLO_DEV int pfa_in_fast(int a, int k2) { return a + 6 * k2 >= kN ? a + 6 * k2 - kN : a + 6 * k2; }
 
 }  // namespace
 
@@ -41,7 +46,7 @@ inline TailLayout tail_layout(int G, int P) {
   const int GP = std::max(4, (G + 3) & ~3);
   L.buf_bytes = std::max(kN * kPC, kN * GP) * 8;
   L.warp_bytes = (L.buf_bytes + kN * kN * 4 + 15) & ~15;
-  L.basis_off = kTailWarps * L.warp_bytes;
+  L.basis_off = kWinPerCta * L.warp_bytes;
   L.total = L.basis_off + (G > 0 ? P * (kN + kN) * GP * 4 : 0);
   return L;
 }
@@ -55,8 +60,8 @@ template <int SS, int ES>
 HOLO_DEV void pfa_pass6(float2* buf, int lane) {
   constexpr int kTasks = kN * 7;
 #pragma unroll 1
-  for (int t0 = lane; t0 < kTasks; t0 += 64) {
-    const int t1 = t0 + 32;
+  for (int t0 = lane; t0 < kTasks; t0 += 2 * kLanes) {
+    const int t1 = t0 + kLanes;
     const bool two = t1 < kTasks;
     const int s0 = t0 / 7, a0 = 6 * (t0 - 7 * s0);
     const int s1 = two ? t1 / 7 : s0, a1 = two ? 6 * (t1 - 7 * s1) : a0;
@@ -89,8 +94,8 @@ template <int SS, int ES>
 HOLO_DEV void pfa_pass7(float2* buf, int lane) {
   constexpr int kTasks = kN * 6;
 #pragma unroll 1
-  for (int t0 = lane; t0 < kTasks; t0 += 64) {
-    const int t1 = t0 + 32;
+  for (int t0 = lane; t0 < kTasks; t0 += 2 * kLanes) {
+    const int t1 = t0 + kLanes;
     const bool two = t1 < kTasks;
     const int s0 = t0 / 6, a0 = 7 * (t0 - 6 * s0);
     const int s1 = two ? t1 / 6 : s0, a1 = two ? 7 * (t1 - 6 * s1) : a0;
@@ -121,17 +126,30 @@ HOLO_DEV void pfa_pass7(float2* buf, int lane) {
 
 }  // namespace
 
-// win: [items][2][42 r][42 c] float (Re plane, Im plane of the masked, recentred window, as K1 writes it)
+// win: [items][4][42 r][42 c] float: K1's column-DFT product planes (Cr Rr, Cr Ri, Ci Rr, Ci Ri)
 __global__ void __launch_bounds__(kTailWarps * 32, 1)
     tail42_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
                   const float* __restrict__ win, TailLayout L) {
   extern __shared__ __align__(16) char smem[];
   const Geometry& g = p.g;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wslot = threadIdx.x / kLanes, lane = threadIdx.x - wslot * kLanes;   // window slot, lane in the pair
+  const int bar_id = 1 + wslot;
+  __shared__ float red[kWinPerCta][kWarpsPerWin];
+  __shared__ int s_lo[kN], s_hi[kN], s_pos[kN], s_nat[kN];   // mask row range per column; PFA position of
+  for (int i = threadIdx.x; i < kN; i += blockDim.x) {          // natural index k, and its inverse
+    s_lo[i] = ft.crange[2 * i];
+    s_hi[i] = ft.crange[2 * i + 1];
+    s_pos[i] = pfa_pos(i);
+    s_nat[pfa_pos(i)] = i;
+  }
+  auto pair_sync = [&]() {   // 64-thread named barrier of this window (warps reconverged first: bar.sync is .aligned)
+    __syncwarp();
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(kLanes) : "memory");
+  };
   const int G = (p.coefs && g.G > 0) ? g.G : 0;
   const int GP = max(4, (g.G + 3) & ~3);
-  float2* __restrict__ buf = reinterpret_cast<float2*>(smem + warp * L.warp_bytes);     // [c][r] pitch 43
-  uint32_t* __restrict__ fq = reinterpret_cast<uint32_t*>(smem + warp * L.warp_bytes + L.buf_bytes);  // [y][x]
+  float2* __restrict__ buf = reinterpret_cast<float2*>(smem + wslot * L.warp_bytes);    // [c][r] pitch 43
+  uint32_t* __restrict__ fq = reinterpret_cast<uint32_t*>(smem + wslot * L.warp_bytes + L.buf_bytes);  // [y][x]
   float* basis = reinterpret_cast<float*>(smem + L.basis_off);                           // [P][x|y][GP]
 
   if (G > 0) {   // basis of every pol, transposed [x][m] / [y][n] (hgbasis.py:95-99 profiles)
@@ -148,27 +166,35 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
   }
   __syncthreads();
 
-  const int nw = gridDim.x * kTailWarps;
-  for (int item = i0 + blockIdx.x * kTailWarps + warp; item < i1; item += nw) {
+  const int nw = gridDim.x * kWinPerCta;
+  for (int item = i0 + blockIdx.x * kWinPerCta + wslot; item < i1; item += nw) {
     const int b = item / g.P, q = item - b * g.P;
     const int w = p.wl ? p.wl[b] : 0;
     const int pl = q * g.L + w;
-    // ------------------------------------------- load W (planar [Re | Im][r][c]) -> buf[c][r]
-    const float* src = win + (size_t)(item - i0) * 2 * kN * kN;
+    // -------------- load the product planes [4][r][c] -> masked W = (P0 - P3) + i (P1 + P2) in buf[c][r]
+    const float* src = win + (size_t)(item - i0) * 4 * kN * kN;
+    {   // element i = lane + 64 j: (r, c) advanced incrementally (64 = 42 + 22)
+      int r = lane >= kN ? 1 : 0, c = lane >= kN ? lane - kN : lane;
 #pragma unroll 4
-    for (int i = lane; i < kN * kN; i += 32) {
-      const int r = i / kN, c = i - kN * r;
-      buf[c * kPC + r] = make_float2(__ldg(src + i), __ldg(src + kN * kN + i));
+      for (int i = lane; i < kN * kN; i += kLanes) {
+        const bool in = r >= s_lo[c] && r <= s_hi[c];
+        const float p0 = __ldg(src + i), p1 = __ldg(src + kN * kN + i);
+        const float p2 = __ldg(src + 2 * kN * kN + i), p3 = __ldg(src + 3 * kN * kN + i);
+        buf[c * kPC + r] = in ? make_float2(p0 - p3, p1 + p2) : make_float2(0.f, 0.f);
+        c += kLanes - kN;
+        r += 1;
+        if (c >= kN) { c -= kN; r += 1; }
+      }
     }
-    __syncwarp();
+    pair_sync();
     // ---------------------------------------- inverse DFT along r (y): 42 columns, prime-factor 6 x 7
     pfa_pass6<kPC, 1>(buf, lane);
-    __syncwarp();
+    pair_sync();
     pfa_pass7<kPC, 1>(buf, lane);
-    __syncwarp();
+    pair_sync();
     // ---------------------------------------------- along c (x): 42 rows (positions), then epilogue
     pfa_pass6<1, kPC>(buf, lane);
-    __syncwarp();
+    pair_sync();
     float2 bc = make_float2(1.f, 0.f);
     if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
     const float2* rc = p.rcal ? p.rcal + ((size_t)(w % p.rcal_count) * g.P + q) * kN * kN : nullptr;
@@ -176,9 +202,9 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
     const float2* ey = p.t.rem_y + pl * kN;
     float lmax = 0.f;
 #pragma unroll 1
-    for (int t = lane; t < kN * 6; t += 32) {   // last pass: DFT-7 along x with the removal phase fused
+    for (int t = lane; t < kN * 6; t += kLanes) {   // last pass: DFT-7 along x with the removal phase fused
       const int pr = t / 6, k1 = t - 6 * pr;    // pr: position of the row (natural y below)
-      const int y = (7 * (pr % 6) + 36 * ((6 * pr) % 7)) % kN;
+      const int y = s_nat[pr];
       const int a = 7 * k1;
       int pc[7];
 #pragma unroll
@@ -190,7 +216,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
       const float2 eyq = __ldg(&ey[y]);
 #pragma unroll
       for (int k2 = 0; k2 < 7; ++k2) {
-        const int x = (a + 36 * k2) % kN;
+        const int x = s_nat[pfa_in_fast(a, k2)];
         float2 o = cmul(cmul(v[k2], eyq), __ldg(&ex[x]));   // same operation order as ct_stage_final_rows
         if (p.bcal) o = cmul(o, bc);
         if (rc) o = cmul(o, __ldg(&rc[y * kN + x]));   // reference calibration (engine.py:250-255)
@@ -202,32 +228,39 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-    __syncwarp();
+    if ((lane & 31) == 0) red[wslot][lane >> 5] = lmax;
+    pair_sync();
+    lmax = fmaxf(red[wslot][0], red[wslot][1]);
     const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;   // pipeline.py:194-198
     // ----------------------------------------------------------- int16 packing, natural [y][x]
     uint32_t* fro = reinterpret_cast<uint32_t*>(p.fr + (size_t)item * kN * kN);
     uint32_t* fio = reinterpret_cast<uint32_t*>(p.fi + (size_t)item * kN * kN);
-    for (int i = lane; i < kN * kN / 2; i += 32) {
-      const int y = i / (kN / 2), x = 2 * (i - y * (kN / 2));
-      const int py = pfa_pos(y);
-      const float2 v0 = buf[pfa_pos(x) * kPC + py], v1 = buf[pfa_pos(x + 1) * kPC + py];
-      if (p.raw) {
-        p.raw[(size_t)item * kN * kN + y * kN + x] = v0;
-        p.raw[(size_t)item * kN * kN + y * kN + x + 1] = v1;
+    {   // pair i = lane + 64 j of row y, columns x, x + 1 (21 pairs per row; 64 = 3 * 21 + 1)
+      int y = lane / 21, x = 2 * (lane - 21 * (lane / 21));
+      for (int i = lane; i < kN * kN / 2; i += kLanes) {
+        const int py = s_pos[y];
+        const float2 v0 = buf[s_pos[x] * kPC + py], v1 = buf[s_pos[x + 1] * kPC + py];
+        if (p.raw) {
+          p.raw[(size_t)item * kN * kN + y * kN + x] = v0;
+          p.raw[(size_t)item * kN * kN + y * kN + x + 1] = v1;
+        }
+        const int r0 = __float2int_rn(__fmul_rn(v0.x, scale)), m0 = __float2int_rn(__fmul_rn(v0.y, scale));
+        const int r1 = __float2int_rn(__fmul_rn(v1.x, scale)), m1 = __float2int_rn(__fmul_rn(v1.y, scale));
+        fro[i] = (uint32_t)(r0 & 0xffff) | ((uint32_t)r1 << 16);
+        fio[i] = (uint32_t)(m0 & 0xffff) | ((uint32_t)m1 << 16);
+        *reinterpret_cast<uint2*>(&fq[y * kN + x]) =
+            make_uint2((uint32_t)(r0 & 0xffff) | ((uint32_t)m0 << 16), (uint32_t)(r1 & 0xffff) | ((uint32_t)m1 << 16));
+        x += 2;   // advance by 64 pairs = 3 rows + 1 pair
+        y += 3;
+        if (x >= kN) { x -= kN; y += 1; }
       }
-      const int r0 = __float2int_rn(__fmul_rn(v0.x, scale)), m0 = __float2int_rn(__fmul_rn(v0.y, scale));
-      const int r1 = __float2int_rn(__fmul_rn(v1.x, scale)), m1 = __float2int_rn(__fmul_rn(v1.y, scale));
-      fro[i] = (uint32_t)(r0 & 0xffff) | ((uint32_t)r1 << 16);
-      fio[i] = (uint32_t)(m0 & 0xffff) | ((uint32_t)m1 << 16);
-      fq[y * kN + x] = (uint32_t)(r0 & 0xffff) | ((uint32_t)m0 << 16);
-      fq[y * kN + x + 1] = (uint32_t)(r1 & 0xffff) | ((uint32_t)m1 << 16);
     }
     if (lane == 0) p.scale[item] = scale;
     if (G == 0) {
-      __syncwarp();
+      pair_sync();
       continue;
     }
-    __syncwarp();
+    pair_sync();
     // --------------------------------------------------------------------- HG overlap (SIMT)
     // U[y][m] = sum_x Fq[y][x] hx[m][x] on the integer-valued field; the dequantisation 1/scale
     // (engine.py:367-369) is applied once per coefficient.
@@ -237,7 +270,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
     const int GQ = GP >> 2;
     constexpr int CX = kN / 2, NPX = kN - 1 - CX;  // parity around the axis origin x = 21
     const bool xsym = (ft.hsym >> (2 * q)) & 1, ysym = (ft.hsym >> (2 * q + 1)) & 1;
-    for (int t = lane; t < kN * GQ; t += 32) {
+    for (int t = lane; t < kN * GQ; t += kLanes) {
       const int y = t / GQ, mq = t - y * GQ;
       const uint32_t* __restrict__ row = fq + y * kN;
       float4 ar = make_float4(0.f, 0.f, 0.f, 0.f), ai = ar;
@@ -283,11 +316,11 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
       u[2] = make_float2(ar.z, ai.z);
       u[3] = make_float2(ar.w, ai.w);
     }
-    __syncwarp();
+    pair_sync();
     const float d = __fdiv_rn(g.dxdy[q], scale);
     float2* out = p.coefs + (size_t)item * g.M;
     constexpr int CY = kN / 2, NPY = kN - 1 - CY;
-    for (int i = lane; i < g.M; i += 32) {
+    for (int i = lane; i < g.M; i += kLanes) {
       const int m = p.t.mode_m[i], n = p.t.mode_n[i];
       float ax = 0.f, ay = 0.f;
       if (ysym) {
@@ -318,7 +351,7 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
       }
       out[i] = make_float2(ax * d, ay * d);
     }
-    __syncwarp();
+    pair_sync();
   }
 }
 

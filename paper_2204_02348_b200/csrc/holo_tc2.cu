@@ -133,7 +133,8 @@ HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, 
   }
 }
 
-// wout: [items][2][42 r][42 c] float (Re plane, Im plane) of the masked window, relative to item i0
+// wout: [items][4][42 r][42 c] float, relative to item i0: the column-DFT product planes Cr Rr, Cr Ri, Ci Rr,
+// Ci Ri (unmasked); the window is W = (P0 - P3) + i (P1 + P2) inside the circular mask
 template <int FMT>
 __global__ void __launch_bounds__(kK1Threads, 1)
     fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft,
@@ -423,15 +424,14 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       tmem_wait_ld();
       tc_fence_before();
       if (ct == 0) TC2_MARK(3, k, 0);
-      // Cr rows -> the planar staging copy in the (now free) B2 buffer, Y[sub][r][c] (sub 0: Cr Rr, 1: Cr Ri);
-      // Ci rows -> X[r][sub * 48 + c]; then every consumer thread combines in place:
-      //   Y[0] = (Cr Rr - Ci Ri) gs,  Y[1] = (Cr Ri + Ci Rr) gs, masked
+      // the four product planes P[2 * (Ci row) + sub][r][c] (Cr Rr, Cr Ri, Ci Rr, Ci Ri), scaled by gs, into a
+      // dense staging copy in the (now free) B2 buffer; the tail forms W = (P0 - P3) + i (P1 + P2) and masks it
       float* Y = reinterpret_cast<float*>(b2);
       const int r = n & 63;
       if (r < kWinH) {
-        float* dst = n >= 64 ? X + r * kXP + sub * kN2 : Y + sub * (kWinH * kWinW) + r * kWinW;
+        float* dst = Y + (((n >= 64) ? 2 : 0) + sub) * (kWinH * kWinW) + r * kWinW;
 #pragma unroll
-        for (int cc = 0; cc < kWinW; ++cc) dst[cc] = __uint_as_float(v[cc]);
+        for (int cc = 0; cc < kWinW; ++cc) dst[cc] = __uint_as_float(v[cc]) * gs;
       }
       if (ct == 0) TC2_MARK(3, k, 1);
       nbar(kBarCons2, kCons2);
@@ -439,25 +439,12 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         TC2_MARK(3, k, 2);
         mbar_arrive(&d2free);   // D2 is in shared memory: the next column GEMM may start
       }
-      if (ct == 64) TC2_MARK(3, k, 6);
-      for (int i = ct; i < kWinH * kWinW; i += kCons2) {
-        const int rr = i / kWinW, cc = i - rr * kWinW;
-        const float crr = Y[i], cri = Y[kWinH * kWinW + i];
-        const float cir = X[rr * kXP + cc], cii = X[rr * kXP + kN2 + cc];
-        const bool in = rr >= crs[2 * cc] && rr <= crs[2 * cc + 1];
-        Y[i] = in ? (crr - cii) * gs : 0.f;
-        Y[kWinH * kWinW + i] = in ? (cri + cir) * gs : 0.f;
-      }
-      if (ct == 64) TC2_MARK(3, k, 7);
-      if (ct == 0) TC2_MARK(3, k, 3);
-      nbar(kBarCons2, kCons2);
-      if (ct == 0) TC2_MARK(3, k, 4);
       // ... and one bulk async copy (TMA engine, not the LSU) of both planes to the item's W
       if (ct == 0) {
         fence_async_smem();
-        float* wo = wout + (size_t)(first + k * gridDim.x - i0) * 2 * (kWinH * kWinW);
+        float* wo = wout + (size_t)(first + k * gridDim.x - i0) * 4 * (kWinH * kWinW);
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wo), "r"(smem_u32(Y)),
-                     "r"((uint32_t)(2 * kWinH * kWinW * sizeof(float)))
+                     "r"((uint32_t)(4 * kWinH * kWinW * sizeof(float)))
                      : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
@@ -503,7 +490,8 @@ struct FieldLayout {
 
 template <int WH, int WW>
 __global__ void __launch_bounds__(256, 3)
-    field128_kernel(const __grid_constant__ RunParams p, int i0, int i1, const float* __restrict__ win) {
+    field128_kernel(const __grid_constant__ RunParams p, int i0, int i1, const float* __restrict__ win,
+                    const int16_t* __restrict__ crange) {
   using LY = FieldLayout<WH, WW>;
   extern __shared__ __align__(1024) char smem[];
   __shared__ float redf[8];
@@ -550,10 +538,13 @@ __global__ void __launch_bounds__(256, 3)
       staged_q = q;
     }
     __syncthreads();
-    const float* Wp = win + (size_t)(item - i0) * 2 * WH * WW;   // planar [Re | Im][r][c]
-    for (int i = tid; i < WH * WW; i += blockDim.x) {            // -> F, column-major [c][r]
+    const float* Wp = win + (size_t)(item - i0) * 4 * WH * WW;   // product planes [4][r][c]
+    for (int i = tid; i < WH * WW; i += blockDim.x) {            // -> masked W in F, column-major [c][r]
       const int r = i / WW, c = i - r * WW;
-      F[c * WH + r] = make_float2(__ldg(Wp + i), __ldg(Wp + WH * WW + i));
+      const bool in = r >= crange[2 * c] && r <= crange[2 * c + 1];
+      F[c * WH + r] = in ? make_float2(__ldg(Wp + i) - __ldg(Wp + 3 * WH * WW + i),
+                                       __ldg(Wp + WH * WW + i) + __ldg(Wp + 2 * WH * WW + i))
+                         : make_float2(0.f, 0.f);
     }
     __syncthreads();
     // IFFT along r (y) first, then along c (x)
@@ -642,7 +633,7 @@ bool tail_supported(const Geometry& g);
 cudaError_t launch_tail(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s, int i0, int i1,
                         const float* win);
 
-constexpr int kTc2Chunk = 4096;   // items per K1/K2 pair: W (14 KB each) stays resident in L2
+constexpr int kTc2Chunk = 2048;   // items per K1/K2 pair: the product planes (28 KB each) stay in L2
 
 bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
                    const void* windows) {
@@ -656,7 +647,7 @@ bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, c
 int64_t tc2_chunk() { return kTc2Chunk; }
 
 size_t tc2_workspace(int64_t items) {
-  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 2 * 42 * 42 * sizeof(float);   // planar W
+  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 4 * 42 * 42 * sizeof(float);   // 4 product planes
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -718,7 +709,7 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
       e = launch_tail(p, ft, num_sms, s, i0, i1, wbuf);
     } else {
       field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(
-          p, i0, i1, wbuf);
+          p, i0, i1, wbuf, ft.crange);
       e = cudaGetLastError();
     }
     if (e != cudaSuccess) return e;

@@ -33,17 +33,18 @@ HOLO_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
-// every lane of the warp polls the barrier (the warp stays converged: no lane parks at a warp barrier
-// while another spins, which was measured to delay the hand-offs by ~1-5 K cycles)
+// every lane of the warp waits (converged) in a try_wait loop with a suspend-time hint, so a waiting warp
+// is parked by the hardware instead of spinning on issue slots the working warps need
 HOLO_DEV void mbar_wait_warp(uint64_t* bar, uint32_t phase) {
-  uint32_t done = 0;
-  while (!__all_sync(0xffffffffu, done)) {
-    if (!done)
-      asm volatile(
-          "{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
-          : "=r"(done)
-          : "r"(smem_u32(bar)), "r"(phase));
-  }
+  asm volatile(
+      "{.reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONE_%=;\n"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n}" ::"r"(smem_u32(bar)),
+      "r"(phase), "r"(0x989680u)
+      : "memory");
 }
 
 HOLO_DEV void tmem_st32(uint32_t taddr, const uint32_t* r) {
