@@ -193,7 +193,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows), "source": self.source, "gpu_uuid": self.uuid}
 
 
-def dist_init(n_gpus):
+def dist_init(n_gpus, need_group=False):
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,6 +204,14 @@ def dist_init(n_gpus):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     elif torch.cuda.is_available():
         torch.cuda.set_device(0)
+        if need_group:   # --split on one GPU: the same NCCL code path over a 1-rank group
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", 0))
     return rank, world, local
 
 
@@ -341,6 +349,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tc", action="store_true", help="use the tcgen05 row-pass kernel (HPG_FLAG_TC)")
     ap.add_argument("--tc2", action="store_true", help="use the two-kernel tensor-core path (HPG_FLAG_TC2)")
+    ap.add_argument("--split", action="store_true",
+                    help="strong scaling: divide the batch over WORLD_SIZE and include distributed.calc_metrics "
+                         "(NCCL all-reduce of the Gram, all-gather of the row sums) in every timed step")
+    ap.add_argument("--tile", type=int, default=0,
+                    help="generate this many distinct frames and tile them in HBM up to the batch (config 5: 1024)")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture")
     args = ap.parse_args()
@@ -349,13 +362,21 @@ def main():
         return
 
     import torch
-    rank, world, local = dist_init(args.gpus)
+    rank, world, local = dist_init(args.gpus, need_group=args.split)
     from paper_2204_02348_b200 import api, native
     from paper_2204_02348_b200.synth import FrameSpec, make_frames
 
     fspec, cfg = config_for(args.config, batch=args.batch or None)
-    B = fspec["batch"]
-    fspec = dict(fspec, seed=fspec["seed"] * 1000 + rank)
+    B_total = fspec["batch"]
+    if args.split:   # strong scaling: the batch is divided over the ranks (distributed.shard)
+        from paper_2204_02348_b200 import distributed as D
+        r0, r1 = D.shard(B_total, world, rank)
+        B = r1 - r0
+    else:            # weak scaling: every rank processes its own full batch
+        B = B_total
+    cfg = dict(cfg, batchCount=B)
+    n_distinct = min(B, args.tile) if args.tile else B
+    fspec = dict(fspec, batch=n_distinct, seed=fspec["seed"] * 1000 + rank)
     frames_host = make_frames(FrameSpec(**fspec))
     dev = torch.device("cuda", torch.cuda.current_device())
 
@@ -366,6 +387,9 @@ def main():
     for k, v in cfg.items():
         setattr(eng.config, k, v)
     frames_dev = torch.from_numpy(frames_host).to(dev)
+    if n_distinct < B:   # BASELINE config 5 at its full size: distinct frames tiled in HBM (21.5 GB at 65,536)
+        reps = -(-B // n_distinct)
+        frames_dev = frames_dev.repeat(reps, 1, 1)[:B].contiguous()
     api.set_batch(h, B, frames_dev)
     eng.run_pipeline(0)
     torch.cuda.synchronize()
@@ -380,8 +404,18 @@ def main():
     launch = eng.prepare_launch()   # one hpg_run on the resident frames, arguments pre-built
     stream_h = native.stream_handle()
 
-    def step():
-        launch.launch(stream_h)
+    metric_launches = 0
+    if args.split:   # the step includes the metric reduction over the process group (NCCL)
+        from paper_2204_02348_b200 import distributed as D
+        L_wl = len(eng.config.wavelength_list())
+        metric_launches = 2 * L_wl   # hpg_metric_partials: row + Gram kernels per wavelength
+
+        def step():
+            launch.launch(stream_h)
+            D.calc_metrics(eng, defer_mdl=True)
+    else:
+        def step():
+            launch.launch(stream_h)
 
     for _ in range(args.warmup):
         step()
@@ -402,7 +436,7 @@ def main():
     per_step = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms_local = float(np.mean(per_step))
     ms = max_over_ranks(ms_local, world)
-    value = B * world / (ms / 1e3)
+    value = (B_total if args.split else B * world) / (ms / 1e3)
     achieved = bpf * B / (ms_local / 1e3) / 1e9
     peaks = {}
     try:
@@ -462,7 +496,11 @@ def main():
 
     e2e = None
     e2e_variants = {}
-    if not args.no_e2e:
+    host_bytes = B * frames_host[0].nbytes
+    if not args.no_e2e and (host_bytes > 8e9 or args.split):
+        e2e_variants["skipped"] = (f"{host_bytes / 1e9:.1f} GB of host frames per step (device-tiled workload)"
+                                   if host_bytes > 8e9 else "split mode times the sharded device path")
+    elif not args.no_e2e:
         reps = max(5, min(args.steps, 20))
         pinned = torch.from_numpy(frames_host).pin_memory()
         e2e = time_e2e(lambda x: api.set_batch(h, B, x), pinned, reps)
@@ -513,11 +551,15 @@ def main():
         line = {
             "metric": "camera frames/sec (FFT->IFFT->HG coefs)", "value": value, "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if args.split else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (seeded HG superposition holograms, BASELINE.md section 3)",
             "config": {"workload": args.config, "frames_per_step_per_gpu": B, "frame": [fspec["height"], fspec["width"]],
                        "pols": P, "fft_window": [ny, nx], "field": [int(gh), int(gw)], "modes_per_pol": int(M),
-                       "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}"},
+                       "l2": "flushed (256 MB write) before every timed step", "parallelism": f"dp{world}",
+                       "frames_total": B_total if args.split else B * world,
+                       "distinct_frames_per_gpu": n_distinct,
+                       "metrics_in_step": "distributed.calc_metrics over NCCL (MDL deferred)" if args.split else None},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name, "bytes_per_frame": bpf,
@@ -525,14 +567,14 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_variants": e2e_variants or None,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": (launches_per_step + metric_launches) * args.steps,
             "clocks": clocks.summary(),
         }
         if autoalign is not None:
             line["autoalign"] = autoalign
         print(json.dumps(line), flush=True)
-    if world > 1:
-        import torch.distributed as dist
+    import torch.distributed as dist
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -62,14 +62,19 @@ def exclusive_prefix(count, group=None, device="cpu"):
 
 
 def reduce_and_finish(row_power, diag_power, group_power, gram, rows_global, cols, group=None,
-                      have_labels=True):
-    """Combine per-rank partials (torch tensors on the process-group device) into the metrics."""
+                      have_labels=True, defer_mdl=False):
+    """Combine per-rank partials (torch tensors on the process-group device) into the metrics.
+
+    ``defer_mdl``: leave METRIC_MDL unset and return the reduced Gram matrix as well (the eigenvalue
+    problem runs only when MDL is read, as the engine does for AutoAlign, analysis.MetricsReport.defer_mdl)."""
     import torch.distributed as dist
     dist.all_reduce(gram, group=group)
     rp = _all_gather_var(row_power, group).cpu().numpy()
     dp = _all_gather_var(diag_power, group).cpu().numpy()
     gp = _all_gather_var(group_power, group).cpu().numpy()
-    return finish_metrics(rp, dp, gp, gram.cpu().numpy(), rows_global, cols, have_labels)
+    g = gram.cpu().numpy()
+    v = finish_metrics(rp, dp, gp, g, rows_global, cols, have_labels, defer_mdl=defer_mdl)
+    return (v, g) if defer_mdl else v
 
 
 def host_partials(coefs, labels, diag_offset, ndiag):
@@ -104,6 +109,7 @@ def shard_partials(coefs, local_rows, labels, diag_offset, ndiag, dev):
     dp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
     gp = torch.full((R,), -1.0, dtype=torch.float64, device=dev)
     gram = torch.zeros((cols, cols), dtype=torch.complex128, device=dev)
+    big = R * cols * cols > (1 << 28)   # large shards: the Gram A^H A is a plain library GEMM (cuBLAS zgemm)
     if R:
         ids = torch.as_tensor(np.asarray(local_rows, np.int32), device=dev)
         a = native.MetricArgs()
@@ -113,11 +119,23 @@ def shard_partials(coefs, local_rows, labels, diag_offset, ndiag, dev):
         a.labels = labels.data_ptr()
         a.ndiag, a.diag_offset, a.gram_rows = ndiag, diag_offset, 0
         a.row_power, a.diag_power, a.group_power = rp.data_ptr(), dp.data_ptr(), gp.data_ptr()
-        a.gram = gram.data_ptr()
+        a.gram = None if big else gram.data_ptr()
         with torch.cuda.device(dev):
             native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle(dev)),
                          "hpg_metric_partials")
+            if big:
+                gram_of_rows(coefs, ids.long(), gram)
     return rp, dp, gp, gram
+
+
+def gram_of_rows(coefs, ids, out, chunk=8192):
+    """out = A^H A for A = coefs[ids] in complex128 (the MDL Gram of hpg_metric_partials, analysis.py:158-162),
+    accumulated over row chunks with cuBLAS zgemm."""
+    import torch
+    for s0 in range(0, ids.numel(), chunk):
+        A = coefs.index_select(0, ids[s0:s0 + chunk]).to(torch.complex128)
+        out.addmm_(A.conj().T, A)
+    return out
 
 
 def mode_labels(P, M, dev):
@@ -135,13 +153,14 @@ def wavelength_of_rows(rows, B, cfg):
     return np.minimum(rows * L // B, L - 1)
 
 
-def calc_metrics(eng, group=None):
+def calc_metrics(eng, group=None, defer_mdl=False):
     """Transfer-matrix metrics of a batch sharded over the process group.
 
     ``eng`` holds this rank's rows (a contiguous shard; its global row offset is the
     sum of the lower ranks' row counts); wavelength membership follows the global
     row index (holopipe/engine.py:102-106).  Returns the MetricsReport, identical on
-    every rank.  Pol-independent / A A^H variants are single-process only.
+    every rank.  Pol-independent / A A^H variants are single-process only.  ``defer_mdl``: MDL is
+    resolved from the reduced Gram matrices on its first read (MetricsReport.defer_mdl).
     """
     cfg = eng.config
     dev = eng.device
@@ -154,11 +173,20 @@ def calc_metrics(eng, group=None):
     wl = wavelength_of_rows(np.arange(start, start + B_local), B, cfg)
     labels = mode_labels(P, M, dev)
     per = np.full((C.METRIC_COUNT, L), C.METRIC_UNSET)
+    pending = []
     for w in range(L):
         local = np.nonzero(wl == w)[0]
         off, n_w = exclusive_prefix(local.size, group, device=dev)
         if n_w == 0:
             continue
         rp, dp, gp, gram = shard_partials(coefs, local, labels, off, min(n_w, cols), dev)
-        per[:, w] = reduce_and_finish(rp, dp, gp, gram, n_w, cols, group)
-    return average_slot(per)
+        out = reduce_and_finish(rp, dp, gp, gram, n_w, cols, group, defer_mdl=defer_mdl)
+        if defer_mdl:
+            per[:, w], g = out
+            pending.append((w, g, min(n_w, cols)))
+        else:
+            per[:, w] = out
+    rep = average_slot(per)
+    if defer_mdl:
+        rep.defer_mdl(pending)
+    return rep

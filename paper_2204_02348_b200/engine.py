@@ -297,6 +297,8 @@ class Engine:
         host = src.host_array() if src._pinned is None else None
         if host is not None and not (src.format() == 1 and src.transpose):
             torch = _torch()
+            with torch.cuda.device(self.device):
+                src.ensure_registered()   # pageable numpy sources: page-locked in place, once per buffer
             st0 = self._st0
             fmt = src.format()
             need = F * st0["W"] * st0["H"]
@@ -1058,10 +1060,16 @@ class Engine:
         a.ndiag, a.diag_offset, a.gram_rows = min(R, cols), 0, gram_rows
         base = packed.data_ptr()
         a.row_power, a.diag_power, a.group_power = base, base + 8 * R, base + 16 * R
-        a.gram = base + 8 * r3
+        big = not gram_rows and R * cols * cols > (1 << 28)   # large batches: Gram by cuBLAS zgemm
+        a.gram = None if big else base + 8 * r3
         with torch.cuda.device(dev):
             native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle(dev)),
                          "hpg_metric_partials")
+            if big:
+                from .distributed import gram_of_rows
+                gview = packed[r3:].view(torch.complex128).view(n, n)
+                gview.zero_()
+                gram_of_rows(self._coefs, t_rows.long(), gview)
         host = packed.cpu().numpy()
         gram = host[r3:].view(np.complex128).reshape(n, n)
         v = finish_metrics(host[:R], host[R:2 * R], host[2 * R:3 * R], gram, R, cols, True,

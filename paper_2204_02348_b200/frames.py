@@ -32,6 +32,7 @@ class FrameSource:
         self.transpose = 0
         self._dev = None          # reusable device staging buffer
         self._pinned = None       # device copy frozen by freeze() (AutoAlign)
+        self._reg = None          # (ptr, nbytes) of a pageable host source registered with the driver
 
     def set_float32(self, buffer):
         if buffer is None:
@@ -40,6 +41,7 @@ class FrameSource:
             buffer = np.asarray(buffer, dtype=np.float32)
         elif buffer.dtype != __import__("torch").float32:
             buffer = buffer.float()
+        self._release_if_other(buffer)
         self.kind, self.f32, self.u16, self._pinned = SOURCE_FLOAT32, buffer, None, None
 
     def set_uint16(self, buffer, transpose_mode=0):
@@ -48,6 +50,7 @@ class FrameSource:
         if not _is_torch(buffer):
             arr = np.asarray(buffer)
             buffer = arr if arr.dtype == np.uint16 else arr.astype(np.uint16)
+        self._release_if_other(buffer)
         self.kind, self.u16, self.f32, self._pinned = SOURCE_UINT16, buffer, None, None
         self.transpose = 1 if transpose_mode else 0
 
@@ -57,6 +60,7 @@ class FrameSource:
         if not os.path.isfile(path):
             raise HoloError(ErrorCode.FILENOTFOUND, path)
         raw = np.fromfile(path, dtype="<u2")
+        self._unregister()
         self.kind, self.u16, self.f32, self._pinned = SOURCE_FILE, raw, None, None
         self.transpose = 0
 
@@ -115,6 +119,51 @@ class FrameSource:
         if self.kind == SOURCE_FLOAT32 and arr.dtype != np.float32:
             return None
         return arr
+
+    def ensure_registered(self):
+        """Page-lock the current pageable host source in place (cudaHostRegister) so that the window
+        uploads run at pinned-memory speed.  holopipe holds the caller's frame buffer by reference and
+        re-reads it on every run (holopipe/frames.py:40-47), so the registration is made once per buffer
+        and released when the source changes (or this object is collected).  A failed registration
+        leaves the buffer pageable (correct, slower)."""
+        arr = self.host_array()
+        if arr is None or _is_torch(arr):
+            return
+        ptr, nbytes = arr.ctypes.data, arr.nbytes
+        if self._reg == (ptr, nbytes) or nbytes == 0:
+            return
+        self._unregister()
+        import torch
+        try:
+            rc = torch.cuda.cudart().cudaHostRegister(ptr, nbytes, 0)
+            if int(rc) == 0:
+                self._reg = (ptr, nbytes)
+        except Exception:
+            self._reg = None
+
+    def _release_if_other(self, buffer):
+        """Keep the registration when the same host buffer is set again (a caller re-arming its batch)."""
+        if self._reg is None:
+            return
+        if not _is_torch(buffer) and isinstance(buffer, np.ndarray) and buffer.flags["C_CONTIGUOUS"] \
+                and (buffer.ctypes.data, buffer.nbytes) == self._reg:
+            return
+        self._unregister()
+
+    def _unregister(self):
+        if self._reg is not None:
+            import torch
+            try:
+                torch.cuda.cudart().cudaHostUnregister(self._reg[0])
+            except Exception:
+                pass
+            self._reg = None
+
+    def __del__(self):
+        try:
+            self._unregister()
+        except Exception:
+            pass
 
     def freeze(self, tensor):
         """Keep a device copy for repeated evaluations (no external mutation expected)."""

@@ -87,3 +87,33 @@ def test_calc_metrics_over_nccl_world1(nccl_world1):
     rep = D.calc_metrics(eng)
     got = np.stack([rep.get_all(i) for i in range(C.METRIC_COUNT)])
     assert np.allclose(got, g["metrics"], atol=METRIC_TOL_DB, rtol=0), np.abs(got - g["metrics"]).max()
+
+
+def test_large_shard_gram_by_library_gemm_matches_native_kernel():
+    """Shards with rows * cols^2 > 2^28 take the MDL Gram from cuBLAS zgemm (distributed.gram_of_rows);
+    it equals hpg_metric_partials' own fp64 Gram kernel."""
+    import ctypes
+    import torch
+    from paper_2204_02348_b200 import distributed as D
+    from paper_2204_02348_b200 import native
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device="cpu").manual_seed(7)
+    R, cols = 2100, 360
+    coefs = torch.complex(torch.randn(R, cols, generator=g), torch.randn(R, cols, generator=g)).to(dev)
+    labels = D.mode_labels(1, cols, dev)
+    rows = np.arange(R)
+    rp, dp, gp, gram = D.shard_partials(coefs, rows, labels, 0, cols, dev)   # big: library GEMM
+    assert R * cols * cols > (1 << 28)
+    ref = torch.zeros((cols, cols), dtype=torch.complex128, device=dev)
+    ids = torch.as_tensor(rows.astype(np.int32), device=dev)
+    a = native.MetricArgs()
+    a.coefs, a.rows, a.cols, a.ld = coefs.data_ptr(), R, cols, cols
+    a.row_ids, a.labels = ids.data_ptr(), labels.data_ptr()
+    a.ndiag, a.diag_offset, a.gram_rows = cols, 0, 0
+    tmp = torch.zeros(3 * R, dtype=torch.float64, device=dev)
+    a.row_power, a.diag_power, a.group_power = tmp.data_ptr(), tmp.data_ptr() + 8 * R, tmp.data_ptr() + 16 * R
+    a.gram = ref.data_ptr()
+    native.check(native.lib().hpg_metric_partials(ctypes.byref(a), native.stream_handle(dev)), "partials")
+    torch.cuda.synchronize()
+    assert torch.allclose(gram, ref, rtol=1e-10, atol=1e-9 * ref.abs().max().item())
+    assert torch.allclose(rp, tmp[:R])
