@@ -233,6 +233,13 @@ int hpg_coef_transform(const void* coefs, int64_t rows, int32_t pols, int32_t mo
 int hpg_upload_windows(const hpg_plan* plan, const void* host_frames, int32_t frame_format,
                        int64_t frame_count, void* dst, void* stream);
 
+/* Page-lock a pageable host frame buffer in place (cudaHostRegister) so that hpg_upload_windows runs at
+ * pinned-memory speed; holopipe re-reads the caller's buffer on every run (holopipe/frames.py:40-47), so a
+ * caller registers it once and unregisters it when the buffer is replaced.  A range that is already
+ * page-locked returns HPG_INVALIDARGUMENT and is left as it is (no sticky runtime error either way). */
+int hpg_host_register(void* ptr, size_t bytes);
+int hpg_host_unregister(void* ptr);
+
 const char* hpg_last_error(void);
 
 #ifdef __cplusplus

@@ -952,3 +952,19 @@ int hpg_extract_coefs(const hpg_plan* P, const int16_t* fr, const int16_t* fi, c
 }
 
 }  // extern "C"
+
+extern "C" int hpg_host_register(void* ptr, size_t bytes) {
+  if (!ptr || bytes == 0) return HPG_NULLPOINTER;
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+  if (e == cudaSuccess) return HPG_SUCCESS;
+  cudaGetLastError();   // not sticky: clear it so later calls do not report it
+  return e == cudaErrorHostMemoryAlreadyRegistered ? HPG_INVALIDARGUMENT : fail(HPG_ERROR, cudaGetErrorString(e));
+}
+
+extern "C" int hpg_host_unregister(void* ptr) {
+  if (!ptr) return HPG_NULLPOINTER;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e == cudaSuccess) return HPG_SUCCESS;
+  cudaGetLastError();
+  return HPG_INVALIDARGUMENT;
+}

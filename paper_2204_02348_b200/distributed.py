@@ -129,12 +129,13 @@ def shard_partials(coefs, local_rows, labels, diag_offset, ndiag, dev):
 
 
 def gram_of_rows(coefs, ids, out, chunk=8192):
-    """out = A^H A for A = coefs[ids] in complex128 (the MDL Gram of hpg_metric_partials, analysis.py:158-162),
-    accumulated over row chunks with cuBLAS zgemm."""
+    """out[i][j] = sum_k A[k][i] conj(A[k][j]) for A = coefs[ids] in complex128 -- the MDL Gram exactly as
+    hpg_metric_partials lays it out (analysis.py:158-162; conj(A^H A), same eigenvalues) -- accumulated over
+    row chunks with cuBLAS zgemm."""
     import torch
     for s0 in range(0, ids.numel(), chunk):
         A = coefs.index_select(0, ids[s0:s0 + chunk]).to(torch.complex128)
-        out.addmm_(A.conj().T, A)
+        out.addmm_(A.T, A.conj())
     return out
 
 

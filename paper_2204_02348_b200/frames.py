@@ -130,16 +130,13 @@ class FrameSource:
         if arr is None or _is_torch(arr):
             return
         ptr, nbytes = arr.ctypes.data, arr.nbytes
-        if self._reg == (ptr, nbytes) or nbytes == 0:
+        if self._reg == (ptr, nbytes) or getattr(self, "_tried", None) == (ptr, nbytes) or nbytes == 0:
             return
         self._unregister()
-        import torch
-        try:
-            rc = torch.cuda.cudart().cudaHostRegister(ptr, nbytes, 0)
-            if int(rc) == 0:
-                self._reg = (ptr, nbytes)
-        except Exception:
-            self._reg = None
+        from . import native
+        self._tried = (ptr, nbytes)   # one attempt per buffer (an already page-locked range stays as it is)
+        if native.lib().hpg_host_register(ptr, nbytes) == 0:
+            self._reg = (ptr, nbytes)
 
     def _release_if_other(self, buffer):
         """Keep the registration when the same host buffer is set again (a caller re-arming its batch)."""
@@ -152,11 +149,8 @@ class FrameSource:
 
     def _unregister(self):
         if self._reg is not None:
-            import torch
-            try:
-                torch.cuda.cudart().cudaHostUnregister(self._reg[0])
-            except Exception:
-                pass
+            from . import native
+            native.lib().hpg_host_unregister(self._reg[0])
             self._reg = None
 
     def __del__(self):

@@ -33,7 +33,7 @@ EXPORTS = [
     "hpg_plan_get_basis", "hpg_workspace_size", "hpg_run", "hpg_finalize_summary",
     "hpg_fourier_full", "hpg_extract_coefs", "hpg_ref_calibration_finish", "hpg_metric_partials", "hpg_plane_summary",
     "hpg_plane_summary_workspace", "hpg_field_intensity", "hpg_upload_windows", "hpg_last_error",
-    "hpg_last_launch_count", "hpg_coef_transform",
+    "hpg_last_launch_count", "hpg_coef_transform", "hpg_host_register", "hpg_host_unregister",
 ]
 
 
@@ -128,6 +128,8 @@ def lib():
     L.hpg_plane_summary_workspace.argtypes = [c_int64, c_int32, c_int32, c_int32]
     L.hpg_ref_calibration_finish.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, c_void_p]
     L.hpg_upload_windows.argtypes = [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p]
+    L.hpg_host_register.argtypes = [c_void_p, c_size_t]
+    L.hpg_host_unregister.argtypes = [c_void_p]
     for name in EXPORTS:
         getattr(L, name).restype = c_int32
     L.hpg_last_error.restype = ctypes.c_char_p

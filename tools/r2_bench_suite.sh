@@ -4,7 +4,7 @@ cd "$(dirname "$0")/.."
 timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/r2_suite_dualpol.json 2> gpurun_out/r2_suite_dualpol.err; echo "dualpol rc=$?"
 timeout 600 python bench.py --config largebasis --batch 65536 --tile 1024 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r2_suite_lb65536.json 2> gpurun_out/r2_suite_lb65536.err; echo "lb65536 rc=$?"
 timeout 600 python bench.py --config largebasis --batch 65536 --tile 1024 --split --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/r2_suite_lb_split.json 2> gpurun_out/r2_suite_lb_split.err; echo "split rc=$?"
-timeout 300 python -m pytest tests/test_autoalign_gpu.py tests/test_sharded_metrics_gpu.py tests/test_api_benchmark.py -q -s 2>&1 | grep -E "deviation|passed|failed" > gpurun_out/r2_suite_tests.txt
+timeout 300 python -m pytest tests/test_autoalign_gpu.py tests/test_sharded_metrics_gpu.py tests/test_api_benchmark.py tests/test_gpu_parity.py -q -s -k "not fields_and_coefs" 2>&1 | grep -E "deviation|passed|failed" > gpurun_out/r2_suite_tests.txt
 cat gpurun_out/r2_suite_tests.txt
 for f in dualpol lb65536 lb_split; do python - "$f" <<'PY'
 import json, sys
