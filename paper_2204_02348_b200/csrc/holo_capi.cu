@@ -352,8 +352,36 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
     }
   }
   if (a2_tc.empty()) a2_tc.push_back(0u);
+  // column DFT as the B operand of holo_tc2.cu's column GEMM (the data, the row-DFT accumulator converted to
+  // fp16 in TMEM, is the A operand): B[n][y] in the canonical K-major no-swizzle shared-memory layout,
+  // rows n < 48 -> Cr[r = n][y], rows 48 + r -> Ci[r][y] (zero for r >= wh), hi part then lo part,
+  // [kstep 8][row/8 12][khalf 2][row%8 8][8 halves] = 24 KB per part.
+  std::vector<uint16_t> c2_tc;
+  if (g.ny == 128 && g.wh <= 48) {
+    const size_t part = 8 * 12 * 2 * 8 * 8;   // halves per part
+    c2_tc.assign((size_t)g.P * 2 * part, 0);
+    for (int q = 0; q < g.P; ++q) {
+      const int ky = g.k0[q][0][1];
+      for (int n = 0; n < 96; ++n) {
+        const int r = n % 48;
+        if (r >= g.wh) continue;
+        const double kr = (double)(ky + r - g.wh / 2);
+        for (int y = 0; y < 128; ++y) {
+          const double ang = -2.0 * kPi * kr * ((double)y - xi[q][1] + g.ny / 2.0) / g.ny;
+          const double v = n < 48 ? std::cos(ang) : std::sin(ang);
+          const __half h = __double2half(v);
+          const __half l = __double2half(v - (double)__half2float(h));
+          const size_t off = (size_t)(y >> 4) * (12 * 128) + ((size_t)(n >> 3) * 2 + ((y >> 3) & 1)) * 64 +
+                             (size_t)(n & 7) * 8 + (y & 7);   // kmaj_off in halves
+          c2_tc[((size_t)q * 2 + 0) * part + off] = __half_as_ushort(h);
+          c2_tc[((size_t)q * 2 + 1) * part + off] = __half_as_ushort(l);
+        }
+      }
+    }
+  }
+  if (c2_tc.empty()) c2_tc.push_back(0);
   std::vector<char> blob;
-  const size_t o1 = push(blob, a_tc), o2 = push(blob, a2_tc);
+  const size_t o1 = push(blob, a_tc), o2 = push(blob, a2_tc), o3 = push(blob, c2_tc);
   cudaError_t e = pool_alloc(P->device, blob.size(), &P->tc_dev);
   if (e != cudaSuccess) { P->tc_dev = nullptr; return e; }
   P->tc_bytes = blob.size();
@@ -361,6 +389,7 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
   if (e != cudaSuccess) return e;
   P->ft.a_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o1);
   P->ft.a2_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o2);
+  P->ft.c2_tc = reinterpret_cast<const uint4*>(static_cast<char*>(P->tc_dev) + o3);
   return cudaSuccess;
 }
 
@@ -636,6 +665,7 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   (void)o_unused;
   P->ft.a_tc = nullptr;    // tensor-core DFT matrices: built on first use (ensure_tc_tables)
   P->ft.a2_tc = nullptr;
+  P->ft.c2_tc = nullptr;
   P->ft.tco_img = tco_ok ? reinterpret_cast<const uint4*>(base + o_timg) : nullptr;
   P->ft.tco_inv = reinterpret_cast<const float*>(base + o_tinv);
   P->ft.tco_gp = tco_ok ? GP16 : 0;

@@ -1,22 +1,23 @@
 // Two-kernel tensor-core path for the 128-window / 42x42 geometry (sm_100a).
 //
-// K1  fourier128_tc2_kernel   frames -> masked, recentred Fourier window W (42 x 42), planar
+// K1  fourier128_tc2_kernel   frames -> the four column-DFT product planes of the Fourier window
 //     Both DFTs of the crop are GEMMs on the 5th-generation tensor cores:
-//       row DFT     D1[n][y]   = sum_x A1[n][x] f[y][x]          M=128 N=64 (per half) K=128
+//       row DFT     D1[c'][y] = sum_x A1[c'][x] f[y][x]       M=128 N=128 K=128   A1 const (TMEM), f (SMEM)
 //                   A1 = [Re; Im] exp(-2 pi i kx_c (x - xi_x + nx/2)/nx)   (recentring folded in)
-//       column DFT  D2[m][c']  = sum_y A2[m][y] B2[c'][y]        M=128 N=96 K=128 (two K halves)
-//                   A2 = [Cr; Ci], C[r][y] = exp(-2 pi i ky_r (y - xi_y + ny/2)/ny), B2 = [Re R | Im R]
-//       W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr), masked (holopipe/pipeline.py:72-127)
+//       column DFT  D2[c'][n] = sum_y D1[c'][y] C2[n][y]      M=128 N=96  K=128   D1 (TMEM, converted to fp16
+//                   hi/lo in place), C2 = [Cr; Ci] const (SMEM), C[r][y] = exp(-2 pi i ky_r (y - xi_y + ny/2)/ny)
+//       lanes c' = c carry Re R, lanes 64 + c carry Im R; columns r carry Cr, 48 + r carry Ci, so D2 holds
+//       Cr Rr, Ci Rr, Cr Ri, Ci Ri; the tail forms W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr) and masks it
+//       (holopipe/pipeline.py:72-127).
 //     fp32-class precision from fp16 hi/lo operand splits (3 products, fp32 accumulation) with exact
-//     power-of-two scalings (per-row for the row DFT operand, per-window for the column operand).
-//     TMEM (512 columns): A1 hi|lo [0,128)  A2 hi|lo [128,256)  D1 [256,384)  D2 [384,480).
+//     power-of-two scalings (per row for the row-DFT operand, per window for the column-DFT operand).
+//     TMEM (512 columns): A1 hi|lo [0,128)  D1 x2 [128,384) (double-buffered)  D2 [384,480).
 //     Warp roles (one CTA per SM, persistent, every CTA owns one pol):
 //       warps 0-7   producers: landed half window -> per-row 2^k scale -> fp16 hi/lo row-DFT operand
-//       warp  8     MMA issuer: S1(k,0) S1(k,1) | S2(k,0) S1(k+1,0) S2(k,1) S1(k+1,1) | ...
+//       warp  8     MMA issuer: S1(0) | S1(k+1) S2(k) ... (the row GEMM runs one window ahead)
 //       warp  9     TMA issuer: half windows into a 3-slot landing ring (two halves ahead)
-//       warps 10-17 consumers: D1 half -> column operand B2 (K-major, scaled to a common exponent);
-//                   D2 -> W through a one-sided exchange, the consumer draining the next window's first
-//                   D1 half while the column GEMM of this window still runs
+//       warps 10-17 consumers: D1(k) -> fp16 hi/lo in TMEM (the column GEMM's A operand, no shared-memory
+//                   round trip); D2(k) -> the product planes, coalesced stores (lanes = window columns)
 // K2  tail (holo_tail.cu, or field128_kernel below): W -> 42x42 IFFT, removal phase, calibrations,
 //     int16 packing, HG overlap.  W lives in the workspace between the two launches; batches are
 //     processed in chunks small enough for W to stay resident in L2.
@@ -40,8 +41,8 @@ constexpr int kTmaWarp = 9;                 // TMA issuer
 constexpr int kConsWarp0 = 10;              // consumers: warps 10-17
 constexpr int kCons2 = 256;
 constexpr int kK1Threads = kProd2 + 64 + kCons2;
-constexpr int kBarProd2 = 1, kBarCons2 = 2;
-constexpr int kN2 = 48;                     // column-DFT N per real part (42 columns, padded)
+constexpr int kBarProd2 = 1, kBarCons2 = 2, kBarSub0 = 3;   // kBarSub0 + sub: the 4 warps of one K half
+constexpr int kN2 = 48;                     // column-DFT N per real part (42 rows, padded)
 constexpr int kWinW = 42, kWinH = 42;
 constexpr int kSlots = 3;                   // landing ring: half windows
 
@@ -51,15 +52,12 @@ constexpr uint32_t kSlot = 8 * kBox;               // one half window: [chunk 2]
 constexpr uint32_t kLand = 0;                      // [slot 3][half window]
 constexpr uint32_t kStage = kSlots * kSlot;        // row-DFT operand, N = 128 rows: [hi 32 KB | lo 32 KB]
 constexpr uint32_t kStageHalf = 32768;
-constexpr uint32_t kB2 = kStage + 2 * kStageHalf;  // B2 hi | B2 lo: rows c (Re R), 48 + c (Im R)
-constexpr uint32_t kB2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
-constexpr uint32_t kXP = 97;                       // exchange pitch (floats): Ci-row products [r][96]
-constexpr uint32_t kX = kB2 + 2 * kB2Part;
-constexpr uint32_t kFac = (kX + kWinH * kXP * 4 + 15) & ~15u;   // fac[2][128] f32 (16-byte aligned)
+constexpr uint32_t kC2 = kStage + 2 * kStageHalf;  // column-DFT constant [Cr; Ci]: hi | lo
+constexpr uint32_t kC2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
+constexpr uint32_t kFac = kC2 + 2 * kC2Part;       // fac[2][128] f32
 constexpr uint32_t kErow = kFac + 2 * 128 * 4;     // e_row[128] int
-constexpr uint32_t kCr = kErow + 128 * 4;          // crange[42][2] int
-constexpr uint32_t kK1Bytes = kCr + 2 * 48 * 4;
-static_assert(kK1Bytes <= 227 * 1024 - 512, "K1 shared memory");
+constexpr uint32_t kK1Bytes = kErow + 128 * 4;
+static_assert(kK1Bytes <= 227 * 1024 - 1024, "K1 shared memory");
 
 // canonical K-major, no-swizzle operand layout: [kstep][row/8][khalf][row%8][8 halves]
 HOLO_DEV uint32_t kmaj_off(int row, int k, int ngroups) {
@@ -140,18 +138,17 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft,
                           const __grid_constant__ CUtensorMap tmap, int i0, int i1, float* __restrict__ wout) {
   extern __shared__ __align__(1024) char smem[];
-  // landfull/landfree[slot]: TMA ring; staged[h]: stage half h written; stfree[h]: row GEMM half h done with
-  // it; meta[s]: fac[s] ready; facfree[s]: fac[s] consumed; d1full[h]: row GEMM half h done; b2ready[h]: D1
-  // half h drained into B2 half h (D1 half h free); b2free[h]: column GEMM K-half h done with B2 half h;
+  // landfull/landfree[slot]: TMA ring; staged[h]: stage half h written; stfree[h]: row GEMM done with the
+  // stage; meta[s]: fac[s] ready; facfree[s]: fac[s] consumed; d1full[b]: row GEMM into D1 buffer b done;
+  // a2ready[b][h]: K half h of the converted D1 buffer b ready; d1free[b]: column GEMM done with D1 buffer b;
   // d2full: column GEMM done; d2free: D2 drained
   __shared__ __align__(8) uint64_t landfull[kSlots], landfree[kSlots], staged[2], stfree[2], meta[2], facfree[2],
-      d1full[2], b2ready[2], b2free[2], d2full, d2free;
+      d1full[2], a2ready[2][2], d1free[2], d2full, d2free;
   __shared__ uint32_t tbase;
   __shared__ int emaxw[8];
   __shared__ int emaxs[2];
   float* fac = reinterpret_cast<float*>(smem + kFac);
   int* erow = reinterpret_cast<int*>(smem + kErow);
-  int* crs = reinterpret_cast<int*>(smem + kCr);
   const Geometry& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int first = i0 + blockIdx.x;
@@ -177,38 +174,43 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       mbar_init(&meta[i], 1);
       mbar_init(&facfree[i], 1);
       mbar_init(&d1full[i], 1);
-      mbar_init(&b2ready[i], 1);
-      mbar_init(&b2free[i], 1);
+      mbar_init(&a2ready[i][0], 1);
+      mbar_init(&a2ready[i][1], 1);
+      mbar_init(&d1free[i], 1);
     }
     mbar_init(&d2full, 1);
     mbar_init(&d2free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  for (int i = tid; i < 2 * kWinW; i += blockDim.x) crs[i] = ft.crange[i];
+  {   // the column-DFT constant of this CTA's pol into shared memory (48 KB, coalesced 16-byte loads)
+    const uint4* src = ft.c2_tc + (size_t)q * (2 * kC2Part / 16);
+    uint4* dst = reinterpret_cast<uint4*>(smem + kC2);
+    if (nk > 0)
+      for (int i = tid; i < (int)(2 * kC2Part / 16); i += blockDim.x) dst[i] = __ldg(src + i);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tm = tbase;
-  const uint32_t tA1 = tm, tA2 = tm + 128, tD1 = tm + 256, tD2 = tm + 384;
-  {   // constant DFT matrices of this CTA's pol into TMEM: A1 by warps 0-3, A2 by warps 4-7
-    const int part_warp = warp & 3;
-    if (warp < 8 && nk > 0) {
-      const uint32_t* src = (warp < 4 ? ft.a_tc : ft.a2_tc) + (size_t)q * 2 * 64 * 128 + part_warp * 32 + lane;
-      const uint32_t dst = (warp < 4 ? tA1 : tA2) + ((uint32_t)(part_warp * 32) << 16);
-      uint32_t r[32];
+  const uint32_t tA1 = tm, tD2 = tm + 384;
+  auto tD1 = [&](int k) { return tm + 128 + 128 * (uint32_t)(k & 1); };
+  if (warp < 4 && nk > 0) {   // row-DFT constant of this CTA's pol into TMEM (column-major table: coalesced)
+    const uint32_t* src = ft.a_tc + (size_t)q * 2 * 64 * 128 + warp * 32 + lane;
+    const uint32_t dst = tA1 + ((uint32_t)(warp * 32) << 16);
+    uint32_t r[32];
 #pragma unroll
-      for (int part = 0; part < 2; ++part) {
+    for (int part = 0; part < 2; ++part) {
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t* s2 = src + ((size_t)part * 64 + hh * 32) * 128;   // column-major: coalesced
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t* s2 = src + ((size_t)part * 64 + hh * 32) * 128;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
-          tmem_st32(dst + part * 64 + hh * 32, r);
-        }
+        for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
+        tmem_st32(dst + part * 64 + hh * 32, r);
       }
-      tmem_wait_st();
     }
+    tmem_wait_st();
   }
+  fence_async_smem();   // C2 written by generic stores, read by the tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -223,7 +225,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       for (int h = 0; h < 2; ++h) {   // half h = rows 64h..64h+63; warp w -> rows 64h + 8w + r8
         const int jh = 2 * k + h, slot = jh % kSlots;
         if (tid == 0) TC2_MARK(0, k, 4 * h + 0);
-        if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM half h of k-1 done with the stage
+        if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM of k-1 done with the stage
         if (tid == 0) TC2_MARK(0, k, 4 * h + 1);
         mbar_wait_warp(&landfull[slot], (jh / kSlots) & 1);
         if (tid == 0) TC2_MARK(0, k, 4 * h + 2);
@@ -284,8 +286,8 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       for (int o = 16; o; o >>= 1) emax_t = max(emax_t, __shfl_xor_sync(0xffffffffu, emax_t, o));
       if (lane == 0) emaxw[warp] = emax_t;
       nbar(kBarProd2, kProd2);
-      if (k >= 2) mbar_wait_warp(&facfree[s], ((k >> 1) - 1) & 1);   // drains of window k-2 done with fac[s]
-      if (tid < 128) {   // column-operand scale per row: B2 = D1 * 2^(e_y - e_max - 6) = R * 2^(8 - e_max)
+      if (k >= 2) mbar_wait_warp(&facfree[s], ((k >> 1) - 1) & 1);   // conversion of window k-2 done with fac[s]
+      if (tid < 128) {   // column-operand scale per row: D1 * 2^(e_y - e_max - 6) = R * 2^(8 - e_max) < 2^15
         int em = emaxw[0];
 #pragma unroll
         for (int j = 1; j < 8; ++j) em = max(em, emaxw[j]);
@@ -296,7 +298,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       nbar(kBarProd2, kProd2);
       if (tid == 0) {
         mbar_arrive(&meta[s]);
-        TC2_MARK(2, k, 2);   // (row_gemm's entry mark is overwritten: slot 2 = meta arrive time)
+        TC2_MARK(2, k, 2);
       }
     }
   } else if (warp == kTmaWarp) {
@@ -310,160 +312,127 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   } else if (warp == kMmaWarp) {
     // ================================ MMA issuer ================================
     const uint32_t idesc1 = idesc_f16(128, 128), idesc2 = idesc_f16(128, 2 * kN2);
-    // row GEMM over the whole window (N = 128: 24 MMAs; two N = 64 halves cost 48 MMAs, each bounded by
-    // its 4 KB TMEM A-operand read rather than by N -- measured 1.4 K cycles per half vs ~1.75 K in one)
-    auto row_gemm = [&](int k) {
+    auto row_gemm = [&](int k) {   // D1(k) = A1 * stage, N = 128 (24 MMAs)
       mbar_wait_warp(&staged[0], k & 1);
-      if (lane == 0) TC2_MARK(2, k, 3);
       mbar_wait_warp(&staged[1], k & 1);
-      if (k >= 1) mbar_wait_warp(&b2ready[1], (k - 1) & 1);   // D1 of k-1 drained (both halves, in order)
+      if (k >= 2) mbar_wait_warp(&d1free[k & 1], ((k >> 1) - 1) & 1);   // column GEMM of k-2 done with it
       if (lane == 0) TC2_MARK(2, k, 0);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t sb = smem_u32(smem + kStage);
+        const uint32_t sb = smem_u32(smem + kStage), d = tD1(k);
 #pragma unroll
         for (int gk = 0; gk < 8; ++gk) {
           const uint64_t bh = umma_desc(sb + gk * 4096, 128, 256);
           const uint64_t bl = umma_desc(sb + 32768 + gk * 4096, 128, 256);
-          mma_f16_ts(tD1, tA1 + gk * 8, bh, idesc1, gk != 0);
-          mma_f16_ts(tD1, tA1 + 64 + gk * 8, bh, idesc1, 1);
-          mma_f16_ts(tD1, tA1 + gk * 8, bl, idesc1, 1);
+          mma_f16_ts(d, tA1 + gk * 8, bh, idesc1, gk != 0);
+          mma_f16_ts(d, tA1 + 64 + gk * 8, bh, idesc1, 1);
+          mma_f16_ts(d, tA1 + gk * 8, bl, idesc1, 1);
         }
         tc_commit(&stfree[0]);
         tc_commit(&stfree[1]);
-        tc_commit(&d1full[0]);
-        tc_commit(&d1full[1]);
+        tc_commit(&d1full[k & 1]);
         TC2_MARK(2, k, 1);
       }
       __syncwarp();
     };
-    auto col_gemm = [&](int k, int h) {   // D2 (+)= A2[:, K-half h] * B2 half h, N = 96
-      mbar_wait_warp(&b2ready[h], k & 1);
+    auto col_gemm = [&](int k, int h) {   // D2 (+)= D1(k)[:, K half h] (fp16 hi/lo in TMEM) * C2, N = 96
+      // per D1 buffer: the consumer may convert window k + 1 before this wait, never window k + 2
+      mbar_wait_warp(&a2ready[k & 1][h], (k >> 1) & 1);
       if (h == 0 && k >= 1) mbar_wait_warp(&d2free, (k - 1) & 1);
       if (lane == 0) TC2_MARK(2, k, 4 + 2 * h);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t sb = smem_u32(smem + kB2);
+        const uint32_t sb = smem_u32(smem + kC2), a = tD1(k);
 #pragma unroll
-        for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {
-          const uint32_t o = ks * 3072;
-          const uint64_t rh = umma_desc(sb + o, 128, 256), rl = umma_desc(sb + kB2Part + o, 128, 256);
-          mma_f16_ts(tD2, tA2 + ks * 8, rh, idesc2, ks != 0);
-          mma_f16_ts(tD2, tA2 + 64 + ks * 8, rh, idesc2, 1);
-          mma_f16_ts(tD2, tA2 + ks * 8, rl, idesc2, 1);
+        for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {   // K-step ks: hi at column 32 (ks/2) + 8 (ks%2), lo +16
+          const uint32_t ah = a + 32 * (ks >> 1) + 8 * (ks & 1), al = ah + 16;
+          const uint64_t bh = umma_desc(sb + ks * 3072, 128, 256), bl = umma_desc(sb + kC2Part + ks * 3072, 128, 256);
+          mma_f16_ts(tD2, ah, bh, idesc2, ks != 0);
+          mma_f16_ts(tD2, al, bh, idesc2, 1);
+          mma_f16_ts(tD2, ah, bl, idesc2, 1);
         }
-        tc_commit(&b2free[h]);
-        if (h == 1) tc_commit(&d2full);
+        if (h == 1) {
+          tc_commit(&d2full);
+          tc_commit(&d1free[k & 1]);
+        }
         TC2_MARK(2, k, 5 + 2 * h);
       }
       __syncwarp();
     };
     if (nk > 0) row_gemm(0);
     for (int k = 0; k < nk; ++k) {
+      if (k + 1 < nk) row_gemm(k + 1);
       col_gemm(k, 0);
       col_gemm(k, 1);
-      if (k + 1 < nk) row_gemm(k + 1);
     }
   } else {
     // ================================= consumers =================================
-    const int ct = tid - kConsWarp0 * 32, cw = warp - kConsWarp0, quarter = warp & 3, sub = cw >> 2;
-    char* b2 = smem + kB2;
-    float* X = reinterpret_cast<float*>(smem + kX);
-    const int n = quarter * 32 + lane, c = n & 63;
-    const int brow = (n >= 64 ? kN2 : 0) + c;   // B2 row: Re R rows then Im R rows
-
-    auto drain_d1 = [&](int k, int h) {   // D1 half h of window k -> B2 half h (this warp: 32 of its 64 y)
-      const int s = k & 1;
-      mbar_wait_warp(&d1full[h], k & 1);
-      if (k >= 1) mbar_wait_warp(&b2free[h], (k - 1) & 1);   // column GEMM of k-1 done with B2 half h
+    const int ct = tid - kConsWarp0 * 32, quarter = warp & 3, sub = (warp - kConsWarp0) >> 2;
+    const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
+    const int n = quarter * 32 + lane, c = n & 63;   // D1 / D2 lane: Re R (n < 64) or Im R of column c
+    float gsv[2] = {1.f, 1.f};   // output scale of the windows in flight, read while fac / emaxs are ours
+    auto convert = [&](int k) {
+      // ---- D1(k) -> fp16 hi/lo in place (this warp: K half `sub`, two 32-column chunks)
+      mbar_wait_warp(&meta[k & 1], (k >> 1) & 1);
+      gsv[k & 1] = pow2f(emaxs[k & 1] - 8);
+      mbar_wait_warp(&d1full[k & 1], (k >> 1) & 1);
       tc_fence_after();
-      if (ct == 0) TC2_MARK(1, k, 2 * h);
-      if (h == 0 && k >= 1) {   // the previous window's W bulk copy has finished reading its staging in B2
-        if (ct == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        nbar(kBarCons2, kCons2);
-      }
-      const int y0 = 64 * h + 32 * sub;
-      uint32_t r[32];
-      tmem_ld32(tD1 + ((uint32_t)(quarter * 32) << 16) + y0, r);
-      tmem_wait_ld();
-      if (c < kN2) {
-        const float4* fs = reinterpret_cast<const float4*>(fac + s * 128 + y0);
+      if (ct == 0) TC2_MARK(1, k, 0);
+      const float* fs = fac + (k & 1) * 128;
+#pragma unroll 1
+      for (int j = 0; j < 2; ++j) {
+        const int y0 = 64 * sub + 32 * j;
+        const uint32_t col = tD1(k) + lanebase + y0;
+        uint32_t r[32];
+        tmem_ld32(col, r);
+        tmem_wait_ld();
+        uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {   // one 16-byte row chunk: y = y0 + 8j .. +7
-          const float4 fa = fs[2 * j], fb = fs[2 * j + 1];
-          const float f[8] = {fa.x, fa.y, fa.z, fa.w, fb.x, fb.y, fb.z, fb.w};
-          uint32_t hi2[4], lo2[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            split2(__uint_as_float(r[8 * j + 2 * e]) * f[2 * e], __uint_as_float(r[8 * j + 2 * e + 1]) * f[2 * e + 1],
-                   hi2[e], lo2[e]);
-          const uint32_t o = kmaj_off(brow, y0 + 8 * j, 2 * kN2 / 8);
-          *reinterpret_cast<uint4*>(b2 + o) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-          *reinterpret_cast<uint4*>(b2 + kB2Part + o) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+        for (int e = 0; e < 8; ++e) {
+          const float4 f4 = *reinterpret_cast<const float4*>(fs + y0 + 4 * e);
+          split2(__uint_as_float(r[4 * e]) * f4.x, __uint_as_float(r[4 * e + 1]) * f4.y, hi[2 * e], lo[2 * e]);
+          split2(__uint_as_float(r[4 * e + 2]) * f4.z, __uint_as_float(r[4 * e + 3]) * f4.w, hi[2 * e + 1],
+                 lo[2 * e + 1]);
         }
+        tmem_st16(col, hi);
+        tmem_st16(col + 16, lo);
       }
-      fence_async_smem();
+      tmem_wait_st();
       tc_fence_before();
-      nbar(kBarCons2, kCons2);
-      if (ct == 0) {
-        mbar_arrive(&b2ready[h]);
-        TC2_MARK(1, k, 2 * h + 1);
-      }
+      nbar(kBarSub0 + sub, 128);
+      if (ct == 0) TC2_MARK(1, k, 1);
+      if ((warp & 3) == 0 && lane == 0) mbar_arrive(&a2ready[k & 1][sub]);   // one arrival per K half
+      nbar(kBarCons2, kCons2);   // both halves converted: fac[k & 1] read by every consumer
+      if (ct == 0) mbar_arrive(&facfree[k & 1]);
     };
-    // D2 -> W.  Lane r < 42 holds the Cr rows [Cr Rr | Cr Ri], lane 64 + r the Ci rows [Ci Rr | Ci Ri]
-    // (sub 0: the Re R products, sub 1: the Im R products).  The Ci rows go through X; the Cr-row
-    // threads form Wr = CrRr - CiRi (sub 0) and Wi = CrRi + CiRr (sub 1), mask, scale, store.
-    auto drain_d2 = [&](int k, float gs) {
+    auto drain = [&](int k) {
+      // ---- D2(k) -> product planes (this warp: columns 48 sub .. 48 sub + 47 = r of Cr (sub 0) / Ci (sub 1))
+      const float gs = gsv[k & 1];
       mbar_wait_warp(&d2full, k & 1);
       tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 5);
       uint32_t v[48];
-      const uint32_t src = tD2 + (sub ? kN2 : 0) + ((uint32_t)(quarter * 32) << 16);
-      tmem_ld32(src, v);
-      tmem_ld16(src + 32, v + 32);
+      tmem_ld32(tD2 + lanebase + kN2 * sub, v);
+      tmem_ld16(tD2 + lanebase + kN2 * sub + 32, v + 32);
       tmem_wait_ld();
       tc_fence_before();
-      if (ct == 0) TC2_MARK(3, k, 0);
-      // the four product planes P[2 * (Ci row) + sub][r][c] (Cr Rr, Cr Ri, Ci Rr, Ci Ri), scaled by gs, into a
-      // dense staging copy in the (now free) B2 buffer; the tail forms W = (P0 - P3) + i (P1 + P2) and masks it
-      float* Y = reinterpret_cast<float*>(b2);
-      const int r = n & 63;
-      if (r < kWinH) {
-        float* dst = Y + (((n >= 64) ? 2 : 0) + sub) * (kWinH * kWinW) + r * kWinW;
-#pragma unroll
-        for (int cc = 0; cc < kWinW; ++cc) dst[cc] = __uint_as_float(v[cc]) * gs;
-      }
-      if (ct == 0) TC2_MARK(3, k, 1);
       nbar(kBarCons2, kCons2);
-      if (ct == 0) {
-        TC2_MARK(3, k, 2);
-        mbar_arrive(&d2free);   // D2 is in shared memory: the next column GEMM may start
+      if (ct == 0) mbar_arrive(&d2free);   // D2 is in registers: the next column GEMM may start
+      if (c < kWinW) {   // plane: Cr Rr (0), Cr Ri (1), Ci Rr (2), Ci Ri (3); lanes = consecutive columns
+        float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 4 + 2 * sub + (n >= 64 ? 1 : 0)) *
+                               (kWinH * kWinW) + c;
+#pragma unroll
+        for (int rr = 0; rr < kWinH; ++rr) wo[rr * kWinW] = __uint_as_float(v[rr]) * gs;
       }
-      // ... and one bulk async copy (TMA engine, not the LSU) of both planes to the item's W
-      if (ct == 0) {
-        fence_async_smem();
-        float* wo = wout + (size_t)(first + k * gridDim.x - i0) * 4 * (kWinH * kWinW);
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(wo), "r"(smem_u32(Y)),
-                     "r"((uint32_t)(4 * kWinH * kWinW * sizeof(float)))
-                     : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
-      if (ct == 0) TC2_MARK(3, k, 5);
-      nbar(kBarCons2, kCons2);   // X free for the next window
       if (ct == 0) TC2_MARK(1, k, 6);
     };
+    // D1 is double-buffered: convert window k + 1 while the column GEMM of window k runs, then drain D2(k)
+    if (nk > 0) convert(0);
     for (int k = 0; k < nk; ++k) {
-      if (ct == 0) TC2_MARK(1, k, 7);
-      mbar_wait_warp(&meta[k & 1], (k >> 1) & 1);
-      if (ct == 0) TC2_MARK(1, k, 4);
-      const float gs = pow2f(emaxs[k & 1] - 8);
-      drain_d1(k, 0);
-      drain_d1(k, 1);   // ends with a consumer barrier: every thread is done with fac[k & 1]
-      if (ct == 0) mbar_arrive(&facfree[k & 1]);
-      drain_d2(k, gs);
+      if (k + 1 < nk) convert(k + 1);
+      drain(k);
     }
   }
-  if (warp >= kConsWarp0 && tid == kConsWarp0 * 32) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

@@ -35,23 +35,20 @@ C = t[1] - t0
 M = t[2] - t0
 D = t[3] - t0
 # P (producers) per half h: 4h+0 start, 4h+1 stfree passed, 4h+2 landed, 4h+3 converted (after barrier)
-# M (MMA): 0/1 S1h0 ready/issued, 2/3 S1h1, 4/5 S2h0, 6/7 S2h1
-# C (consumers): 0/1 D1h0 ready/drained, 2/3 D1h1 ready/drained, 4 fac ready, 5 D2 ready, 6 W stored
+# M: 0 S1 ready, 1 S1 issued, 2 fac/meta arrived (producer), 4/5 S2h0 ready/issued, 6/7 S2h1 ready/issued
+# C: 0 D1 ready (meta + d1full), 1 D1 converted (sub), 5 D2 ready, 6 planes stored
 n = 14
-np.set_printoptions(linewidth=200)
 for k in range(n):
     print(f"k={k:2d} P " + " ".join(f"{v:7.0f}" for v in P[k]))
     print(f"     M " + " ".join(f"{v:7.0f}" for v in M[k]))
     print(f"     C " + " ".join(f"{v:7.0f}" for v in C[k]))
-    print(f"     D " + " ".join(f"{v:7.0f}" for v in D[k]))
 a, b = 3, n - 1
 d = lambda X, i, j: (X[a:b, j] - X[a:b, i]).mean()
-print("period", np.diff(M[a:b, 3]).mean())
-print("P h0: stfree wait", d(P, 0, 1), "land wait", d(P, 1, 2), "convert", d(P, 2, 3), "| h1: gap", d(P, 3, 4),
-      "stfree wait", d(P, 4, 5), "land wait", d(P, 5, 6), "convert", d(P, 6, 7))
-print("M: S1h0 issue", d(M, 0, 1), "S1h1 issue", d(M, 2, 3), "S2h0 issue", d(M, 4, 5), "S2h1 issue", d(M, 6, 7))
-print("C: D1h0 drain", d(C, 0, 1), "D1h1 drain", d(C, 2, 3), "D2 drain", d(C, 5, 6))
-
+print("period (S1 issue)", np.diff(M[a:b, 1]).mean())
+print("P h0: stfree wait", d(P, 0, 1), "land wait", d(P, 1, 2), "convert", d(P, 2, 3), "| h1: stfree", d(P, 4, 5),
+      "land", d(P, 5, 6), "convert", d(P, 6, 7))
+print("M: S1 issue", d(M, 0, 1), "S2h0 issue", d(M, 4, 5), "S2h1 issue", d(M, 6, 7))
+print("C: D1 convert", d(C, 0, 1), "D2 drain", d(C, 5, 6))
 sp = (ctypes.c_longlong * (160 * 4))()
 lib.hpg_debug_span.argtypes = [ctypes.c_void_p]
 assert lib.hpg_debug_span(sp) == 0
