@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libholo_b200.so")
-SOURCES = ["holo_pipeline.cu", "holo_fast.cu", "holo_fast_tc.cu", "holo_tc2.cu", "holo_tail.cu", "holo_capi.cu", "holo_metrics.cu"]
+SOURCES = ["holo_pipeline.cu", "holo_fast.cu", "holo_fast_tc.cu", "holo_tc2.cu", "holo_tail.cu", "holo_tailr.cu", "holo_capi.cu", "holo_metrics.cu"]
 HEADERS = ["holo_fft.cuh", "holo_internal.h", "holo_fast_common.cuh", "holo_tc_common.cuh", "../../include/holo_b200.h"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -126,7 +126,7 @@ HOLO_DEV void pfa_pass7(float2* buf, int lane) {
 
 }  // namespace
 
-// win: [items][4][42 r][42 c] float: K1's column-DFT product planes (Cr Rr, Cr Ri, Ci Rr, Ci Ri)
+// win: [items][2][42 r][42 c] float: Re / Im of K1's masked Fourier window
 __global__ void __launch_bounds__(kTailWarps * 32, 1)
     tail42_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
                   const float* __restrict__ win, TailLayout L) {
@@ -171,16 +171,13 @@ __global__ void __launch_bounds__(kTailWarps * 32, 1)
     const int b = item / g.P, q = item - b * g.P;
     const int w = p.wl ? p.wl[b] : 0;
     const int pl = q * g.L + w;
-    // -------------- load the product planes [4][r][c] -> masked W = (P0 - P3) + i (P1 + P2) in buf[c][r]
-    const float* src = win + (size_t)(item - i0) * 4 * kN * kN;
+    // -------------- load the masked window planes [Re | Im][r][c] -> buf[c][r]
+    const float* src = win + (size_t)(item - i0) * 2 * kN * kN;
     {   // element i = lane + 64 j: (r, c) advanced incrementally (64 = 42 + 22)
       int r = lane >= kN ? 1 : 0, c = lane >= kN ? lane - kN : lane;
 #pragma unroll 4
       for (int i = lane; i < kN * kN; i += kLanes) {
-        const bool in = r >= s_lo[c] && r <= s_hi[c];
-        const float p0 = __ldg(src + i), p1 = __ldg(src + kN * kN + i);
-        const float p2 = __ldg(src + 2 * kN * kN + i), p3 = __ldg(src + 3 * kN * kN + i);
-        buf[c * kPC + r] = in ? make_float2(p0 - p3, p1 + p2) : make_float2(0.f, 0.f);
+        buf[c * kPC + r] = make_float2(__ldg(src + i), __ldg(src + kN * kN + i));
         c += kLanes - kN;
         r += 1;
         if (c >= kN) { c -= kN; r += 1; }

@@ -13,7 +13,8 @@
 //     power-of-two scalings (per row for the row-DFT operand, per window for the column-DFT operand).
 //     TMEM (512 columns): A1 hi|lo [0,128)  D1 x2 [128,384) (double-buffered)  D2 [384,480).
 //     Warp roles (one CTA per SM, persistent, every CTA owns one pol):
-//       warps 0-7   producers: landed half window -> per-row 2^k scale -> fp16 hi/lo row-DFT operand
+//       warps 0-7   producers: landed window -> registers -> per-row 2^k scale -> fp16 hi/lo row-DFT operand,
+//                   written one K half at a time (the row GEMM of K half 0 overlaps the conversion of half 1)
 //       warp  8     MMA issuer: S1(0) | S1(k+1) S2(k) ... (the row GEMM runs one window ahead)
 //       warp  9     TMA issuer: half windows into a 3-slot landing ring (two halves ahead)
 //       warps 10-17 consumers: D1(k) -> fp16 hi/lo in TMEM (the column GEMM's A operand, no shared-memory
@@ -56,7 +57,8 @@ constexpr uint32_t kC2 = kStage + 2 * kStageHalf;  // column-DFT constant [Cr; C
 constexpr uint32_t kC2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
 constexpr uint32_t kFac = kC2 + 2 * kC2Part;       // fac[2][128] f32
 constexpr uint32_t kErow = kFac + 2 * 128 * 4;     // e_row[128] int
-constexpr uint32_t kK1Bytes = kErow + 128 * 4;
+constexpr uint32_t kXch = kErow + 128 * 4;         // consumer exchange [Ci Rr | Ci Ri][42 r][42 c] f32
+constexpr uint32_t kK1Bytes = kXch + 2 * 42 * 42 * 4;
 static_assert(kK1Bytes <= 227 * 1024 - 1024, "K1 shared memory");
 
 // canonical K-major, no-swizzle operand layout: [kstep][row/8][khalf][row%8][8 halves]
@@ -131,19 +133,18 @@ HOLO_DEV void issue_half(const RunParams& p, const CUtensorMap* tmap, int item, 
   }
 }
 
-// wout: [items][4][42 r][42 c] float, relative to item i0: the column-DFT product planes Cr Rr, Cr Ri, Ci Rr,
-// Ci Ri (unmasked); the window is W = (P0 - P3) + i (P1 + P2) inside the circular mask
+// wout: [items][2][42 r][42 c] float, relative to item i0: Re W and Im W of the masked Fourier window
 template <int FMT>
 __global__ void __launch_bounds__(kK1Threads, 1)
     fourier128_tc2_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft,
                           const __grid_constant__ CUtensorMap tmap, int i0, int i1, float* __restrict__ wout) {
   extern __shared__ __align__(1024) char smem[];
-  // landfull/landfree[slot]: TMA ring; staged[h]: stage half h written; stfree[h]: row GEMM done with the
-  // stage; meta[s]: fac[s] ready; facfree[s]: fac[s] consumed; d1full[b]: row GEMM into D1 buffer b done;
+  // landfull/landfree[slot]: TMA ring; staged[h]: K half h of the stage written; stfree[h]: row GEMM done with
+  // K half h of the stage; meta[s]: fac[s] ready; facfree[s]: fac[s] consumed; d1full[b]: row GEMM into D1 buffer b done;
   // a2ready[b][h]: K half h of the converted D1 buffer b ready; d1free[b]: column GEMM done with D1 buffer b;
   // d2full: column GEMM done; d2free: D2 drained
   __shared__ __align__(8) uint64_t landfull[kSlots], landfree[kSlots], staged[2], stfree[2], meta[2], facfree[2],
-      d1full[2], a2ready[2][2], d1free[2], d2full, d2free;
+      d1full[2], a2ready[2][2], d1free[2], d2full, d2free, c2full;
   __shared__ uint32_t tbase;
   __shared__ int emaxw[8];
   __shared__ int emaxs[2];
@@ -166,10 +167,10 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   if (tid == 0) {
     for (int i = 0; i < kSlots; ++i) {
       mbar_init(&landfull[i], 1);
-      mbar_init(&landfree[i], 1);
+      mbar_init(&landfree[i], kProd2 / 32);   // one arrival per producer warp
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&staged[i], 1);
+      mbar_init(&staged[i], kProd2 / 32);     // K half i written: one arrival per producer warp
       mbar_init(&stfree[i], 1);
       mbar_init(&meta[i], 1);
       mbar_init(&facfree[i], 1);
@@ -179,59 +180,63 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       mbar_init(&d1free[i], 1);
     }
     mbar_init(&d2full, 1);
+    mbar_init(&c2full, 1);
     mbar_init(&d2free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
-  {   // the column-DFT constant of this CTA's pol into shared memory (48 KB, coalesced 16-byte loads)
-    const uint4* src = ft.c2_tc + (size_t)q * (2 * kC2Part / 16);
-    uint4* dst = reinterpret_cast<uint4*>(smem + kC2);
-    if (nk > 0)
-      for (int i = tid; i < (int)(2 * kC2Part / 16); i += blockDim.x) dst[i] = __ldg(src + i);
-  }
   tc_fence_before();
-  __syncthreads();
+  __syncthreads();   // barriers initialised, TMEM base published
   tc_fence_after();
   const uint32_t tm = tbase;
   const uint32_t tA1 = tm, tD2 = tm + 384;
   auto tD1 = [&](int k) { return tm + 128 + 128 * (uint32_t)(k & 1); };
-  if (warp < 4 && nk > 0) {   // row-DFT constant of this CTA's pol into TMEM (column-major table: coalesced)
-    const uint32_t* src = ft.a_tc + (size_t)q * 2 * 64 * 128 + warp * 32 + lane;
-    const uint32_t dst = tA1 + ((uint32_t)(warp * 32) << 16);
+  const int pre = min(kSlots, 2 * nk);   // the first frame loads fly while the constant tables are set up
+  if (warp == kTmaWarp && lane == 0 && nk > 0) {
+    for (int jh = 0; jh < pre; ++jh)
+      issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, jh, &landfull[jh]);
+    // the column-DFT constant of this CTA's pol: one 48 KB bulk copy into shared memory
+    mbar_expect_tx(&c2full, 2 * kC2Part);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(smem + kC2)),
+                 "l"(ft.c2_tc + (size_t)q * (2 * kC2Part / 16)), "r"(2 * kC2Part), "r"(smem_u32(&c2full))
+                 : "memory");
+  }
+  if (warp != kMmaWarp && warp != kTmaWarp && nk > 0) {
+    // row-DFT constant of this CTA's pol into TMEM (column-major table: coalesced): 16 warps, one 32-column
+    // chunk each -- a warp reaches the TMEM lane quarter warp % 4
+    const int quarter = warp & 3, chunk = warp < 8 ? warp >> 2 : 2 + ((warp - kConsWarp0) >> 2);
+    const int part = chunk >> 1, hh = chunk & 1;
+    const uint32_t* s2 = ft.a_tc + (size_t)q * 2 * 64 * 128 + quarter * 32 + lane + ((size_t)part * 64 + hh * 32) * 128;
     uint32_t r[32];
 #pragma unroll
-    for (int part = 0; part < 2; ++part) {
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const uint32_t* s2 = src + ((size_t)part * 64 + hh * 32) * 128;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
-        tmem_st32(dst + part * 64 + hh * 32, r);
-      }
-    }
+    for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
+    tmem_st32(tA1 + ((uint32_t)(quarter * 32) << 16) + part * 64 + hh * 32, r);
     tmem_wait_st();
   }
-  fence_async_smem();   // C2 written by generic stores, read by the tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
 
   if (warp < kMmaWarp) {
     // ================================= producers =================================
+    // Phase A: both halves of the window into registers (row max -> exact power-of-two row scale), landing
+    // slots released at once.  Phase B: the row-DFT operand is written one K half (64 samples of every row)
+    // at a time, so the row GEMM of K half 0 runs while K half 1 is converted and the stage halves are
+    // refilled for the next window while the other half's MMAs run.
     const int r8 = lane & 7, gq = lane >> 3;   // row within the warp's 8, octet group
     for (int k = 0; k < nk; ++k) {
       const int s = k & 1;
       int emax_t = -1000;
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {   // half h = rows 64h..64h+63; warp w -> rows 64h + 8w + r8
+      float v[2][32];   // rows y = 64 h + 8 warp + r8; octets o = gq + 4 i, i = 0..3
+      float sc[2];
+      if (tid == 0) TC2_MARK(0, k, 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
         const int jh = 2 * k + h, slot = jh % kSlots;
-        if (tid == 0) TC2_MARK(0, k, 4 * h + 0);
-        if (k >= 1) mbar_wait_warp(&stfree[h], (k - 1) & 1);   // row GEMM of k-1 done with the stage
-        if (tid == 0) TC2_MARK(0, k, 4 * h + 1);
         mbar_wait_warp(&landfull[slot], (jh / kSlots) & 1);
-        if (tid == 0) TC2_MARK(0, k, 4 * h + 2);
+        if (tid == 0) TC2_MARK(0, k, 1 + h);
         const int yl = 8 * warp + r8, y = 64 * h + yl;
         const int jj = yl >> 5, rb = y & 31;   // chunk within the half, row in box
-        float v[32];   // octets o = gq + 4 i, i = 0..3
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int o = gq + 4 * i;
@@ -240,47 +245,55 @@ __global__ void __launch_bounds__(kK1Threads, 1)
             const int c0 = (2 * (o & 3)) ^ (rb & 7), c1 = (2 * (o & 3) + 1) ^ (rb & 7);
             const float4 a = *reinterpret_cast<const float4*>(box + c0 * 16);
             const float4 c = *reinterpret_cast<const float4*>(box + c1 * 16);
-            v[8 * i + 0] = a.x; v[8 * i + 1] = a.y; v[8 * i + 2] = a.z; v[8 * i + 3] = a.w;
-            v[8 * i + 4] = c.x; v[8 * i + 5] = c.y; v[8 * i + 6] = c.z; v[8 * i + 7] = c.w;
+            v[h][8 * i + 0] = a.x; v[h][8 * i + 1] = a.y; v[h][8 * i + 2] = a.z; v[h][8 * i + 3] = a.w;
+            v[h][8 * i + 4] = c.x; v[h][8 * i + 5] = c.y; v[h][8 * i + 6] = c.z; v[h][8 * i + 7] = c.w;
           } else {            // u16: box qx = o / 8, one 16-byte chunk o%8
             const char* box = smem + kLand + slot * kSlot + (jj * 4 + (o >> 3)) * kBox + rb * 128;
             const uint4 a = *reinterpret_cast<const uint4*>(box + (((o & 7) ^ (rb & 7)) * 16));
             const uint32_t w4[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              v[8 * i + 2 * e] = (float)(w4[e] & 0xffffu);
-              v[8 * i + 2 * e + 1] = (float)(w4[e] >> 16);
+              v[h][8 * i + 2 * e] = (float)(w4[e] & 0xffffu);
+              v[h][8 * i + 2 * e + 1] = (float)(w4[e] >> 16);
             }
           }
         }
         float m = 0.f;
 #pragma unroll
-        for (int e = 0; e < 32; ++e) m = fmaxf(m, fabsf(v[e]));
+        for (int e = 0; e < 32; ++e) m = fmaxf(m, fabsf(v[h][e]));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 8));
         m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, 16));
+        if (lane == 0) mbar_arrive(&landfree[slot]);   // this warp's rows are in registers (8 arrivals free the slot)
         // exact power-of-two row scale: |f| * sc < 2^14, fh + fl keep 22 bits
         const int ey = exp_of(m);
-        const float sc = ey > -1000 ? pow2f(14 - ey) : 1.f;
+        sc[h] = ey > -1000 ? pow2f(14 - ey) : 1.f;
         if (gq == 0) erow[y] = ey;
         emax_t = max(emax_t, ey);
-        char* st = smem + kStage;   // one K-major N = 128 operand: hi [0, 32 KB), lo [32 KB, 64 KB)
+      }
+      char* st = smem + kStage;   // one K-major N = 128 operand: hi [0, 32 KB), lo [32 KB, 64 KB)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t off = kmaj_off(y, 8 * (gq + 4 * i), 16);
-          uint32_t hi2[4], lo2[4];
+      for (int kh = 0; kh < 2; ++kh) {   // K half kh = samples 64 kh .. 64 kh + 63 = octets 8 kh .. 8 kh + 7
+        if (k >= 1) mbar_wait_warp(&stfree[kh], (k - 1) & 1);   // row GEMM of k-1 done with this K half
+        if (tid == 0) TC2_MARK(0, k, 3 + 2 * kh);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) split2(v[8 * i + 2 * e] * sc, v[8 * i + 2 * e + 1] * sc, hi2[e], lo2[e]);
-          *reinterpret_cast<uint4*>(st + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
-          *reinterpret_cast<uint4*>(st + 32768 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+        for (int h = 0; h < 2; ++h) {
+          const int y = 64 * h + 8 * warp + r8;
+#pragma unroll
+          for (int ii = 0; ii < 2; ++ii) {
+            const int i = 2 * kh + ii;
+            const uint32_t off = kmaj_off(y, 8 * (gq + 4 * i), 16);
+            uint32_t hi2[4], lo2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              split2(v[h][8 * i + 2 * e] * sc[h], v[h][8 * i + 2 * e + 1] * sc[h], hi2[e], lo2[e]);
+            *reinterpret_cast<uint4*>(st + off) = make_uint4(hi2[0], hi2[1], hi2[2], hi2[3]);
+            *reinterpret_cast<uint4*>(st + 32768 + off) = make_uint4(lo2[0], lo2[1], lo2[2], lo2[3]);
+          }
         }
         fence_async_smem();
-        tc_fence_before();
-        nbar(kBarProd2, kProd2);   // half h consumed: landing slot free, stage half written
-        if (tid == 0) TC2_MARK(0, k, 4 * h + 3);
-        if (tid == 0) {
-          mbar_arrive(&staged[h]);
-          mbar_arrive(&landfree[slot]);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&staged[kh]);   // 8 arrivals: K half written by every producer warp
+        if (tid == 0) TC2_MARK(0, k, 4 + 2 * kh);
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) emax_t = max(emax_t, __shfl_xor_sync(0xffffffffu, emax_t, o));
@@ -298,42 +311,47 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       nbar(kBarProd2, kProd2);
       if (tid == 0) {
         mbar_arrive(&meta[s]);
-        TC2_MARK(2, k, 2);
+        TC2_MARK(0, k, 7);
       }
     }
   } else if (warp == kTmaWarp) {
     // ================================ TMA issuer ================================
-    for (int jh = 0; jh < 2 * nk; ++jh) {   // the whole warp walks the ring (converged), lane 0 issues
+    for (int jh = pre; jh < 2 * nk; ++jh) {   // the whole warp walks the ring (converged), lane 0 issues
       const int slot = jh % kSlots;
-      if (jh >= kSlots) mbar_wait_warp(&landfree[slot], ((jh / kSlots) - 1) & 1);
+      mbar_wait_warp(&landfree[slot], ((jh / kSlots) - 1) & 1);
       if (lane == 0) issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, slot, &landfull[slot]);
       __syncwarp();
     }
   } else if (warp == kMmaWarp) {
     // ================================ MMA issuer ================================
-    const uint32_t idesc1 = idesc_f16(128, 128), idesc2 = idesc_f16(128, 2 * kN2);
-    auto row_gemm = [&](int k) {   // D1(k) = A1 * stage, N = 128 (24 MMAs)
-      mbar_wait_warp(&staged[0], k & 1);
-      mbar_wait_warp(&staged[1], k & 1);
-      if (k >= 2) mbar_wait_warp(&d1free[k & 1], ((k >> 1) - 1) & 1);   // column GEMM of k-2 done with it
-      if (lane == 0) TC2_MARK(2, k, 0);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sb = smem_u32(smem + kStage), d = tD1(k);
+    const uint32_t idesc2 = idesc_f16(128, 2 * kN2);
+    const uint32_t idesc1 = idesc_f16(128, 128);
+    auto row_gemm = [&](int k) {   // D1(k) = A1 * stage, N = 128: 12 MMAs per K half as the halves are staged
+      // D1 buffer k & 1 was last read by the column GEMM of window k-2: tcgen05.mma instructions of one thread
+      // execute in issue order, so the overwrite needs no barrier
+#pragma unroll 1
+      for (int kh = 0; kh < 2; ++kh) {
+        mbar_wait_warp(&staged[kh], k & 1);
+        if (lane == 0 && kh == 0) TC2_MARK(2, k, 0);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sb = smem_u32(smem + kStage), d = tD1(k);
 #pragma unroll
-        for (int gk = 0; gk < 8; ++gk) {
-          const uint64_t bh = umma_desc(sb + gk * 4096, 128, 256);
-          const uint64_t bl = umma_desc(sb + 32768 + gk * 4096, 128, 256);
-          mma_f16_ts(d, tA1 + gk * 8, bh, idesc1, gk != 0);
-          mma_f16_ts(d, tA1 + 64 + gk * 8, bh, idesc1, 1);
-          mma_f16_ts(d, tA1 + gk * 8, bl, idesc1, 1);
+          for (int gk = 4 * kh; gk < 4 * kh + 4; ++gk) {
+            const uint64_t bh = umma_desc(sb + gk * 4096, 128, 256);
+            const uint64_t bl = umma_desc(sb + 32768 + gk * 4096, 128, 256);
+            mma_f16_ts(d, tA1 + gk * 8, bh, idesc1, gk != 0);
+            mma_f16_ts(d, tA1 + 64 + gk * 8, bh, idesc1, 1);
+            mma_f16_ts(d, tA1 + gk * 8, bl, idesc1, 1);
+          }
+          tc_commit(&stfree[kh]);   // the producers may refill this K half while the other half's MMAs run
+          if (kh == 1) {
+            tc_commit(&d1full[k & 1]);
+            TC2_MARK(2, k, 1);
+          }
         }
-        tc_commit(&stfree[0]);
-        tc_commit(&stfree[1]);
-        tc_commit(&d1full[k & 1]);
-        TC2_MARK(2, k, 1);
+        __syncwarp();
       }
-      __syncwarp();
     };
     auto col_gemm = [&](int k, int h) {   // D2 (+)= D1(k)[:, K half h] (fp16 hi/lo in TMEM) * C2, N = 96
       // per D1 buffer: the consumer may convert window k + 1 before this wait, never window k + 2
@@ -341,7 +359,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       if (h == 0 && k >= 1) mbar_wait_warp(&d2free, (k - 1) & 1);
       if (lane == 0) TC2_MARK(2, k, 4 + 2 * h);
       tc_fence_after();
-      if (lane == 0) {
+      if (elect_one()) {
         const uint32_t sb = smem_u32(smem + kC2), a = tD1(k);
 #pragma unroll
         for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {   // K-step ks: hi at column 32 (ks/2) + 8 (ks%2), lo +16
@@ -360,6 +378,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       __syncwarp();
     };
     if (nk > 0) row_gemm(0);
+    if (nk > 0) mbar_wait_warp(&c2full, 0);   // the column-DFT constant has landed
     for (int k = 0; k < nk; ++k) {
       if (k + 1 < nk) row_gemm(k + 1);
       col_gemm(k, 0);
@@ -405,8 +424,12 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       nbar(kBarCons2, kCons2);   // both halves converted: fac[k & 1] read by every consumer
       if (ct == 0) mbar_arrive(&facfree[k & 1]);
     };
+    float* xch = reinterpret_cast<float*>(smem + kXch);
+    const int mlo = c < kWinW ? ft.crange[2 * c] : 1, mhi = c < kWinW ? ft.crange[2 * c + 1] : 0;
     auto drain = [&](int k) {
-      // ---- D2(k) -> product planes (this warp: columns 48 sub .. 48 sub + 47 = r of Cr (sub 0) / Ci (sub 1))
+      // ---- D2(k) -> W.  This warp holds columns 48 sub .. 48 sub + 47 of its lanes: Cr R (sub 0) or Ci R (sub 1)
+      // of Re R (n < 64) / Im R (n >= 64).  W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr): the sub-1 warps hand their
+      // products over through shared memory, the sub-0 warps combine, mask (pipeline.py:72-76) and store.
       const float gs = gsv[k & 1];
       mbar_wait_warp(&d2full, k & 1);
       tc_fence_after();
@@ -416,13 +439,24 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       tmem_ld16(tD2 + lanebase + kN2 * sub + 32, v + 32);
       tmem_wait_ld();
       tc_fence_before();
-      nbar(kBarCons2, kCons2);
+      nbar(kBarCons2, kCons2);   // also: the sub-0 warps are done reading the previous window's exchange
       if (ct == 0) mbar_arrive(&d2free);   // D2 is in registers: the next column GEMM may start
-      if (c < kWinW) {   // plane: Cr Rr (0), Cr Ri (1), Ci Rr (2), Ci Ri (3); lanes = consecutive columns
-        float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 4 + 2 * sub + (n >= 64 ? 1 : 0)) *
-                               (kWinH * kWinW) + c;
+      if (sub == 1 && c < kWinW) {   // [Ci Rr | Ci Ri][r][c]
+        float* xo = xch + (n >= 64 ? kWinH * kWinW : 0) + c;
 #pragma unroll
-        for (int rr = 0; rr < kWinH; ++rr) wo[rr * kWinW] = __uint_as_float(v[rr]) * gs;
+        for (int rr = 0; rr < kWinH; ++rr) xo[rr * kWinW] = __uint_as_float(v[rr]);
+      }
+      nbar(kBarCons2, kCons2);
+      if (sub == 0 && c < kWinW) {   // planes: Re W (lanes n < 64), Im W (n >= 64); lanes = consecutive columns
+        const bool im = n >= 64;
+        const float* xi = xch + (im ? 0 : kWinH * kWinW) + c;   // Im: + Ci Rr; Re: - Ci Ri
+        const float sg = im ? gs : -gs;
+        float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 2 + (im ? 1 : 0)) * (kWinH * kWinW) + c;
+#pragma unroll
+        for (int rr = 0; rr < kWinH; ++rr) {
+          const float val = fmaf(xi[rr * kWinW], sg, __uint_as_float(v[rr]) * gs);
+          wo[rr * kWinW] = (rr >= mlo && rr <= mhi) ? val : 0.f;
+        }
       }
       if (ct == 0) TC2_MARK(1, k, 6);
     };
@@ -507,13 +541,10 @@ __global__ void __launch_bounds__(256, 3)
       staged_q = q;
     }
     __syncthreads();
-    const float* Wp = win + (size_t)(item - i0) * 4 * WH * WW;   // product planes [4][r][c]
-    for (int i = tid; i < WH * WW; i += blockDim.x) {            // -> masked W in F, column-major [c][r]
+    const float* Wp = win + (size_t)(item - i0) * 2 * WH * WW;   // masked window planes [Re | Im][r][c]
+    for (int i = tid; i < WH * WW; i += blockDim.x) {            // -> F, column-major [c][r]
       const int r = i / WW, c = i - r * WW;
-      const bool in = r >= crange[2 * c] && r <= crange[2 * c + 1];
-      F[c * WH + r] = in ? make_float2(__ldg(Wp + i) - __ldg(Wp + 3 * WH * WW + i),
-                                       __ldg(Wp + WH * WW + i) + __ldg(Wp + 2 * WH * WW + i))
-                         : make_float2(0.f, 0.f);
+      F[c * WH + r] = make_float2(__ldg(Wp + i), __ldg(Wp + WH * WW + i));
     }
     __syncthreads();
     // IFFT along r (y) first, then along c (x)
@@ -601,6 +632,8 @@ extern "C" int hpg_debug_trace(long long* out) {   // copies g_tc2_trace (2*64*8
 bool tail_supported(const Geometry& g);
 cudaError_t launch_tail(const RunParams& p, const FastTables& ft, int num_sms, cudaStream_t s, int i0, int i1,
                         const float* win);
+bool tailr_supported(const Geometry& g, const void* rcal);
+cudaError_t launch_tailr(const RunParams& p, const FastTables& ft, cudaStream_t s, int i0, int i1, const float* win);
 
 constexpr int kTc2Chunk = 2048;   // items per K1/K2 pair: the product planes (28 KB each) stay in L2
 
@@ -616,7 +649,7 @@ bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, c
 int64_t tc2_chunk() { return kTc2Chunk; }
 
 size_t tc2_workspace(int64_t items) {
-  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 4 * 42 * 42 * sizeof(float);   // 4 product planes
+  return (size_t)std::min<int64_t>(items, kTc2Chunk) * 2 * 42 * 42 * sizeof(float);   // Re W, Im W
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -673,8 +706,11 @@ cudaError_t launch_tc2(const RunParams& p, const FastTables& ft, int num_sms, cu
       fourier128_tc2_kernel<1><<<g1, kK1Threads, kK1Bytes, s>>>(p, ft, tmap, i0, i1, wbuf);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const char* env = getenv("HOLO_TAIL");   // diagnostic: HOLO_TAIL=0 runs the round-1 CTA-wide tail
-    if (tail_supported(p.g) && !(env && env[0] == '0')) {
+    // diagnostic: HOLO_TAIL=0 runs the round-1 CTA-wide tail, HOLO_TAIL=2 the warp-pair tail
+    const char* env = getenv("HOLO_TAIL");
+    if (tailr_supported(p.g, p.rcal) && !(env && (env[0] == '0' || env[0] == '2'))) {
+      e = launch_tailr(p, ft, s, i0, i1, wbuf);
+    } else if (tail_supported(p.g) && !(env && env[0] == '0')) {
       e = launch_tail(p, ft, num_sms, s, i0, i1, wbuf);
     } else {
       field128_kernel<42, 42><<<std::max(1, std::min(n, num_sms * std::max(k2_per_sm, 1))), 256, k2_bytes, s>>>(

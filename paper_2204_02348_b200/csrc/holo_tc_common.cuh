@@ -23,6 +23,16 @@ HOLO_DEV void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// One lane of a CONVERGED warp.  tcgen05.mma must be issued under this predicate, not under `lane == 0`:
+// ptxas then emits the UTCHMMA directly, while for an arbitrary one-lane predicate it wraps every MMA in an
+// ELECT / BRA.U.ANY loop -- measured 112 cycles per issued MMA against 69 (N = 128) / 54 (N = 96) / 38 (N = 64)
+// (tools/mma_rate.cu).
+HOLO_DEV bool elect_one() {
+  uint32_t e;
+  asm volatile("{.reg .pred p; elect.sync _|p, 0xffffffff; selp.u32 %0, 1, 0, p;}" : "=r"(e));
+  return e != 0;
+}
+
 HOLO_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   uint32_t done = 0;
   while (!done) {

@@ -34,20 +34,21 @@ P = t[0] - t0
 C = t[1] - t0
 M = t[2] - t0
 D = t[3] - t0
-# P (producers) per half h: 4h+0 start, 4h+1 stfree passed, 4h+2 landed, 4h+3 converted (after barrier)
-# M: 0 S1 ready, 1 S1 issued, 2 fac/meta arrived (producer), 4/5 S2h0 ready/issued, 6/7 S2h1 ready/issued
-# C: 0 D1 ready (meta + d1full), 1 D1 converted (sub), 5 D2 ready, 6 planes stored
+# P (producers): 0 window start, 1 half 0 landed, 2 half 1 landed, 3 stfree[K0] passed, 4 K half 0 staged,
+#   5 stfree[K1] passed, 6 K half 1 staged, 7 fac / meta published
+# M: 0 K half 0 staged seen, 1 row GEMM issued, 4/5 S2h0 ready/issued, 6/7 S2h1 ready/issued
+# C: 0 D1 ready (meta + d1full), 1 D1 converted (sub), 5 D2 ready, 6 W stored
 n = 14
 for k in range(n):
     print(f"k={k:2d} P " + " ".join(f"{v:7.0f}" for v in P[k]))
-    print(f"     M " + " ".join(f"{v:7.0f}" for v in M[k]))
-    print(f"     C " + " ".join(f"{v:7.0f}" for v in C[k]))
+    print(f"     M " + " ".join(f"{v:7.0f}" if v > -1e9 else "      -" for v in M[k]))
+    print(f"     C " + " ".join(f"{v:7.0f}" if v > -1e9 else "      -" for v in C[k]))
 a, b = 3, n - 1
 d = lambda X, i, j: (X[a:b, j] - X[a:b, i]).mean()
-print("period (S1 issue)", np.diff(M[a:b, 1]).mean())
-print("P h0: stfree wait", d(P, 0, 1), "land wait", d(P, 1, 2), "convert", d(P, 2, 3), "| h1: stfree", d(P, 4, 5),
-      "land", d(P, 5, 6), "convert", d(P, 6, 7))
-print("M: S1 issue", d(M, 0, 1), "S2h0 issue", d(M, 4, 5), "S2h1 issue", d(M, 6, 7))
+print("period (row GEMM issued)", np.diff(M[a:b, 1]).mean())
+print("P: land wait h0", d(P, 0, 1), "read+max h0 / land h1", d(P, 1, 2), "read+max h1 / stfree K0", d(P, 2, 3),
+      "write K0", d(P, 3, 4), "stfree K1 wait", d(P, 4, 5), "write K1", d(P, 5, 6), "fac", d(P, 6, 7))
+print("M: row GEMM (staged K0 -> issued)", d(M, 0, 1), "S2h0 issue", d(M, 4, 5), "S2h1 issue", d(M, 6, 7))
 print("C: D1 convert", d(C, 0, 1), "D2 drain", d(C, 5, 6))
 sp = (ctypes.c_longlong * (160 * 4))()
 lib.hpg_debug_span.argtypes = [ctypes.c_void_p]
