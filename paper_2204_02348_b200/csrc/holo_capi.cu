@@ -322,6 +322,19 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
     }
   }
   if (a_tc.empty()) a_tc.push_back(0u);
+  // the same matrix with packed rows for the two-kernel path (holo_tc2.cu): row c < ww -> Re, row ww + c -> Im
+  std::vector<uint32_t> a_tcp;
+  if (g.nx == 128 && g.ww <= 64) {
+    a_tcp.assign((size_t)g.P * 2 * 128 * 64, 0u);
+    for (int q = 0; q < g.P; ++q)
+      for (int n = 0; n < 2 * g.ww; ++n) {
+        const int src = n < g.ww ? n : 64 + (n - g.ww);
+        for (int part = 0; part < 2; ++part)
+          for (int x2 = 0; x2 < 64; ++x2)
+            a_tcp[(((size_t)q * 2 + part) * 64 + x2) * 128 + n] = a_tc[(((size_t)q * 2 + part) * 64 + x2) * 128 + src];
+      }
+  }
+  if (a_tcp.empty()) a_tcp.push_back(0u);
   // tensor-core column DFT (holo_tc2.cu): rows r < wh -> Cr, rows 64 + r -> Ci of
   // C[r][y] = exp(-2 pi i ky_r y / ny) * py[r] = exp(-2 pi i ky_r (y - xi_y + ny/2) / ny),
   // ky_r = k0y + r - wh/2; K = y (0..127), fp16 hi + lo.  ny == 128, wh <= 64, wavelength 0.
@@ -381,7 +394,7 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
   }
   if (c2_tc.empty()) c2_tc.push_back(0);
   std::vector<char> blob;
-  const size_t o1 = push(blob, a_tc), o2 = push(blob, a2_tc), o3 = push(blob, c2_tc);
+  const size_t o1 = push(blob, a_tc), o2 = push(blob, a2_tc), o3 = push(blob, c2_tc), o4 = push(blob, a_tcp);
   cudaError_t e = pool_alloc(P->device, blob.size(), &P->tc_dev);
   if (e != cudaSuccess) { P->tc_dev = nullptr; return e; }
   P->tc_bytes = blob.size();
@@ -389,6 +402,7 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
   if (e != cudaSuccess) return e;
   P->ft.a_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o1);
   P->ft.a2_tc = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o2);
+  P->ft.a_tcp = reinterpret_cast<const uint32_t*>(static_cast<char*>(P->tc_dev) + o4);
   P->ft.c2_tc = reinterpret_cast<const uint4*>(static_cast<char*>(P->tc_dev) + o3);
   return cudaSuccess;
 }

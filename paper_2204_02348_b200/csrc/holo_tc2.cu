@@ -36,13 +36,16 @@ namespace holo {
 
 namespace {
 
-constexpr int kProd2 = 256;                 // producer threads (warps 0-7)
-constexpr int kMmaWarp = 8;                 // tcgen05.mma issuer
-constexpr int kTmaWarp = 9;                 // TMA issuer
-constexpr int kConsWarp0 = 10;              // consumers: warps 10-17
-constexpr int kCons2 = 256;
-constexpr int kK1Threads = kProd2 + 64 + kCons2;
-constexpr int kBarProd2 = 1, kBarCons2 = 2, kBarSub0 = 3;   // kBarSub0 + sub: the 4 warps of one K half
+// Warp roles.  A warp reaches the TMEM lane quarter warp % 4, and the DFT rows are packed into lanes 0..83
+// (Re R of column c at lane c, Im R at lane 42 + c), so the six consumer warps are the ones with
+// warp % 4 < 3 among warps 0-7; warps 3 and 7 issue the MMAs and the TMA loads; warps 8-15 are the producers.
+constexpr int kMmaWarp = 3;                 // tcgen05.mma issuer
+constexpr int kTmaWarp = 7;                 // TMA issuer
+constexpr int kProdWarp0 = 8;               // producers: warps 8-15
+constexpr int kProd2 = 256;                 // producer threads
+constexpr int kCons2 = 192;                 // consumer threads (warps 0-2, 4-6)
+constexpr int kK1Threads = 512;
+constexpr int kBarCons2 = 2, kBarSub0 = 3;   // kBarSub0 + sub: the 3 warps of one K half
 constexpr int kN2 = 48;                     // column-DFT N per real part (42 rows, padded)
 constexpr int kWinW = 42, kWinH = 42;
 constexpr int kSlots = 3;                   // landing ring: half windows
@@ -55,9 +58,8 @@ constexpr uint32_t kStage = kSlots * kSlot;        // row-DFT operand, N = 128 r
 constexpr uint32_t kStageHalf = 32768;
 constexpr uint32_t kC2 = kStage + 2 * kStageHalf;  // column-DFT constant [Cr; Ci]: hi | lo
 constexpr uint32_t kC2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
-constexpr uint32_t kFac = kC2 + 2 * kC2Part;       // fac[2][128] f32
-constexpr uint32_t kErow = kFac + 2 * 128 * 4;     // e_row[128] int
-constexpr uint32_t kXch = kErow + 128 * 4;         // consumer exchange [Ci Rr | Ci Ri][42 r][42 c] f32
+constexpr uint32_t kFac = kC2 + 2 * kC2Part;       // facrow[2][128] f32: 2^e_y of every window row
+constexpr uint32_t kXch = kFac + 2 * 128 * 4;      // consumer exchange [Ci Rr | Ci Ri][42 r][42 c] f32
 constexpr uint32_t kK1Bytes = kXch + 2 * 42 * 42 * 4;
 static_assert(kK1Bytes <= 227 * 1024 - 1024, "K1 shared memory");
 
@@ -140,16 +142,14 @@ __global__ void __launch_bounds__(kK1Threads, 1)
                           const __grid_constant__ CUtensorMap tmap, int i0, int i1, float* __restrict__ wout) {
   extern __shared__ __align__(1024) char smem[];
   // landfull/landfree[slot]: TMA ring; staged[h]: K half h of the stage written; stfree[h]: row GEMM done with
-  // K half h of the stage; meta[s]: fac[s] ready; facfree[s]: fac[s] consumed; d1full[b]: row GEMM into D1 buffer b done;
+  // K half h of the stage; meta[s]: row scales of slot s published; facfree[s]: slot s consumed; d1full[b]: row GEMM into D1 buffer b done;
   // a2ready[b][h]: K half h of the converted D1 buffer b ready; d1free[b]: column GEMM done with D1 buffer b;
   // d2full: column GEMM done; d2free: D2 drained
   __shared__ __align__(8) uint64_t landfull[kSlots], landfree[kSlots], staged[2], stfree[2], meta[2], facfree[2],
       d1full[2], a2ready[2][2], d1free[2], d2full, d2free, c2full;
   __shared__ uint32_t tbase;
-  __shared__ int emaxw[8];
-  __shared__ int emaxs[2];
-  float* fac = reinterpret_cast<float*>(smem + kFac);
-  int* erow = reinterpret_cast<int*>(smem + kErow);
+  __shared__ int emaxw[2][8];   // per window slot: largest row exponent seen by each producer warp
+  float* facrow = reinterpret_cast<float*>(smem + kFac);
   const Geometry& g = p.g;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int first = i0 + blockIdx.x;
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&staged[i], kProd2 / 32);     // K half i written: one arrival per producer warp
       mbar_init(&stfree[i], 1);
-      mbar_init(&meta[i], 1);
+      mbar_init(&meta[i], kProd2 / 32);       // row scales published: one arrival per producer warp
       mbar_init(&facfree[i], 1);
       mbar_init(&d1full[i], 1);
       mbar_init(&a2ready[i][0], 1);
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   const uint32_t tA1 = tm, tD2 = tm + 384;
   auto tD1 = [&](int k) { return tm + 128 + 128 * (uint32_t)(k & 1); };
   const int pre = min(kSlots, 2 * nk);   // the first frame loads fly while the constant tables are set up
-  if (warp == kTmaWarp && lane == 0 && nk > 0) {
+  if (warp == kTmaWarp && nk > 0 && elect_one()) {
     for (int jh = 0; jh < pre; ++jh)
       issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, jh, &landfull[jh]);
     // the column-DFT constant of this CTA's pol: one 48 KB bulk copy into shared memory
@@ -201,12 +201,12 @@ __global__ void __launch_bounds__(kK1Threads, 1)
                  "l"(ft.c2_tc + (size_t)q * (2 * kC2Part / 16)), "r"(2 * kC2Part), "r"(smem_u32(&c2full))
                  : "memory");
   }
-  if (warp != kMmaWarp && warp != kTmaWarp && nk > 0) {
-    // row-DFT constant of this CTA's pol into TMEM (column-major table: coalesced): 16 warps, one 32-column
-    // chunk each -- a warp reaches the TMEM lane quarter warp % 4
-    const int quarter = warp & 3, chunk = warp < 8 ? warp >> 2 : 2 + ((warp - kConsWarp0) >> 2);
+  if ((warp & 3) != 3 && nk > 0) {
+    // row-DFT constant of this CTA's pol into TMEM lanes 0..95 (column-major table: coalesced): 12 warps,
+    // one 32-column chunk each (lanes 96..127 carry no DFT row and are never read back)
+    const int quarter = warp & 3, chunk = warp >> 2;
     const int part = chunk >> 1, hh = chunk & 1;
-    const uint32_t* s2 = ft.a_tc + (size_t)q * 2 * 64 * 128 + quarter * 32 + lane + ((size_t)part * 64 + hh * 32) * 128;
+    const uint32_t* s2 = ft.a_tcp + (size_t)q * 2 * 64 * 128 + quarter * 32 + lane + ((size_t)part * 64 + hh * 32) * 128;
     uint32_t r[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
@@ -217,25 +217,28 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   __syncthreads();
   tc_fence_after();
 
-  if (warp < kMmaWarp) {
+  if (warp >= kProdWarp0) {
     // ================================= producers =================================
     // Phase A: both halves of the window into registers (row max -> exact power-of-two row scale), landing
     // slots released at once.  Phase B: the row-DFT operand is written one K half (64 samples of every row)
     // at a time, so the row GEMM of K half 0 runs while K half 1 is converted and the stage halves are
     // refilled for the next window while the other half's MMAs run.
     const int r8 = lane & 7, gq = lane >> 3;   // row within the warp's 8, octet group
+    const int pw = warp - kProdWarp0;
+    const bool mark = tid == kProdWarp0 * 32;
     for (int k = 0; k < nk; ++k) {
       const int s = k & 1;
       int emax_t = -1000;
-      float v[2][32];   // rows y = 64 h + 8 warp + r8; octets o = gq + 4 i, i = 0..3
+      float v[2][32];   // rows y = 64 h + 8 pw + r8; octets o = gq + 4 i, i = 0..3
       float sc[2];
-      if (tid == 0) TC2_MARK(0, k, 0);
+      if (mark) TC2_MARK(0, k, 0);
+      if (k >= 2) mbar_wait_warp(&facfree[s], ((k >> 1) - 1) & 1);   // conversion of window k-2 done with slot s
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int jh = 2 * k + h, slot = jh % kSlots;
         mbar_wait_warp(&landfull[slot], (jh / kSlots) & 1);
-        if (tid == 0) TC2_MARK(0, k, 1 + h);
-        const int yl = 8 * warp + r8, y = 64 * h + yl;
+        if (mark) TC2_MARK(0, k, 1 + h);
+        const int yl = 8 * pw + r8, y = 64 * h + yl;
         const int jj = yl >> 5, rb = y & 31;   // chunk within the half, row in box
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -267,17 +270,24 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         // exact power-of-two row scale: |f| * sc < 2^14, fh + fl keep 22 bits
         const int ey = exp_of(m);
         sc[h] = ey > -1000 ? pow2f(14 - ey) : 1.f;
-        if (gq == 0) erow[y] = ey;
+        if (gq == 0) facrow[s * 128 + y] = ey > -1000 ? pow2f(ey) : 0.f;   // undone after the row GEMM
         emax_t = max(emax_t, ey);
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) emax_t = max(emax_t, __shfl_xor_sync(0xffffffffu, emax_t, o));
+      __syncwarp();   // the warp's row scales are written
+      if (lane == 0) {
+        emaxw[s][pw] = emax_t;
+        mbar_arrive(&meta[s]);
       }
       char* st = smem + kStage;   // one K-major N = 128 operand: hi [0, 32 KB), lo [32 KB, 64 KB)
 #pragma unroll
       for (int kh = 0; kh < 2; ++kh) {   // K half kh = samples 64 kh .. 64 kh + 63 = octets 8 kh .. 8 kh + 7
         if (k >= 1) mbar_wait_warp(&stfree[kh], (k - 1) & 1);   // row GEMM of k-1 done with this K half
-        if (tid == 0) TC2_MARK(0, k, 3 + 2 * kh);
+        if (mark) TC2_MARK(0, k, 3 + 2 * kh);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int y = 64 * h + 8 * warp + r8;
+          const int y = 64 * h + 8 * pw + r8;
 #pragma unroll
           for (int ii = 0; ii < 2; ++ii) {
             const int i = 2 * kh + ii;
@@ -293,25 +303,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&staged[kh]);   // 8 arrivals: K half written by every producer warp
-        if (tid == 0) TC2_MARK(0, k, 4 + 2 * kh);
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) emax_t = max(emax_t, __shfl_xor_sync(0xffffffffu, emax_t, o));
-      if (lane == 0) emaxw[warp] = emax_t;
-      nbar(kBarProd2, kProd2);
-      if (k >= 2) mbar_wait_warp(&facfree[s], ((k >> 1) - 1) & 1);   // conversion of window k-2 done with fac[s]
-      if (tid < 128) {   // column-operand scale per row: D1 * 2^(e_y - e_max - 6) = R * 2^(8 - e_max) < 2^15
-        int em = emaxw[0];
-#pragma unroll
-        for (int j = 1; j < 8; ++j) em = max(em, emaxw[j]);
-        const int e = erow[tid];
-        fac[s * 128 + tid] = e > -1000 ? pow2f(e - em - 6) : 0.f;
-        if (tid == 0) emaxs[s] = em;
-      }
-      nbar(kBarProd2, kProd2);
-      if (tid == 0) {
-        mbar_arrive(&meta[s]);
-        TC2_MARK(0, k, 7);
+        if (mark) TC2_MARK(0, k, 4 + 2 * kh);
       }
     }
   } else if (warp == kTmaWarp) {
@@ -319,7 +311,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     for (int jh = pre; jh < 2 * nk; ++jh) {   // the whole warp walks the ring (converged), lane 0 issues
       const int slot = jh % kSlots;
       mbar_wait_warp(&landfree[slot], ((jh / kSlots) - 1) & 1);
-      if (lane == 0) issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, slot, &landfull[slot]);
+      if (elect_one()) issue_half<FMT>(p, &tmap, first + (jh >> 1) * gridDim.x, jh & 1, smem, slot, &landfull[slot]);
       __syncwarp();
     }
   } else if (warp == kMmaWarp) {
@@ -386,18 +378,25 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     }
   } else {
     // ================================= consumers =================================
-    const int ct = tid - kConsWarp0 * 32, quarter = warp & 3, sub = (warp - kConsWarp0) >> 2;
+    const int ct = tid, quarter = warp & 3, sub = warp >> 2;   // warps 0-2 (sub 0), 4-6 (sub 1)
     const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
-    const int n = quarter * 32 + lane, c = n & 63;   // D1 / D2 lane: Re R (n < 64) or Im R of column c
-    float gsv[2] = {1.f, 1.f};   // output scale of the windows in flight, read while fac / emaxs are ours
+    const int n = quarter * 32 + lane;   // D1 / D2 lane: Re R of column n (n < 42), Im R of column n - 42 (n < 84)
+    const bool re = n < kWinW, used = n < 2 * kWinW;
+    const int c = re ? n : n - kWinW;
+    float gsv[2] = {1.f, 1.f};   // output scale of the windows in flight, read while the slot's scales are ours
     auto convert = [&](int k) {
       // ---- D1(k) -> fp16 hi/lo in place (this warp: K half `sub`, two 32-column chunks)
       mbar_wait_warp(&meta[k & 1], (k >> 1) & 1);
-      gsv[k & 1] = pow2f(emaxs[k & 1] - 8);
+      int em = emaxw[k & 1][0];
+#pragma unroll
+      for (int j = 1; j < 8; ++j) em = max(em, emaxw[k & 1][j]);
+      // column-operand scale per row: D1 * 2^(e_y - e_max - 6) = R * 2^(8 - e_max) < 2^15
+      const float gdn = pow2f(max(-126, min(127, -em - 6)));
+      gsv[k & 1] = pow2f(max(-126, min(127, em - 8)));
       mbar_wait_warp(&d1full[k & 1], (k >> 1) & 1);
       tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 0);
-      const float* fs = fac + (k & 1) * 128;
+      const float* fs = facrow + (k & 1) * 128;
 #pragma unroll 1
       for (int j = 0; j < 2; ++j) {
         const int y0 = 64 * sub + 32 * j;
@@ -408,7 +407,8 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const float4 f4 = *reinterpret_cast<const float4*>(fs + y0 + 4 * e);
+          float4 f4 = *reinterpret_cast<const float4*>(fs + y0 + 4 * e);
+          f4.x *= gdn; f4.y *= gdn; f4.z *= gdn; f4.w *= gdn;
           split2(__uint_as_float(r[4 * e]) * f4.x, __uint_as_float(r[4 * e + 1]) * f4.y, hi[2 * e], lo[2 * e]);
           split2(__uint_as_float(r[4 * e + 2]) * f4.z, __uint_as_float(r[4 * e + 3]) * f4.w, hi[2 * e + 1],
                  lo[2 * e + 1]);
@@ -418,17 +418,17 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       }
       tmem_wait_st();
       tc_fence_before();
-      nbar(kBarSub0 + sub, 128);
+      nbar(kBarSub0 + sub, 96);
       if (ct == 0) TC2_MARK(1, k, 1);
-      if ((warp & 3) == 0 && lane == 0) mbar_arrive(&a2ready[k & 1][sub]);   // one arrival per K half
-      nbar(kBarCons2, kCons2);   // both halves converted: fac[k & 1] read by every consumer
+      if (quarter == 0 && lane == 0) mbar_arrive(&a2ready[k & 1][sub]);   // one arrival per K half
+      nbar(kBarCons2, kCons2);   // both halves converted: the slot's scales were read by every consumer
       if (ct == 0) mbar_arrive(&facfree[k & 1]);
     };
     float* xch = reinterpret_cast<float*>(smem + kXch);
-    const int mlo = c < kWinW ? ft.crange[2 * c] : 1, mhi = c < kWinW ? ft.crange[2 * c + 1] : 0;
+    const int mlo = used ? ft.crange[2 * c] : 1, mhi = used ? ft.crange[2 * c + 1] : 0;
     auto drain = [&](int k) {
       // ---- D2(k) -> W.  This warp holds columns 48 sub .. 48 sub + 47 of its lanes: Cr R (sub 0) or Ci R (sub 1)
-      // of Re R (n < 64) / Im R (n >= 64).  W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr): the sub-1 warps hand their
+      // of Re R (n < 42) / Im R (42 <= n < 84).  W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr): the sub-1 warps hand their
       // products over through shared memory, the sub-0 warps combine, mask (pipeline.py:72-76) and store.
       const float gs = gsv[k & 1];
       mbar_wait_warp(&d2full, k & 1);
@@ -441,14 +441,14 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       tc_fence_before();
       nbar(kBarCons2, kCons2);   // also: the sub-0 warps are done reading the previous window's exchange
       if (ct == 0) mbar_arrive(&d2free);   // D2 is in registers: the next column GEMM may start
-      if (sub == 1 && c < kWinW) {   // [Ci Rr | Ci Ri][r][c]
-        float* xo = xch + (n >= 64 ? kWinH * kWinW : 0) + c;
+      if (sub == 1 && used) {   // [Ci Rr | Ci Ri][r][c]
+        float* xo = xch + (re ? 0 : kWinH * kWinW) + c;
 #pragma unroll
         for (int rr = 0; rr < kWinH; ++rr) xo[rr * kWinW] = __uint_as_float(v[rr]);
       }
       nbar(kBarCons2, kCons2);
-      if (sub == 0 && c < kWinW) {   // planes: Re W (lanes n < 64), Im W (n >= 64); lanes = consecutive columns
-        const bool im = n >= 64;
+      if (sub == 0 && used) {   // planes: Re W (lanes n < 42), Im W (the next 42); lanes = consecutive columns
+        const bool im = !re;
         const float* xi = xch + (im ? 0 : kWinH * kWinW) + c;   // Im: + Ci Rr; Re: - Ci Ri
         const float sg = im ? gs : -gs;
         float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 2 + (im ? 1 : 0)) * (kWinH * kWinW) + c;
