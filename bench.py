@@ -348,6 +348,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tc", action="store_true", help="use the tcgen05 row-pass kernel (HPG_FLAG_TC)")
+    ap.add_argument("--simt", action="store_true", help="keep the fused SIMT kernel (HPG_FLAG_SIMT) where the two-kernel "
+                    "tensor-core path would be chosen")
     ap.add_argument("--tc2", action="store_true", help="use the two-kernel tensor-core path (HPG_FLAG_TC2)")
     ap.add_argument("--split", action="store_true",
                     help="strong scaling: divide the batch over WORLD_SIZE and include distributed.calc_metrics "
@@ -383,6 +385,7 @@ def main():
     h = api.create_handle()
     eng = api.engine(h)
     eng.use_tc = args.tc
+    eng.force_simt = args.simt
     eng.use_tc2 = args.tc2
     for k, v in cfg.items():
         setattr(eng.config, k, v)
@@ -447,11 +450,14 @@ def main():
 
     # DRAM traffic of the dominant kernel per launch, from the committed `ncu --set full`
     # capture of the same command (profiles/ncu_traffic.json); rescaled per launch size
-    if args.tc2:
-        kernel_name = "holo::fourier128_tc2_kernel+holo::field128_kernel<42,42>"
+    fast_geom = nx == 128 and ny == 128 and gh == 42 and gw == 42
+    if args.tc2 or (fast_geom and not args.tc and launches_per_step == 2):
+        # the two-kernel tensor-core path (chosen by hpg_run for large batches): the roofline is taken over
+        # the whole step (both kernels), against the same algorithmic bytes
+        kernel_name = "holo::fourier128_tc2_kernel+holo::tail42r_kernel"
     elif args.tc:
         kernel_name = "holo::fast128tc_kernel<42,42>"
-    elif nx == 128 and ny == 128 and gh == 42 and gw == 42:
+    elif fast_geom:
         kernel_name = "holo::fast128_kernel<42,42>"
     elif nx == 512 and ny == 512:
         # one hpg_run = the five L2-chunked large-window kernels; the roofline is taken over all of them

@@ -129,7 +129,8 @@ typedef struct hpg_outputs {
 #define HPG_FLAG_GENERIC 2u      /* diagnostic: force the generic (any-size) kernel */
 #define HPG_FLAG_SIMT 4u         /* diagnostic: specialised kernel without tensor cores */
 #define HPG_FLAG_TC 8u           /* tcgen05 row-pass kernel (warp-specialised) where it applies */
-#define HPG_FLAG_TC2 16u         /* two-kernel path: row + column DFT on tcgen05, then the field kernel */
+#define HPG_FLAG_TC2 16u         /* two-kernel path: row + column DFT on tcgen05, then the field kernel
+                                    (chosen automatically for large batches; HPG_FLAG_SIMT opts out) */
 #define HPG_FLAG_SIMT_OVERLAP 32u  /* diagnostic: HG overlap on SIMT instead of tcgen05 in the fast kernel */
 
 int hpg_version(void);

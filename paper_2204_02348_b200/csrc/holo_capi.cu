@@ -854,8 +854,15 @@ int hpg_run(const hpg_plan* P, const hpg_batch* b, const hpg_outputs* o, uint32_
     return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
   cudaError_t e;
   const int64_t items = (int64_t)b->batch_count * P->g.P;
-  if ((flags & HPG_FLAG_TC2) && !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
-      tc2_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows)) {
+  // Two-kernel tensor-core path (holo_tc2.cu): asked for with HPG_FLAG_TC2, and chosen automatically for
+  // batches of at least 6 windows per SM with a basis of at most 16 orders -- below that its persistent
+  // set-up and second launch cost more than they save, and larger bases run the tensor-core overlap of the
+  // fused kernel.  HPG_FLAG_SIMT / HPG_FLAG_TC / HPG_FLAG_GENERIC keep their kernels.
+  const bool tc2_ok = !(flags & (HPG_FLAG_GENERIC | HPG_FLAG_SIMT)) && !b->members &&
+                      tc2_supported(rp.g, A, b->frame_format, b->transpose, P->fill, b->ref_cal, flags, o->windows);
+  const bool tc2_auto = tc2_ok && !(flags & HPG_FLAG_TC) && items >= 6 * (int64_t)P->num_sms && rp.g.G <= 16 &&
+                        o->workspace && o->workspace_bytes >= tc2_workspace(items) && !getenv("HOLO_NO_TC2");
+  if (tc2_ok && ((flags & HPG_FLAG_TC2) || tc2_auto)) {
     if (!o->workspace || o->workspace_bytes < tc2_workspace((int64_t)b->batch_count * P->g.P))
       return fail(HPG_INVALIDARGUMENT, "workspace too small (hpg_workspace_size)");
     e = ensure_tc_tables(P);
