@@ -105,7 +105,8 @@ HOLO_DEV void tco_overlap(const RunParams& p, const FastTables& ft, int item, in
   tc_fence_after();
   const uint32_t idesc = idesc_f16(128, GP);
   const uint32_t sa = smem_u32(A), sb = smem_u32(bsm);
-  if (tid == 0) {   // GEMM 1: D1[row][m] = sum_x A[row][x] qx[m][x]
+  // issued under elect.sync by the converged warp 0 (holo_tc_common.cuh: 112 -> ~40 cycles per issued MMA)
+  if (warp == 0 && elect_one()) {   // GEMM 1: D1[row][m] = sum_x A[row][x] qx[m][x]
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) {
       const uint64_t ah = umma_desc(sa + ks * 256, 128, 768), al = umma_desc(sa + kTcoPart + ks * 256, 128, 768);
@@ -149,7 +150,7 @@ HOLO_DEV void tco_overlap(const RunParams& p, const FastTables& ft, int item, in
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (tid == 0) {   // GEMM 2: D2[row2][n] = sum_y A[row2][y] qy[n][y]
+  if (warp == 0 && elect_one()) {   // GEMM 2: D2[row2][n] = sum_y A[row2][y] qy[n][y]
 #pragma unroll
     for (int ks = 0; ks < 3; ++ks) {
       const uint64_t ah = umma_desc(sa + ks * 256, 128, 768), al = umma_desc(sa + kTcoPart + ks * 256, 128, 768);

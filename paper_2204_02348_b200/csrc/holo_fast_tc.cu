@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(kProd + kCons, 1) fast128tc_kernel(const __gri
       asm volatile("tcgen05.fence::before_thread_sync;");
       nbar(kBarProd, kProd);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      if (tid == 0) {
+      if (warp == 0 && elect_one()) {   // elect.sync: direct UTCHMMA issue (holo_tc_common.cuh)
         const uint32_t d = tm + 128 + 128 * s;
         const uint32_t sb = smem_u32(stage);
 #pragma unroll

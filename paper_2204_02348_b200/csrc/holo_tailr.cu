@@ -17,6 +17,7 @@
 //   phase 3  CTA-wide: coalesced int16 plane stores from the staged words; second contraction
 //            c[m, n] = sum_y U[m][y] hy[n][y], one (window, mode) per thread.
 #include <algorithm>
+#include <cstdlib>
 
 #include "holo_internal.h"
 #include "holo_tc_common.cuh"
@@ -87,7 +88,10 @@ inline TailRLayout tailr_layout(int G) {
 // win: [items][2][42 r][42 c] float, relative to item i0: Re / Im of K1's masked Fourier window
 // (holopipe/pipeline.py:72-127).  CTA (pol q, task): the three windows
 // i0 + q + P (3 task + {0, 1, 2}) (i0 is a multiple of P).
-__global__ void __launch_bounds__(kThr, 4)
+#ifndef TAILR_CTAS
+#define TAILR_CTAS 4
+#endif
+__global__ void __launch_bounds__(kThr, TAILR_CTAS)
     tail42r_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
                    const float* __restrict__ win, TailRLayout L) {
   extern __shared__ __align__(16) char smem[];
@@ -134,6 +138,9 @@ __global__ void __launch_bounds__(kThr, 4)
   __syncthreads();
   constexpr uint32_t kWinBytes = 2 * kN * kN * 4;
   if (tid == 0) {
+    // programmatic dependent launch: everything above overlapped the end of the Fourier kernel; its window
+    // buffer is complete (and visible) once the whole primary grid has finished
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     int nv = 0;
     for (int w = 0; w < kWin; ++w) nv += (i0 + q + P * (task * kWin + w)) < i1;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&landed)), "r"(nv * kWinBytes)
@@ -338,14 +345,27 @@ bool tailr_supported(const Geometry& g, const void* rcal) {
 }
 
 cudaError_t launch_tailr(const RunParams& p, const FastTables& ft, cudaStream_t s, int i0, int i1, const float* win) {
-  const TailRLayout L = tailr_layout(p.coefs ? p.g.G : 0);
+  TailRLayout L = tailr_layout(p.coefs ? p.g.G : 0);
+  if (getenv("HOLO_TAILR_HACK")) {   // timing experiment only (wrong coefficients): basis aliased onto window 0
+    L.basis_off = 0;
+    L.total = L.ph_off + 2 * kN * 8;
+  }
   cudaError_t e = ensure_smem_optin((const void*)tail42r_kernel, (size_t)L.total);
   if (e != cudaSuccess) return e;
   const int n = i1 - i0, P = p.g.P;
   const int per_pol = (n + P - 1) / P;
   const int grid = std::max(1, P * ((per_pol + kWin - 1) / kWin));
-  tail42r_kernel<<<grid, kThr, L.total, s>>>(p, ft, i0, i1, win, L);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThr);
+  cfg.dynamicSmemBytes = (size_t)L.total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddepcontrol.wait in the kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, tail42r_kernel, p, ft, i0, i1, win, L);
 }
 
 }  // namespace holo

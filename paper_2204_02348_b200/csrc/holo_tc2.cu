@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   // a2ready[b][h]: K half h of the converted D1 buffer b ready; d1free[b]: column GEMM done with D1 buffer b;
   // d2full: column GEMM done; d2free: D2 drained
   __shared__ __align__(8) uint64_t landfull[kSlots], landfree[kSlots], staged[2], stfree[2], meta[2], facfree[2],
-      d1full[2], a2ready[2][2], d1free[2], d2full, d2free, c2full;
+      d1full[2], a2ready[2][2], d1free[2], d2full, d2free, c2full, a1ready;
   __shared__ uint32_t tbase;
   __shared__ int emaxw[2][8];   // per window slot: largest row exponent seen by each producer warp
   float* facrow = reinterpret_cast<float*>(smem + kFac);
@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     }
     mbar_init(&d2full, 1);
     mbar_init(&c2full, 1);
+    mbar_init(&a1ready, 12);   // one arrival per warp that loads a chunk of the row-DFT constant
     mbar_init(&d2free, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
@@ -212,10 +213,11 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     for (int j = 0; j < 32; ++j) r[j] = __ldg(s2 + j * 128);
     tmem_st32(tA1 + ((uint32_t)(quarter * 32) << 16) + part * 64 + hh * 32, r);
     tmem_wait_st();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&a1ready);   // no CTA-wide barrier: the producers start on the first window at once
   }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
+  asm volatile("griddepcontrol.launch_dependents;");   // the tail's CTAs may take over SMs as this grid's CTAs exit
 
   if (warp >= kProdWarp0) {
     // ================================= producers =================================
@@ -369,7 +371,11 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       }
       __syncwarp();
     };
-    if (nk > 0) row_gemm(0);
+    if (nk > 0) {
+      mbar_wait_warp(&a1ready, 0);   // the row-DFT constant is in TMEM
+      tc_fence_after();
+      row_gemm(0);
+    }
     if (nk > 0) mbar_wait_warp(&c2full, 0);   // the column-DFT constant has landed
     for (int k = 0; k < nk; ++k) {
       if (k + 1 < nk) row_gemm(k + 1);
@@ -379,6 +385,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
   } else {
     // ================================= consumers =================================
     const int ct = tid, quarter = warp & 3, sub = warp >> 2;   // warps 0-2 (sub 0), 4-6 (sub 1)
+    const int ci = sub * 96 + quarter * 32 + lane;             // consumer thread index 0..191
     const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
     const int n = quarter * 32 + lane;   // D1 / D2 lane: Re R of column n (n < 42), Im R of column n - 42 (n < 84)
     const bool re = n < kWinW, used = n < 2 * kWinW;
@@ -393,6 +400,8 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       // column-operand scale per row: D1 * 2^(e_y - e_max - 6) = R * 2^(8 - e_max) < 2^15
       const float gdn = pow2f(max(-126, min(127, -em - 6)));
       gsv[k & 1] = pow2f(max(-126, min(127, em - 8)));
+      if (ci < 128) facrow[(k & 1) * 128 + ci] *= gdn;   // one multiply per row instead of one per element
+      nbar(kBarCons2, kCons2);
       mbar_wait_warp(&d1full[k & 1], (k >> 1) & 1);
       tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 0);
@@ -407,8 +416,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
         uint32_t hi[16], lo[16];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          float4 f4 = *reinterpret_cast<const float4*>(fs + y0 + 4 * e);
-          f4.x *= gdn; f4.y *= gdn; f4.z *= gdn; f4.w *= gdn;
+          const float4 f4 = *reinterpret_cast<const float4*>(fs + y0 + 4 * e);
           split2(__uint_as_float(r[4 * e]) * f4.x, __uint_as_float(r[4 * e + 1]) * f4.y, hi[2 * e], lo[2 * e]);
           split2(__uint_as_float(r[4 * e + 2]) * f4.z, __uint_as_float(r[4 * e + 3]) * f4.w, hi[2 * e + 1],
                  lo[2 * e + 1]);
@@ -673,7 +681,7 @@ static cudaError_t frame_tensor_map(const RunParams& p, CUtensorMap* map) {
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = encode(map, p.fmt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
                       const_cast<void*>(p.frames), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
