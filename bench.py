@@ -454,7 +454,7 @@ def main():
     if args.tc2 or (fast_geom and not args.tc and launches_per_step == 2):
         # the two-kernel tensor-core path (chosen by hpg_run for large batches): the roofline is taken over
         # the whole step (both kernels), against the same algorithmic bytes
-        kernel_name = "holo::fourier128_tc2_kernel+holo::tail42r_kernel"
+        kernel_name = "holo::fourier128_tc2_kernel+holo::tail42p_kernel"
     elif args.tc:
         kernel_name = "holo::fast128tc_kernel<42,42>"
     elif fast_geom:

@@ -685,6 +685,8 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.tco_gp = tco_ok ? GP16 : 0;
   // HG parity on the symmetric part of the field axes (pipeline.py:152-160 puts the origin at index w / 2),
   // verified bit for bit on the quantised profiles: the fast kernel then folds each +-d pair of the overlap
+  P->ft.hx_host = P->hx.empty() ? nullptr : P->hx.data();
+  P->ft.hy_host = P->hy.empty() ? nullptr : P->hy.data();
   P->ft.hsym = 0;
   for (int q = 0; q < g.P && G > 0; ++q) {
     for (int ax = 0; ax < 2; ++ax) {

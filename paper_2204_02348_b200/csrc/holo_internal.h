@@ -43,6 +43,8 @@ struct FastTables {
   const uint4* tco_img;    // [P][hx hi, hx lo, hy hi, hy lo][GP16 x 48 halves]: exact fp16 split of the int16 basis
   const float* tco_inv;    // [P][2][GP16] 1 / per-order basis scale (x, y)
   int tco_gp;              // GP16 (0: tensor-core overlap unavailable)
+  const float* hx_host;    // HOST copies of the dequantised basis [P][G][gw] / [P][G][gh] (kernel-parameter basis of
+  const float* hy_host;    // holo_tailr.cu); never dereferenced on the device
   int hsym;                // bit 2q: pol q's x profiles satisfy h_m(c - d) = (-1)^m h_m(c + d) exactly on the
                            // quantised basis (c = gw / 2, the axis origin); bit 2q + 1: the y profiles
 };

@@ -85,15 +85,89 @@ inline TailRLayout tailr_layout(int G) {
   return L;
 }
 
+// Basis profiles passed as a kernel parameter (constant bank): with every index a compile-time constant the
+// overlap FMAs take their basis value as a constant operand -- no loads, no registers, no shared memory,
+// which lets five CTAs fit an SM (the whole 2,000-window dual-pol batch resident in one wave).
+constexpr int kPG = 16;   // padded order count of the parameter-basis variant
+struct TailBasis {
+  float hx[kMaxPol][kN * kPG];   // [pol][x][m], zero beyond G
+  float hy[kMaxPol][kN * kPG];   // [pol][y][n]
+};
+struct NoBasis {
+  int unused;
+};
+
+namespace {
+
+// U[m][y = s] = sum_x F[y][x] hx[m][x] for the x-symmetric basis of pol Q; v holds the folded row
+// (v[pos(21 + d)] = F(21 + d) + F(21 - d), v[pos(21 - d)] = the difference, d = 1..20; x = 21 and x = 0 plain)
+template <int Q>
+HOLO_DEV void overlap_x_param(const TailBasis& tb, const float2 (&v)[kN], float2* U, int s) {
+  constexpr int CX = kN / 2;
+#pragma unroll
+  for (int mq = 0; mq < kPG / 4; ++mq) {
+    float ar[4], ai[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float h0 = tb.hx[Q][CX * kPG + 4 * mq + j], h1 = tb.hx[Q][4 * mq + j];
+      ar[j] = fmaf(v[pos_of(0)].x, h1, v[pos_of(CX)].x * h0);
+      ai[j] = fmaf(v[pos_of(0)].y, h1, v[pos_of(CX)].y * h0);
+    }
+#pragma unroll
+    for (int d = 1; d < CX; ++d) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {   // even orders take the sums, odd orders the differences
+        const float2 a = (j & 1) ? v[pos_of(CX - d)] : v[pos_of(CX + d)];
+        const float h = tb.hx[Q][(CX + d) * kPG + 4 * mq + j];
+        ar[j] = fmaf(a.x, h, ar[j]);
+        ai[j] = fmaf(a.y, h, ai[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) U[(4 * mq + j) * kP + s] = make_float2(ar[j], ai[j]);
+  }
+}
+
+// c[m, n] = sum_y U[m][y] hy[n][y] for every n of one (window, m), y-symmetric basis of pol Q
+template <int Q>
+HOLO_DEV void overlap_y_param(const TailBasis& tb, const float2* Um, int m, int G, float d, float2* out) {
+  constexpr int CY = kN / 2;
+  float ax[kPG], ay[kPG];
+  {
+    const float2 u0 = Um[CY], u1 = Um[0];
+#pragma unroll
+    for (int n = 0; n < kPG; ++n) {
+      const float h0 = tb.hy[Q][CY * kPG + n], h1 = tb.hy[Q][n];
+      ax[n] = fmaf(u1.x, h1, u0.x * h0);
+      ay[n] = fmaf(u1.y, h1, u0.y * h0);
+    }
+  }
+#pragma unroll 4
+  for (int dd = 1; dd < CY; ++dd) {
+    const float2 vp = Um[CY + dd], vm = Um[CY - dd];
+    const float2 se = cadd(vp, vm), so = csub(vp, vm);
+#pragma unroll
+    for (int n = 0; n < kPG; ++n) {
+      const float h = tb.hy[Q][(CY + dd) * kPG + n];
+      ax[n] = fmaf((n & 1) ? so.x : se.x, h, ax[n]);
+      ay[n] = fmaf((n & 1) ? so.y : se.y, h, ay[n]);
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < kPG; ++n) {
+    const int gg = m + n;   // group-major mode index (hgbasis.py:17-27)
+    if (gg < G) out[gg * (gg + 1) / 2 + n] = make_float2(ax[n] * d, ay[n] * d);
+  }
+}
+
+}  // namespace
+
 // win: [items][2][42 r][42 c] float, relative to item i0: Re / Im of K1's masked Fourier window
 // (holopipe/pipeline.py:72-127).  CTA (pol q, task): the three windows
 // i0 + q + P (3 task + {0, 1, 2}) (i0 is a multiple of P).
-#ifndef TAILR_CTAS
-#define TAILR_CTAS 4
-#endif
-__global__ void __launch_bounds__(kThr, TAILR_CTAS)
-    tail42r_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
-                   const float* __restrict__ win, TailRLayout L) {
+template <bool PB, class TB>
+HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1, const float* __restrict__ win,
+                        const TailRLayout& L, const TB& tb) {
   extern __shared__ __align__(16) char smem[];
   __shared__ int s_max[kWin];
   __shared__ float s_scale[kWin];
@@ -117,7 +191,7 @@ __global__ void __launch_bounds__(kThr, TAILR_CTAS)
     sex[i] = p.t.rem_x[q * g.L * kN + i];
     sey[i] = p.t.rem_y[q * g.L * kN + i];
   }
-  if (G > 0) {   // basis of this pol, transposed [x][m] / [y][n] (hgbasis.py:95-99 profiles)
+  if (!PB && G > 0) {   // basis of this pol, transposed [x][m] / [y][n] (hgbasis.py:95-99 profiles)
     const float* hx = p.t.hx + (size_t)q * g.G * kN;
     const float* hy = p.t.hy + (size_t)q * g.G * kN;
     for (int i = tid; i < kN * GP; i += kThr) {
@@ -231,6 +305,11 @@ __global__ void __launch_bounds__(kThr, TAILR_CTAS)
         v[pos_of(CX + d)] = cadd(a, c);
         v[pos_of(CX - d)] = csub(a, c);
       }
+    }
+    if constexpr (PB) {   // launched only for symmetric bases of at most kPG orders
+      if (q == 0) overlap_x_param<0>(tb, v, U, s);
+      else overlap_x_param<1>(tb, v, U, s);
+    } else if (xsym) {
 #pragma unroll 1
       for (int mq = 0; mq < GQ; ++mq) {
         const float* hq = hxT + 4 * mq;
@@ -283,6 +362,22 @@ __global__ void __launch_bounds__(kThr, TAILR_CTAS)
 
   // ------------------------------------------------------------------ phase 3 (CTA-wide)
   const int item0 = i0 + q + P * (task * kWin);
+  // parameter-basis variant: threads 0..47 = (window, m) run the second contraction while the other 80 store
+  constexpr int kYThr = PB ? kWin * kPG : 0;
+  if (PB && tid < kYThr) {
+    const int w = tid / kPG, m = tid - w * kPG;
+    const int it = item0 + P * w;
+    if (G > 0 && it < i1 && m < G) {
+      const float2* Um = reinterpret_cast<const float2*>(smem + w * L.win_bytes + kN * kP * 4) + m * kP;
+      const float d = __fdiv_rn(g.dxdy[q], s_scale[w]);
+      float2* out = p.coefs + (size_t)it * g.M;
+      if constexpr (PB) {
+        if (q == 0) overlap_y_param<0>(tb, Um, m, G, d, out);
+        else overlap_y_param<1>(tb, Um, m, G, d, out);
+      }
+    }
+    return;
+  }
 #pragma unroll 1
   for (int w = 0; w < kWin; ++w) {   // int16 planes, natural [y][x], coalesced (pipeline.py:188-199)
     const int it = item0 + P * w;
@@ -290,14 +385,14 @@ __global__ void __launch_bounds__(kThr, TAILR_CTAS)
     const uint32_t* fw = reinterpret_cast<const uint32_t*>(smem + w * L.win_bytes);
     uint32_t* fro = reinterpret_cast<uint32_t*>(p.fr + (size_t)it * kN * kN);
     uint32_t* fio = reinterpret_cast<uint32_t*>(p.fi + (size_t)it * kN * kN);
-    for (int i = tid; i < kN * kN / 2; i += kThr) {
+    for (int i = tid - kYThr; i < kN * kN / 2; i += kThr - kYThr) {
       const int y = i / (kN / 2), xp = i - y * (kN / 2);
       const uint32_t a = fw[y * kP + 2 * xp], c = fw[y * kP + 2 * xp + 1];
       fro[i] = __byte_perm(a, c, 0x5410);
       fio[i] = __byte_perm(a, c, 0x7632);
     }
   }
-  if (G > 0) {   // second contraction; the dequantisation 1/scale (engine.py:367-369) once per coefficient
+  if (!PB && G > 0) {   // second contraction; the dequantisation 1/scale (engine.py:367-369) once per coefficient
     const bool ysym = (ft.hsym >> (2 * q + 1)) & 1;
     constexpr int CY = kN / 2;
     const int M = g.M;
@@ -339,32 +434,60 @@ __global__ void __launch_bounds__(kThr, TAILR_CTAS)
   }
 }
 
+__global__ void __launch_bounds__(kThr, 4)
+    tail42r_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
+                   const float* __restrict__ win, TailRLayout L) {
+  tail_body<false>(p, ft, i0, i1, win, L, NoBasis{0});
+}
+
+// parameter-basis variant: symmetric bases of at most kPG orders, five CTAs per SM
+__global__ void __launch_bounds__(kThr, 5)
+    tail42p_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
+                   const float* __restrict__ win, TailRLayout L, const __grid_constant__ TailBasis tb) {
+  tail_body<true>(p, ft, i0, i1, win, L, tb);
+}
+
 bool tailr_supported(const Geometry& g, const void* rcal) {
   return g.wh == kN && g.ww == kN && g.gh == kN && g.gw == kN && g.G <= 48 && g.L == 1 && g.P <= kMaxPol &&
          rcal == nullptr && tailr_layout(g.G).total <= 110 * 1024;
 }
 
 cudaError_t launch_tailr(const RunParams& p, const FastTables& ft, cudaStream_t s, int i0, int i1, const float* win) {
-  TailRLayout L = tailr_layout(p.coefs ? p.g.G : 0);
-  if (getenv("HOLO_TAILR_HACK")) {   // timing experiment only (wrong coefficients): basis aliased onto window 0
-    L.basis_off = 0;
-    L.total = L.ph_off + 2 * kN * 8;
-  }
-  cudaError_t e = ensure_smem_optin((const void*)tail42r_kernel, (size_t)L.total);
-  if (e != cudaSuccess) return e;
+  const int G = p.coefs ? p.g.G : 0;
   const int n = i1 - i0, P = p.g.P;
   const int per_pol = (n + P - 1) / P;
   const int grid = std::max(1, P * ((per_pol + kWin - 1) / kWin));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThr);
-  cfg.dynamicSmemBytes = (size_t)L.total;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // see griddepcontrol.wait in the kernel
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const bool all_sym = (ft.hsym & ((1 << (2 * P)) - 1)) == (1 << (2 * P)) - 1;
+  const char* env = getenv("HOLO_TAILR_SMEM_BASIS");   // diagnostic: keep the shared-memory basis variant
+  if (G > 0 && G <= kPG && all_sym && ft.hx_host && ft.hy_host && !(env && env[0] == '1')) {
+    TailRLayout L = tailr_layout(0);   // no basis in shared memory; U of kPG orders fits the window region
+    static_assert(kN * kP * 4 + kPG * kP * 8 <= kN * kP * 8, "Fq + U must fit the window region");
+    TailBasis tb;
+    for (int q = 0; q < kMaxPol; ++q)
+      for (int x = 0; x < kN; ++x)
+        for (int m = 0; m < kPG; ++m) {
+          const bool on = q < P && m < G;
+          tb.hx[q][x * kPG + m] = on ? ft.hx_host[((size_t)q * G + m) * kN + x] : 0.f;
+          tb.hy[q][x * kPG + m] = on ? ft.hy_host[((size_t)q * G + m) * kN + x] : 0.f;
+        }
+    cudaError_t e = ensure_smem_optin((const void*)tail42p_kernel, (size_t)L.total);
+    if (e != cudaSuccess) return e;
+    cfg.dynamicSmemBytes = (size_t)L.total;
+    return cudaLaunchKernelEx(&cfg, tail42p_kernel, p, ft, i0, i1, win, L, tb);
+  }
+  const TailRLayout L = tailr_layout(G);
+  cudaError_t e = ensure_smem_optin((const void*)tail42r_kernel, (size_t)L.total);
+  if (e != cudaSuccess) return e;
+  cfg.dynamicSmemBytes = (size_t)L.total;
   return cudaLaunchKernelEx(&cfg, tail42r_kernel, p, ft, i0, i1, win, L);
 }
 
