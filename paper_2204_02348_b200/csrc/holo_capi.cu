@@ -322,13 +322,13 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
     }
   }
   if (a_tc.empty()) a_tc.push_back(0u);
-  // the same matrix with packed rows for the two-kernel path (holo_tc2.cu): row c < ww -> Re, row ww + c -> Im
+  // the same matrix with packed, interleaved rows for the two-kernel path (holo_tc2.cu): row 2c -> Re, 2c + 1 -> Im
   std::vector<uint32_t> a_tcp;
   if (g.nx == 128 && g.ww <= 64) {
     a_tcp.assign((size_t)g.P * 2 * 128 * 64, 0u);
     for (int q = 0; q < g.P; ++q)
       for (int n = 0; n < 2 * g.ww; ++n) {
-        const int src = n < g.ww ? n : 64 + (n - g.ww);
+        const int src = (n & 1) ? 64 + (n >> 1) : (n >> 1);
         for (int part = 0; part < 2; ++part)
           for (int x2 = 0; x2 < 64; ++x2)
             a_tcp[(((size_t)q * 2 + part) * 64 + x2) * 128 + n] = a_tc[(((size_t)q * 2 + part) * 64 + x2) * 128 + src];

@@ -37,7 +37,7 @@ struct FastTables {
   const float2* py;        // [P][L][WH] recentring phase along y
   const int16_t* crange;   // [WW][2] first/last row inside the circular mask, per column
   const uint32_t* a_tc;    // [P][2][128][64] f16x2: row-DFT matrix (hi, lo) for wavelength 0
-  const uint32_t* a_tcp;   // the same matrix with the rows packed: Re of column c at row c, Im at row ww + c (holo_tc2.cu)
+  const uint32_t* a_tcp;   // the same matrix with the rows packed: Re of column c at row 2c, Im at row 2c + 1 (holo_tc2.cu)
   const uint32_t* a2_tc;   // [P][2][128][64] f16x2: column-DFT matrix [Cr; Ci] (hi, lo) for wavelength 0
   const uint4* c2_tc;      // [P][hi | lo][24 KB]: the same [Cr; Ci] as a K-major shared-memory B operand
   const uint4* tco_img;    // [P][hx hi, hx lo, hy hi, hy lo][GP16 x 48 halves]: exact fp16 split of the int16 basis

@@ -37,7 +37,7 @@ namespace holo {
 namespace {
 
 // Warp roles.  A warp reaches the TMEM lane quarter warp % 4, and the DFT rows are packed into lanes 0..83
-// (Re R of column c at lane c, Im R at lane 42 + c), so the six consumer warps are the ones with
+// (Re R of column c at lane 2c, Im R at lane 2c + 1), so the six consumer warps are the ones with
 // warp % 4 < 3 among warps 0-7; warps 3 and 7 issue the MMAs and the TMA loads; warps 8-15 are the producers.
 constexpr int kMmaWarp = 3;                 // tcgen05.mma issuer
 constexpr int kTmaWarp = 7;                 // TMA issuer
@@ -59,8 +59,7 @@ constexpr uint32_t kStageHalf = 32768;
 constexpr uint32_t kC2 = kStage + 2 * kStageHalf;  // column-DFT constant [Cr; Ci]: hi | lo
 constexpr uint32_t kC2Part = 8 * 3072;             // [8 ksteps][12 ngroups][2][8][16 B]
 constexpr uint32_t kFac = kC2 + 2 * kC2Part;       // facrow[2][128] f32: 2^e_y of every window row
-constexpr uint32_t kXch = kFac + 2 * 128 * 4;      // consumer exchange [Ci Rr | Ci Ri][42 r][42 c] f32
-constexpr uint32_t kK1Bytes = kXch + 2 * 42 * 42 * 4;
+constexpr uint32_t kK1Bytes = kFac + 2 * 128 * 4;
 static_assert(kK1Bytes <= 227 * 1024 - 1024, "K1 shared memory");
 
 // canonical K-major, no-swizzle operand layout: [kstep][row/8][khalf][row%8][8 halves]
@@ -182,7 +181,7 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     mbar_init(&d2full, 1);
     mbar_init(&c2full, 1);
     mbar_init(&a1ready, 12);   // one arrival per warp that loads a chunk of the row-DFT constant
-    mbar_init(&d2free, 1);
+    mbar_init(&d2free, kCons2 / 32);   // D2 copied to registers: one arrival per consumer warp
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   tc_fence_before();
@@ -387,9 +386,9 @@ __global__ void __launch_bounds__(kK1Threads, 1)
     const int ct = tid, quarter = warp & 3, sub = warp >> 2;   // warps 0-2 (sub 0), 4-6 (sub 1)
     const int ci = sub * 96 + quarter * 32 + lane;             // consumer thread index 0..191
     const uint32_t lanebase = (uint32_t)(quarter * 32) << 16;
-    const int n = quarter * 32 + lane;   // D1 / D2 lane: Re R of column n (n < 42), Im R of column n - 42 (n < 84)
-    const bool re = n < kWinW, used = n < 2 * kWinW;
-    const int c = re ? n : n - kWinW;
+    const int n = quarter * 32 + lane;   // D1 / D2 lane: Re R (even n) / Im R (odd n) of column n / 2, n < 84
+    const bool im = n & 1, used = n < 2 * kWinW;
+    const int c = n >> 1;
     float gsv[2] = {1.f, 1.f};   // output scale of the windows in flight, read while the slot's scales are ours
     auto convert = [&](int k) {
       // ---- D1(k) -> fp16 hi/lo in place (this warp: K half `sub`, two 32-column chunks)
@@ -432,39 +431,32 @@ __global__ void __launch_bounds__(kK1Threads, 1)
       nbar(kBarCons2, kCons2);   // both halves converted: the slot's scales were read by every consumer
       if (ct == 0) mbar_arrive(&facfree[k & 1]);
     };
-    float* xch = reinterpret_cast<float*>(smem + kXch);
     const int mlo = used ? ft.crange[2 * c] : 1, mhi = used ? ft.crange[2 * c + 1] : 0;
     auto drain = [&](int k) {
-      // ---- D2(k) -> W.  This warp holds columns 48 sub .. 48 sub + 47 of its lanes: Cr R (sub 0) or Ci R (sub 1)
-      // of Re R (n < 42) / Im R (42 <= n < 84).  W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr): the sub-1 warps hand their
-      // products over through shared memory, the sub-0 warps combine, mask (pipeline.py:72-76) and store.
+      // ---- D2(k) -> W = (Cr Rr - Ci Ri) + i (Cr Ri + Ci Rr).  D2 columns r hold Cr R, columns 48 + r hold
+      // Ci R of the lane's R part; the Re / Im lanes of a column are neighbours, so the cross term comes by one
+      // shuffle.  This warp handles the 24 rows r = 24 sub .. 24 sub + 23; masked (pipeline.py:72-76) stores.
       const float gs = gsv[k & 1];
       mbar_wait_warp(&d2full, k & 1);
       tc_fence_after();
       if (ct == 0) TC2_MARK(1, k, 5);
-      uint32_t v[48];
-      tmem_ld32(tD2 + lanebase + kN2 * sub, v);
-      tmem_ld16(tD2 + lanebase + kN2 * sub + 32, v + 32);
+      uint32_t a[24], b[24];
+      tmem_ld16(tD2 + lanebase + 24 * sub, a);
+      tmem_ld8(tD2 + lanebase + 24 * sub + 16, a + 16);
+      tmem_ld16(tD2 + lanebase + kN2 + 24 * sub, b);
+      tmem_ld8(tD2 + lanebase + kN2 + 24 * sub + 16, b + 16);
       tmem_wait_ld();
       tc_fence_before();
-      nbar(kBarCons2, kCons2);   // also: the sub-0 warps are done reading the previous window's exchange
-      if (ct == 0) mbar_arrive(&d2free);   // D2 is in registers: the next column GEMM may start
-      if (sub == 1 && used) {   // [Ci Rr | Ci Ri][r][c]
-        float* xo = xch + (re ? 0 : kWinH * kWinW) + c;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d2free);   // D2 is in registers (6 arrivals): the next column GEMM may start
+      const float sg = im ? gs : -gs;        // Im: + Ci Rr (from the Re lane); Re: - Ci Ri (from the Im lane)
+      float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 2 + (im ? 1 : 0)) * (kWinH * kWinW) + c;
 #pragma unroll
-        for (int rr = 0; rr < kWinH; ++rr) xo[rr * kWinW] = __uint_as_float(v[rr]);
-      }
-      nbar(kBarCons2, kCons2);
-      if (sub == 0 && used) {   // planes: Re W (lanes n < 42), Im W (the next 42); lanes = consecutive columns
-        const bool im = !re;
-        const float* xi = xch + (im ? 0 : kWinH * kWinW) + c;   // Im: + Ci Rr; Re: - Ci Ri
-        const float sg = im ? gs : -gs;
-        float* wo = wout + ((size_t)(first + k * gridDim.x - i0) * 2 + (im ? 1 : 0)) * (kWinH * kWinW) + c;
-#pragma unroll
-        for (int rr = 0; rr < kWinH; ++rr) {
-          const float val = fmaf(xi[rr * kWinW], sg, __uint_as_float(v[rr]) * gs);
-          wo[rr * kWinW] = (rr >= mlo && rr <= mhi) ? val : 0.f;
-        }
+      for (int j = 0; j < 24; ++j) {
+        const int rr = 24 * sub + j;
+        const float other = __uint_as_float(__shfl_xor_sync(0xffffffffu, b[j], 1));
+        const float val = fmaf(other, sg, __uint_as_float(a[j]) * gs);
+        if (used && rr < kWinH) wo[rr * kWinW] = (rr >= mlo && rr <= mhi) ? val : 0.f;
       }
       if (ct == 0) TC2_MARK(1, k, 6);
     };
@@ -679,9 +671,15 @@ static cudaError_t frame_tensor_map(const RunParams& p, CUtensorMap* map) {
   const cuuint64_t strides[2] = {(cuuint64_t)p.g.W * es, (cuuint64_t)p.g.W * p.g.H * es};
   const cuuint32_t box[3] = {(cuuint32_t)(128 / es), 32, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
+  const char* env = getenv("HOLO_TMA_PROMO");   // diagnostic: 0 none, 1 64 B, 2 128 B (default: measured best), 3 256 B
+  const CUtensorMapL2promotion promo = !env ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                       : env[0] == '0' ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                       : env[0] == '1' ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                       : env[0] == '2' ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                       : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
   CUresult r = encode(map, p.fmt == 0 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16, 3,
                       const_cast<void*>(p.frames), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_SWIZZLE_128B, promo,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
