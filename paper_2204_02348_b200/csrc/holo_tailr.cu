@@ -101,15 +101,15 @@ namespace {
 
 // U[m][y = s] = sum_x F[y][x] hx[m][x] for the x-symmetric basis of pol Q; v holds the folded row
 // (v[pos(21 + d)] = F(21 + d) + F(21 - d), v[pos(21 - d)] = the difference, d = 1..20; x = 21 and x = 0 plain)
-template <int Q>
-HOLO_DEV void overlap_x_param(const TailBasis& tb, const float2 (&v)[kN], float2* U, int s) {
+// (q and mq are warp-uniform: the basis values come through uniform-register constant loads, one code copy)
+HOLO_DEV void overlap_x_param(const TailBasis& tb, int q, const float2 (&v)[kN], float2* U, int s) {
   constexpr int CX = kN / 2;
-#pragma unroll
+#pragma unroll 1
   for (int mq = 0; mq < kPG / 4; ++mq) {
     float ar[4], ai[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float h0 = tb.hx[Q][CX * kPG + 4 * mq + j], h1 = tb.hx[Q][4 * mq + j];
+      const float h0 = tb.hx[q][CX * kPG + 4 * mq + j], h1 = tb.hx[q][4 * mq + j];
       ar[j] = fmaf(v[pos_of(0)].x, h1, v[pos_of(CX)].x * h0);
       ai[j] = fmaf(v[pos_of(0)].y, h1, v[pos_of(CX)].y * h0);
     }
@@ -118,7 +118,7 @@ HOLO_DEV void overlap_x_param(const TailBasis& tb, const float2 (&v)[kN], float2
 #pragma unroll
       for (int j = 0; j < 4; ++j) {   // even orders take the sums, odd orders the differences
         const float2 a = (j & 1) ? v[pos_of(CX - d)] : v[pos_of(CX + d)];
-        const float h = tb.hx[Q][(CX + d) * kPG + 4 * mq + j];
+        const float h = tb.hx[q][(CX + d) * kPG + 4 * mq + j];
         ar[j] = fmaf(a.x, h, ar[j]);
         ai[j] = fmaf(a.y, h, ai[j]);
       }
@@ -129,15 +129,14 @@ HOLO_DEV void overlap_x_param(const TailBasis& tb, const float2 (&v)[kN], float2
 }
 
 // c[m, n] = sum_y U[m][y] hy[n][y] for every n of one (window, m), y-symmetric basis of pol Q
-template <int Q>
-HOLO_DEV void overlap_y_param(const TailBasis& tb, const float2* Um, int m, int G, float d, float2* out) {
+HOLO_DEV void overlap_y_param(const TailBasis& tb, int q, const float2* Um, int m, int G, float d, float2* out) {
   constexpr int CY = kN / 2;
   float ax[kPG], ay[kPG];
   {
     const float2 u0 = Um[CY], u1 = Um[0];
 #pragma unroll
     for (int n = 0; n < kPG; ++n) {
-      const float h0 = tb.hy[Q][CY * kPG + n], h1 = tb.hy[Q][n];
+      const float h0 = tb.hy[q][CY * kPG + n], h1 = tb.hy[q][n];
       ax[n] = fmaf(u1.x, h1, u0.x * h0);
       ay[n] = fmaf(u1.y, h1, u0.y * h0);
     }
@@ -148,7 +147,7 @@ HOLO_DEV void overlap_y_param(const TailBasis& tb, const float2* Um, int m, int 
     const float2 se = cadd(vp, vm), so = csub(vp, vm);
 #pragma unroll
     for (int n = 0; n < kPG; ++n) {
-      const float h = tb.hy[Q][(CY + dd) * kPG + n];
+      const float h = tb.hy[q][(CY + dd) * kPG + n];
       ax[n] = fmaf((n & 1) ? so.x : se.x, h, ax[n]);
       ay[n] = fmaf((n & 1) ? so.y : se.y, h, ay[n]);
     }
@@ -307,8 +306,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
       }
     }
     if constexpr (PB) {   // launched only for symmetric bases of at most kPG orders
-      if (q == 0) overlap_x_param<0>(tb, v, U, s);
-      else overlap_x_param<1>(tb, v, U, s);
+      overlap_x_param(tb, q, v, U, s);
     } else if (xsym) {
 #pragma unroll 1
       for (int mq = 0; mq < GQ; ++mq) {
@@ -371,10 +369,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
       const float2* Um = reinterpret_cast<const float2*>(smem + w * L.win_bytes + kN * kP * 4) + m * kP;
       const float d = __fdiv_rn(g.dxdy[q], s_scale[w]);
       float2* out = p.coefs + (size_t)it * g.M;
-      if constexpr (PB) {
-        if (q == 0) overlap_y_param<0>(tb, Um, m, G, d, out);
-        else overlap_y_param<1>(tb, Um, m, G, d, out);
-      }
+      if constexpr (PB) overlap_y_param(tb, q, Um, m, G, d, out);
     }
     return;
   }
