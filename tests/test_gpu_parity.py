@@ -233,6 +233,69 @@ def test_two_kernel_tensor_core_path_matches_reference(name):
     assert rel_l2_rows(coefs, g["coefs"]) <= COEF_TOL
 
 
+def _outputs(eng):
+    out = [t.cpu().numpy().copy() for t in eng.fields16_device()]
+    co = eng.coefs_device()
+    return out + [None if co is None or co.numel() == 0 else co.cpu().numpy().copy()]
+
+
+def test_two_kernel_path_uint16_frames_equal_float32():
+    """The Fourier kernel's uint16 instantiation (camera format, holopipe/frames.py:49-59): bit-equal to the
+    float32 run of the same integers."""
+    case, g, frames = load("dualpol")
+    frames = np.rint(frames)
+    a = _engine(case, frames.astype(np.float32))
+    a.use_tc2 = True
+    a.run_pipeline(0)
+    b = _engine(case, frames.astype(np.float32))
+    b.source.set_uint16(frames.astype(np.uint16))
+    b.use_tc2 = True
+    b.run_pipeline(0)
+    for x, y in zip(_outputs(a), _outputs(b)):
+        assert np.array_equal(x, y)
+
+
+def test_two_kernel_path_fields_only():
+    """No basis (basisGroupCount 0): the tail stops after the int16 fields; same fields as the fused kernel."""
+    case, g, frames = load("dualpol")
+    case = dict(case, config=dict(case["config"], basisGroupCount=0))
+    a = _engine(case, frames)
+    a.use_tc2 = True
+    a.run_pipeline(0)
+    b = _engine(case, frames)
+    b.run_pipeline(0)
+    fa, fb = _outputs(a), _outputs(b)
+    assert fa[3] is None and fb[3] is None
+    assert np.abs(fa[0].astype(int) - fb[0]).max() <= 2 and np.abs(fa[1].astype(int) - fb[1]).max() <= 2
+    assert np.allclose(fa[2], fb[2], rtol=1e-5)
+    ef = rel_l2_rows(dequant(fa[0], fa[1], fa[2]), dequant(g["fr"], g["fi"], g["scale"]))
+    assert ef <= FIELD_TOL
+
+
+def test_two_kernel_path_chosen_for_large_batches_and_chunked():
+    """hpg_run picks the two-kernel path by itself for >= 6 windows per SM; 1,100 dual-pol rows = 2,200 windows
+    cross its 2,048-window chunk boundary.  Every repetition of the tiled golden frames must reproduce the
+    first bit for bit, and the rows must match the reference fixture."""
+    import torch
+    from paper_2204_02348_b200 import native
+    case, g, frames = load("dualpol")
+    n = frames.shape[0]
+    rows = 1100
+    reps = -(-rows // n)
+    big = np.ascontiguousarray(np.concatenate([frames] * reps)[:rows])
+    case = dict(case, config=dict(case["config"], batchCount=rows))
+    eng = _engine(case, torch.from_numpy(big).cuda())
+    eng.run_pipeline(0)
+    assert native.lib().hpg_last_launch_count() == 4   # two chunks x (Fourier kernel + tail)
+    fr, fi, sc, co = _outputs(eng)
+    for r in range(1, rows // n):
+        for x in (fr, fi, sc, co):
+            assert np.array_equal(x[r * n:(r + 1) * n], x[:n])
+    ef = rel_l2_rows(dequant(fr[:n], fi[:n], sc[:n]), dequant(g["fr"], g["fi"], g["scale"]))
+    assert ef <= FIELD_TOL
+    assert rel_l2_rows(co[:n], g["coefs"]) <= COEF_TOL
+
+
 @pytest.mark.parametrize("name", ["dualpol", "pr1", "multiwl"])
 def test_pipelined_process_batch_matches_staged(name):
     """api.process_batch on host frames (chunked upload / kernel / readback) == run_pipeline + coef_view."""
