@@ -679,7 +679,9 @@ __global__ void __launch_bounds__(512) lw_rows512_kernel(const __grid_constant__
                         (int64_t)(g.row0[q] + y) * g.W + g.col0[q];
       const float* rb = ra + (int64_t)ny2 * g.W;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) a[st][j] = make_float2(__ldg(ra + t + 64 * j), __ldg(rb + t + 64 * j));
+      // streaming (evict-first) loads: the frame is read once and must not push the row-pass output R,
+      // which the column kernel reads back from L2, out to DRAM
+      for (int j = 0; j < 8; ++j) a[st][j] = make_float2(__ldcs(ra + t + 64 * j), __ldcs(rb + t + 64 * j));
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j)
@@ -734,6 +736,11 @@ __global__ void __launch_bounds__(512) lw_cols512_kernel(const __grid_constant__
 #pragma unroll
   for (int j = 0; j < 8; ++j) a[j] = Rc[t + 64 * j];
   fft512_group(a, t, p.t.tw_ny, S1, S2);
+  // The column is consumed (fft512_group synchronises the CTA, so the duplicate reads of a partial block are
+  // done too): drop its 32 dirty lines from L2 instead of letting them be written back to DRAM -- R is scratch,
+  // rewritten by the next slot's row pass.  (Measured: 18.3 MB of DRAM writes per 26-window slot before.)
+  if (grp < cc && t < 32)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(reinterpret_cast<const char*>(Rc) + t * 128) : "memory");
   // crop + window table -> Wg[c][r] (global, column-major); the IFFT along r runs in lw_ifft_y
   const float2* wtab = p.t.win_tab + (size_t)(q * g.L + w) * wh * ww;
   const float2* X0 = reinterpret_cast<const float2*>(smem);
