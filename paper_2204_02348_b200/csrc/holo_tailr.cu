@@ -164,9 +164,18 @@ HOLO_DEV void overlap_y_param(const TailBasis& tb, int q, const float2* Um, int 
 // win: [items][2][42 r][42 c] float, relative to item i0: Re / Im of K1's masked Fourier window
 // (holopipe/pipeline.py:72-127).  CTA (pol q, task): the three windows
 // i0 + q + P (3 task + {0, 1, 2}) (i0 is a multiple of P).
+// Phase timestamps of two CTAs (clock64) for tools/tail_trace.py; compiled in with -DHOLO_TAIL_TRACE only.
+#ifdef HOLO_TAIL_TRACE
+__device__ long long g_tail_trace[2][16];
+#define TAIL_MARK(i) do { if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x / 2)) g_tail_trace[blockIdx.x ? 1 : 0][i] = clock64(); } while (0)
+#else
+#define TAIL_MARK(i) do { } while (0)
+#endif
+
 template <bool PB, class TB>
 HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1, const float* __restrict__ win,
                         const TailRLayout& L, const TB& tb) {
+  TAIL_MARK(0);
   extern __shared__ __align__(16) char smem[];
   __shared__ int s_max[kWin];
   __shared__ float s_scale[kWin];
@@ -228,7 +237,9 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
     }
   }
   float2 v[kN];
+  TAIL_MARK(1);
   mbar_wait(&landed, 0);
+  TAIL_MARK(2);
   {
     const float* wp = reinterpret_cast<const float*>(smem + w3 * L.win_bytes) + s;
 #pragma unroll
@@ -236,7 +247,9 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
       v[r] = valid ? make_float2(wp[r * kN], wp[kN * kN + r * kN]) : make_float2(0.f, 0.f);
   }
   __syncthreads();   // every column is in registers: the landing area becomes T
+  TAIL_MARK(3);
   dft42<true>(v);   // along y (holopipe/pipeline.py:130-149)
+  TAIL_MARK(4);
   float2* T = reinterpret_cast<float2*>(smem + w3 * L.win_bytes);   // [y][kP]
   if (lane_on) {
 #pragma unroll
@@ -249,7 +262,9 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
 #pragma unroll
     for (int c = 0; c < kN; ++c) v[c] = T[s * kP + c];
   }
+  TAIL_MARK(6);
   dft42<true>(v);   // along x; F[y][x] is v[pos_of(x)]
+  TAIL_MARK(7);
   const int b = valid ? item / P : 0;
   float2 bc = make_float2(1.f, 0.f);
   if (p.bcal) bc = p.bcal[(size_t)min(q, p.cal_pols - 1) * p.cal_batch + ((p.row_offset + b) % p.cal_batch)];
@@ -271,7 +286,9 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
     const int mx = __reduce_max_sync(seg, __float_as_int(lmax));   // lmax >= 0: integer order = float order
     if (lane_on && (tid & 31) == __ffs(seg) - 1) atomicMax(&s_max[w3], mx);
   }
+  TAIL_MARK(8);
   __syncthreads();   // every T row has been read: the window's region is free for Fq / U
+  TAIL_MARK(9);
   lmax = __int_as_float(s_max[w3]);
   const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;   // pipeline.py:194-198
   if (valid && p.raw) {
@@ -306,7 +323,9 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
       }
     }
     if constexpr (PB) {   // launched only for symmetric bases of at most kPG orders
+      TAIL_MARK(10);
       overlap_x_param(tb, q, v, U, s);
+      TAIL_MARK(11);
     } else if (xsym) {
 #pragma unroll 1
       for (int mq = 0; mq < GQ; ++mq) {
@@ -359,6 +378,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
   __syncthreads();
 
   // ------------------------------------------------------------------ phase 3 (CTA-wide)
+  TAIL_MARK(12);
   const int item0 = i0 + q + P * (task * kWin);
   // parameter-basis variant: threads 0..47 = (window, m) run the second contraction while the other 80 store
   constexpr int kYThr = PB ? kWin * kPG : 0;
@@ -371,6 +391,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
       float2* out = p.coefs + (size_t)it * g.M;
       if constexpr (PB) overlap_y_param(tb, q, Um, m, G, d, out);
     }
+    TAIL_MARK(13);
     return;
   }
 #pragma unroll 1
@@ -428,6 +449,12 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
     }
   }
 }
+
+#ifdef HOLO_TAIL_TRACE
+extern "C" int hpg_debug_tail_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 __global__ void __launch_bounds__(kThr, 4)
     tail42r_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
