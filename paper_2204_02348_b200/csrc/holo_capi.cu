@@ -644,6 +644,22 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   if (hxv.empty()) hxv.push_back(0.f);
   if (hyv.empty()) hyv.push_back(0.f);
   const size_t o_hx = push(blob, hxv), o_hy = push(blob, hyv);
+  // half tables of the register-resident tail (holo_tailr.cu): [pol][x | y][22 rows: axis index 0, then
+  // n/2 .. n-1][16 orders], transposed and zero-padded, for 42-point axes and at most 16 orders
+  std::vector<float> half_tab;
+  if (G > 0 && G <= 16 && g.gw == 42 && g.gh == 42) {
+    half_tab.assign((size_t)g.P * 2 * 22 * 16, 0.f);
+    for (int q = 0; q < g.P; ++q)
+      for (int ax = 0; ax < 2; ++ax)
+        for (int j = 0; j < 22; ++j)
+          for (int m = 0; m < G; ++m) {
+            const int x = j == 0 ? 0 : 20 + j;
+            half_tab[(((size_t)q * 2 + ax) * 22 + j) * 16 + m] = (ax == 0 ? P->hx : P->hy)[((size_t)q * G + m) * 42 + x];
+          }
+  }
+  const bool half_ok = !half_tab.empty();
+  if (half_tab.empty()) half_tab.push_back(0.f);
+  const size_t o_half = push(blob, half_tab);
   const size_t o_xa = push(blob, P->xa), o_ya = push(blob, P->ya);
   std::vector<double> xad(P->xa.begin(), P->xa.end()), yad(P->ya.begin(), P->ya.end());
   const size_t o_xad = push(blob, xad), o_yad = push(blob, yad);
@@ -685,8 +701,7 @@ int hpg_plan_create(const hpg_plan_desc* d, hpg_plan** out) {
   P->ft.tco_gp = tco_ok ? GP16 : 0;
   // HG parity on the symmetric part of the field axes (pipeline.py:152-160 puts the origin at index w / 2),
   // verified bit for bit on the quantised profiles: the fast kernel then folds each +-d pair of the overlap
-  P->ft.hx_host = P->hx.empty() ? nullptr : P->hx.data();
-  P->ft.hy_host = P->hy.empty() ? nullptr : P->hy.data();
+  P->ft.half_tab = half_ok ? reinterpret_cast<const float*>(base + o_half) : nullptr;
   P->ft.hsym = 0;
   for (int q = 0; q < g.P && G > 0; ++q) {
     for (int ax = 0; ax < 2; ++ax) {

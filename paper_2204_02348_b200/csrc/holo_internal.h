@@ -43,8 +43,8 @@ struct FastTables {
   const uint4* tco_img;    // [P][hx hi, hx lo, hy hi, hy lo][GP16 x 48 halves]: exact fp16 split of the int16 basis
   const float* tco_inv;    // [P][2][GP16] 1 / per-order basis scale (x, y)
   int tco_gp;              // GP16 (0: tensor-core overlap unavailable)
-  const float* hx_host;    // HOST copies of the dequantised basis [P][G][gw] / [P][G][gh] (kernel-parameter basis of
-  const float* hy_host;    // holo_tailr.cu); never dereferenced on the device
+  const float* half_tab;   // [P][x | y][22][16]: transposed half profiles (axis index 0, then n/2..n-1) of the
+                           // register-resident tail (holo_tailr.cu); null unless G <= 16 on 42-point axes
   int hsym;                // bit 2q: pol q's x profiles satisfy h_m(c - d) = (-1)^m h_m(c + d) exactly on the
                            // quantised basis (c = gw / 2, the axis origin); bit 2q + 1: the y profiles
 };

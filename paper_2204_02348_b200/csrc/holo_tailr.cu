@@ -85,60 +85,63 @@ inline TailRLayout tailr_layout(int G) {
   return L;
 }
 
-// Basis profiles passed as a kernel parameter (constant bank): with every index a compile-time constant the
-// overlap FMAs take their basis value as a constant operand -- no loads, no registers, no shared memory,
-// which lets five CTAs fit an SM (the whole 2,000-window dual-pol batch resident in one wave).
-constexpr int kPG = 16;   // padded order count of the parameter-basis variant
-struct TailBasis {
-  float hx[kMaxPol][kN * kPG];   // [pol][x][m], zero beyond G
-  float hy[kMaxPol][kN * kPG];   // [pol][y][n]
-};
-struct NoBasis {
-  int unused;
-};
+// Small symmetric bases (G <= 16, HG parity on both axes: every batch the two-kernel path is chosen for): only
+// x = 0 and x >= 21 of the transposed profiles are needed, 22 rows x 16 orders = 1.4 KB per axis -- small enough
+// for the spare 1.7 KB behind Fq + U in a window's region.  With no basis region of its own the CTA needs
+// 44 KB of shared memory and five fit an SM: the whole 2,000-window batch is resident in a single wave.
+// (Round 2 first passed these tables as a kernel parameter so that the FMAs took them as constant operands;
+// the constant loads of 20 warps walking a 5.4 KB table thrashed the constant cache -- the first contraction
+// took 17 K of the CTA's 53 K cycles, tools/tail_trace.py.)
+constexpr int kPG = 16;                        // padded order count of the half tables
+constexpr int kHalfRows = kN / 2 + 1;          // row 0: x = 0; row 1 + d: x = 21 + d, d = 0..20
+constexpr int kHalfOff = (kN * kP * 4 + kPG * kP * 8 + 15) & ~15;   // behind Fq + U
+static_assert(kHalfOff + kHalfRows * kPG * 4 <= kN * kP * 8, "the half table must fit the window region");
 
 namespace {
 
-// U[m][y = s] = sum_x F[y][x] hx[m][x] for the x-symmetric basis of pol Q; v holds the folded row
-// (v[pos(21 + d)] = F(21 + d) + F(21 - d), v[pos(21 - d)] = the difference, d = 1..20; x = 21 and x = 0 plain)
-// (q and mq are warp-uniform: the basis values come through uniform-register constant loads, one code copy)
-HOLO_DEV void overlap_x_param(const TailBasis& tb, int q, const float2 (&v)[kN], float2* U, int s) {
+// U[m][y = s] = sum_x F[y][x] hx[m][x] for an x-symmetric basis; v holds the folded row (v[pos(21 + d)] =
+// F(21 + d) + F(21 - d), v[pos(21 - d)] = the difference, d = 1..20; x = 21 and x = 0 plain); hxh: half table.
+// Two orders (one even, one odd) per pass: four accumulators and one 8-byte basis load live next to the row.
+HOLO_DEV void overlap_x_half(const float* __restrict__ hxh, const float2 (&v)[kN], float2* U, int s) {
   constexpr int CX = kN / 2;
 #pragma unroll 1
-  for (int mq = 0; mq < kPG / 4; ++mq) {
-    float ar[4], ai[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float h0 = tb.hx[q][CX * kPG + 4 * mq + j], h1 = tb.hx[q][4 * mq + j];
-      ar[j] = fmaf(v[pos_of(0)].x, h1, v[pos_of(CX)].x * h0);
-      ai[j] = fmaf(v[pos_of(0)].y, h1, v[pos_of(CX)].y * h0);
-    }
+  for (int mp = 0; mp < kPG / 2; ++mp) {
+    const float* hq = hxh + 2 * mp;
+    const float2 h1 = *reinterpret_cast<const float2*>(hq), h0 = *reinterpret_cast<const float2*>(hq + kPG);
+    float2 ae = make_float2(fmaf(v[pos_of(0)].x, h1.x, v[pos_of(CX)].x * h0.x),
+                            fmaf(v[pos_of(0)].y, h1.x, v[pos_of(CX)].y * h0.x));
+    float2 ao = make_float2(fmaf(v[pos_of(0)].x, h1.y, v[pos_of(CX)].x * h0.y),
+                            fmaf(v[pos_of(0)].y, h1.y, v[pos_of(CX)].y * h0.y));
 #pragma unroll
     for (int d = 1; d < CX; ++d) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {   // even orders take the sums, odd orders the differences
-        const float2 a = (j & 1) ? v[pos_of(CX - d)] : v[pos_of(CX + d)];
-        const float h = tb.hx[q][(CX + d) * kPG + 4 * mq + j];
-        ar[j] = fmaf(a.x, h, ar[j]);
-        ai[j] = fmaf(a.y, h, ai[j]);
-      }
+      const float2 h = *reinterpret_cast<const float2*>(hq + (1 + d) * kPG);
+      const float2 sv = v[pos_of(CX + d)], dv = v[pos_of(CX - d)];   // even order: sums, odd order: differences
+      ae.x = fmaf(sv.x, h.x, ae.x);
+      ae.y = fmaf(sv.y, h.x, ae.y);
+      ao.x = fmaf(dv.x, h.y, ao.x);
+      ao.y = fmaf(dv.y, h.y, ao.y);
     }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) U[(4 * mq + j) * kP + s] = make_float2(ar[j], ai[j]);
+    U[(2 * mp) * kP + s] = ae;
+    U[(2 * mp + 1) * kP + s] = ao;
   }
 }
 
-// c[m, n] = sum_y U[m][y] hy[n][y] for every n of one (window, m), y-symmetric basis of pol Q
-HOLO_DEV void overlap_y_param(const TailBasis& tb, int q, const float2* Um, int m, int G, float d, float2* out) {
+// c[m, n] = sum_y U[m][y] hy[n][y] for every n of one (window, m), y-symmetric basis; hyh: half table
+HOLO_DEV void overlap_y_half(const float* __restrict__ hyh, const float2* Um, int m, int G, float d, float2* out) {
   constexpr int CY = kN / 2;
   float ax[kPG], ay[kPG];
   {
     const float2 u0 = Um[CY], u1 = Um[0];
 #pragma unroll
-    for (int n = 0; n < kPG; ++n) {
-      const float h0 = tb.hy[q][CY * kPG + n], h1 = tb.hy[q][n];
-      ax[n] = fmaf(u1.x, h1, u0.x * h0);
-      ay[n] = fmaf(u1.y, h1, u0.y * h0);
+    for (int n4 = 0; n4 < kPG / 4; ++n4) {
+      const float4 a1 = *reinterpret_cast<const float4*>(hyh + 4 * n4);
+      const float4 a0 = *reinterpret_cast<const float4*>(hyh + kPG + 4 * n4);
+      const float h1v[4] = {a1.x, a1.y, a1.z, a1.w}, h0v[4] = {a0.x, a0.y, a0.z, a0.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ax[4 * n4 + j] = fmaf(u1.x, h1v[j], u0.x * h0v[j]);
+        ay[4 * n4 + j] = fmaf(u1.y, h1v[j], u0.y * h0v[j]);
+      }
     }
   }
 #pragma unroll 4
@@ -146,10 +149,15 @@ HOLO_DEV void overlap_y_param(const TailBasis& tb, int q, const float2* Um, int 
     const float2 vp = Um[CY + dd], vm = Um[CY - dd];
     const float2 se = cadd(vp, vm), so = csub(vp, vm);
 #pragma unroll
-    for (int n = 0; n < kPG; ++n) {
-      const float h = tb.hy[q][(CY + dd) * kPG + n];
-      ax[n] = fmaf((n & 1) ? so.x : se.x, h, ax[n]);
-      ay[n] = fmaf((n & 1) ? so.y : se.y, h, ay[n]);
+    for (int n4 = 0; n4 < kPG / 4; ++n4) {
+      const float4 h4 = *reinterpret_cast<const float4*>(hyh + (1 + dd) * kPG + 4 * n4);
+      const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = 4 * n4 + j;
+        ax[n] = fmaf((n & 1) ? so.x : se.x, hv[j], ax[n]);
+        ay[n] = fmaf((n & 1) ? so.y : se.y, hv[j], ay[n]);
+      }
     }
   }
 #pragma unroll
@@ -172,9 +180,9 @@ __device__ long long g_tail_trace[2][16];
 #define TAIL_MARK(i) do { } while (0)
 #endif
 
-template <bool PB, class TB>
+template <bool PB>
 HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1, const float* __restrict__ win,
-                        const TailRLayout& L, const TB& tb) {
+                        const TailRLayout& L) {
   TAIL_MARK(0);
   extern __shared__ __align__(16) char smem[];
   __shared__ int s_max[kWin];
@@ -289,6 +297,23 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
   TAIL_MARK(8);
   __syncthreads();   // every T row has been read: the window's region is free for Fq / U
   TAIL_MARK(9);
+  float* hxh = reinterpret_cast<float*>(smem + kHalfOff);                 // spare space of window 0's region
+  float* hyh = reinterpret_cast<float*>(smem + L.win_bytes + kHalfOff);   // ... of window 1's region
+  if (PB && G > 0 && tid == 0) {   // the two half tables of this pol by bulk copy behind the int16 rounding
+    constexpr uint32_t kHalfBytes = kHalfRows * kPG * 4;
+    const float* src = ft.half_tab + (size_t)q * 2 * kHalfRows * kPG;
+    fence_async_smem();   // the regions were last touched through the generic proxy (T)
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&landed)), "r"(2 * kHalfBytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(hxh)),
+                 "l"(src), "r"(kHalfBytes), "r"(smem_u32(&landed))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(hyh)),
+                 "l"(src + kHalfRows * kPG), "r"(kHalfBytes), "r"(smem_u32(&landed))
+                 : "memory");
+  }
   lmax = __int_as_float(s_max[w3]);
   const float scale = lmax > 0.f ? (float)(32767.0 / (double)lmax) : 1.0f;   // pipeline.py:194-198
   if (valid && p.raw) {
@@ -310,6 +335,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
   if (valid && s == 0) p.scale[item] = scale;
 
   // ------------------------------------------- first overlap contraction, from registers (row y = s)
+  if (PB && G > 0) mbar_wait(&landed, 1);   // the half tables have landed (second phase of the barrier)
   if (G > 0 && lane_on) {
     constexpr int CX = kN / 2;   // axis origin x = 21: x = 21 +- d for d = 1..20, plus x = 21 and x = 0
     const bool xsym = (ft.hsym >> (2 * q)) & 1;
@@ -324,7 +350,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
     }
     if constexpr (PB) {   // launched only for symmetric bases of at most kPG orders
       TAIL_MARK(10);
-      overlap_x_param(tb, q, v, U, s);
+      overlap_x_half(hxh, v, U, s);
       TAIL_MARK(11);
     } else if (xsym) {
 #pragma unroll 1
@@ -389,7 +415,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
       const float2* Um = reinterpret_cast<const float2*>(smem + w * L.win_bytes + kN * kP * 4) + m * kP;
       const float d = __fdiv_rn(g.dxdy[q], s_scale[w]);
       float2* out = p.coefs + (size_t)it * g.M;
-      if constexpr (PB) overlap_y_param(tb, q, Um, m, G, d, out);
+      if constexpr (PB) overlap_y_half(hyh, Um, m, G, d, out);
     }
     TAIL_MARK(13);
     return;
@@ -459,14 +485,14 @@ extern "C" int hpg_debug_tail_trace(long long* out) {
 __global__ void __launch_bounds__(kThr, 4)
     tail42r_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
                    const float* __restrict__ win, TailRLayout L) {
-  tail_body<false>(p, ft, i0, i1, win, L, NoBasis{0});
+  tail_body<false>(p, ft, i0, i1, win, L);
 }
 
-// parameter-basis variant: symmetric bases of at most kPG orders, five CTAs per SM
+// half-table variant: symmetric bases of at most kPG orders, five CTAs per SM
 __global__ void __launch_bounds__(kThr, 5)
     tail42p_kernel(const __grid_constant__ RunParams p, const __grid_constant__ FastTables ft, int i0, int i1,
-                   const float* __restrict__ win, TailRLayout L, const __grid_constant__ TailBasis tb) {
-  tail_body<true>(p, ft, i0, i1, win, L, tb);
+                   const float* __restrict__ win, TailRLayout L) {
+  tail_body<true>(p, ft, i0, i1, win, L);
 }
 
 bool tailr_supported(const Geometry& g, const void* rcal) {
@@ -489,22 +515,13 @@ cudaError_t launch_tailr(const RunParams& p, const FastTables& ft, cudaStream_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const bool all_sym = (ft.hsym & ((1 << (2 * P)) - 1)) == (1 << (2 * P)) - 1;
-  const char* env = getenv("HOLO_TAILR_SMEM_BASIS");   // diagnostic: keep the shared-memory basis variant
-  if (G > 0 && G <= kPG && all_sym && ft.hx_host && ft.hy_host && !(env && env[0] == '1')) {
-    TailRLayout L = tailr_layout(0);   // no basis in shared memory; U of kPG orders fits the window region
-    static_assert(kN * kP * 4 + kPG * kP * 8 <= kN * kP * 8, "Fq + U must fit the window region");
-    TailBasis tb;
-    for (int q = 0; q < kMaxPol; ++q)
-      for (int x = 0; x < kN; ++x)
-        for (int m = 0; m < kPG; ++m) {
-          const bool on = q < P && m < G;
-          tb.hx[q][x * kPG + m] = on ? ft.hx_host[((size_t)q * G + m) * kN + x] : 0.f;
-          tb.hy[q][x * kPG + m] = on ? ft.hy_host[((size_t)q * G + m) * kN + x] : 0.f;
-        }
+  const char* env = getenv("HOLO_TAILR_SMEM_BASIS");   // diagnostic: keep the full shared-memory basis variant
+  if (G > 0 && G <= kPG && all_sym && ft.half_tab && !(env && env[0] == '1')) {
+    TailRLayout L = tailr_layout(0);   // no basis region: the half tables live behind Fq + U of windows 0 and 1
     cudaError_t e = ensure_smem_optin((const void*)tail42p_kernel, (size_t)L.total);
     if (e != cudaSuccess) return e;
     cfg.dynamicSmemBytes = (size_t)L.total;
-    return cudaLaunchKernelEx(&cfg, tail42p_kernel, p, ft, i0, i1, win, L, tb);
+    return cudaLaunchKernelEx(&cfg, tail42p_kernel, p, ft, i0, i1, win, L);
   }
   const TailRLayout L = tailr_layout(G);
   cudaError_t e = ensure_smem_optin((const void*)tail42r_kernel, (size_t)L.total);
