@@ -233,6 +233,43 @@ def test_two_kernel_tensor_core_path_matches_reference(name):
     assert rel_l2_rows(coefs, g["coefs"]) <= COEF_TOL
 
 
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_two_kernel_flag_on_every_case(name):
+    """HPG_FLAG_TC2 on every golden case: where the two-kernel path applies (128 window, 42 x 42 field, one
+    wavelength, no reference calibration / fill factor / averaging) it must match the reference, and where it
+    does not hpg_run must fall back to the kernel that does."""
+    case, g, frames = load(name)
+    eng = _engine(case, frames)
+    eng.use_tc2 = True
+    _run(eng, case)
+    fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
+    ef = rel_l2_rows(dequant(fr, fi, sc), dequant(g["fr"], g["fi"], g["scale"]))
+    assert ef <= FIELD_TOL, f"{name}: field rel L2 {ef:.3e}"
+    assert max(np.abs(fr.astype(int) - g["fr"]).max(), np.abs(fi.astype(int) - g["fi"]).max()) <= 2
+    if "coefs" in g:
+        coefs, _, _, _ = eng.coef_view()
+        assert rel_l2_rows(coefs, g["coefs"]) <= COEF_TOL
+
+
+def test_two_kernel_tail_variants_agree(monkeypatch):
+    """The half-table tail (five CTAs per SM) and the full shared-memory-basis tail (the variant of large or
+    non-symmetric bases) on the same windows: same int16 fields, coefficients to 2e-6."""
+    case, g, frames = load("dualpol")
+    a = _engine(case, frames)
+    a.use_tc2 = True
+    a.run_pipeline(0)
+    fa = _outputs(a)
+    monkeypatch.setenv("HOLO_TAILR_SMEM_BASIS", "1")
+    b = _engine(case, frames)
+    b.use_tc2 = True
+    b.run_pipeline(0)
+    fb = _outputs(b)
+    for x, y in zip(fa[:3], fb[:3]):
+        assert np.array_equal(x, y)
+    assert rel_l2_rows(fa[3], fb[3]) <= 2e-6
+    assert rel_l2_rows(fb[3], g["coefs"]) <= COEF_TOL
+
+
 def _outputs(eng):
     out = [t.cpu().numpy().copy() for t in eng.fields16_device()]
     co = eng.coefs_device()
