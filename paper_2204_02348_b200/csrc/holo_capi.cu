@@ -322,17 +322,39 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
     }
   }
   if (a_tc.empty()) a_tc.push_back(0u);
-  // the same matrix with packed, interleaved rows for the two-kernel path (holo_tc2.cu): row 2c -> Re, 2c + 1 -> Im
+  // the same matrix with packed, interleaved rows for the two-kernel path (holo_tc2.cu): row 2c -> Re, 2c + 1 -> Im;
+  // the fill-factor envelope (pipeline.py:99-103; separable inside the Nyquist band, see the fast-path tables
+  // in hpg_plan_create) is folded into the rows here and into the rows of the column-DFT matrix below
+  auto env = [&](int k, int n) {   // 1 / sinc of the signed bin k of an n-point axis
+    if (!P->fill) return 1.0;
+    int t = k % n;
+    if (t < 0) t += n;
+    return 1.0 / sinc((double)(t <= n / 2 ? t : n - t) / n);
+  };
   std::vector<uint32_t> a_tcp;
   if (g.nx == 128 && g.ww <= 64) {
     a_tcp.assign((size_t)g.P * 2 * 128 * 64, 0u);
-    for (int q = 0; q < g.P; ++q)
+    for (int q = 0; q < g.P; ++q) {
+      const int kx = g.k0[q][0][0];
       for (int n = 0; n < 2 * g.ww; ++n) {
-        const int src = (n & 1) ? 64 + (n >> 1) : (n >> 1);
-        for (int part = 0; part < 2; ++part)
-          for (int x2 = 0; x2 < 64; ++x2)
-            a_tcp[(((size_t)q * 2 + part) * 64 + x2) * 128 + n] = a_tc[(((size_t)q * 2 + part) * 64 + x2) * 128 + src];
+        const int c = n >> 1;
+        const double kc = (double)(kx + c - g.ww / 2), ex = env(kx + c - g.ww / 2, g.nx);
+        for (int x2 = 0; x2 < 64; ++x2) {
+          uint16_t hh[2], ll[2];
+          for (int e = 0; e < 2; ++e) {
+            const int x = 2 * x2 + e;
+            const double ang = -2.0 * kPi * kc * ((double)x - xi[q][0] + g.nx / 2.0) / g.nx;
+            const double v = ((n & 1) ? std::sin(ang) : std::cos(ang)) * ex;
+            const __half h = __double2half(v);
+            const __half l = __double2half(v - (double)__half2float(h));
+            hh[e] = __half_as_ushort(h);
+            ll[e] = __half_as_ushort(l);
+          }
+          a_tcp[(((size_t)q * 2 + 0) * 64 + x2) * 128 + n] = (uint32_t)hh[0] | ((uint32_t)hh[1] << 16);
+          a_tcp[(((size_t)q * 2 + 1) * 64 + x2) * 128 + n] = (uint32_t)ll[0] | ((uint32_t)ll[1] << 16);
+        }
       }
+    }
   }
   if (a_tcp.empty()) a_tcp.push_back(0u);
   // tensor-core column DFT (holo_tc2.cu): rows r < wh -> Cr, rows 64 + r -> Ci of
@@ -378,10 +400,10 @@ static cudaError_t ensure_tc_tables(const hpg_plan* Pc) {
       for (int n = 0; n < 96; ++n) {
         const int r = n % 48;
         if (r >= g.wh) continue;
-        const double kr = (double)(ky + r - g.wh / 2);
+        const double kr = (double)(ky + r - g.wh / 2), ey = env(ky + r - g.wh / 2, g.ny);
         for (int y = 0; y < 128; ++y) {
           const double ang = -2.0 * kPi * kr * ((double)y - xi[q][1] + g.ny / 2.0) / g.ny;
-          const double v = n < 48 ? std::cos(ang) : std::sin(ang);
+          const double v = (n < 48 ? std::cos(ang) : std::sin(ang)) * ey;
           const __half h = __double2half(v);
           const __half l = __double2half(v - (double)__half2float(h));
           const size_t off = (size_t)(y >> 4) * (12 * 128) + ((size_t)(n >> 3) * 2 + ((y >> 3) & 1)) * 64 +

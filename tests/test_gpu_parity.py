@@ -509,3 +509,18 @@ def test_fill_factor_in_the_fast_kernel_matches_generic(name):
     assert np.abs(a[0].astype(int) - b[0]).max() <= 2 and np.abs(a[1].astype(int) - b[1]).max() <= 2
     assert np.allclose(a[2], b[2], rtol=1e-5)
     assert rel_l2_rows(a[3], b[3]) <= 2e-5
+    # ... and folded into the DFT matrices of the two-kernel tensor-core path
+    from paper_2204_02348_b200 import native
+    eng.force_generic = False
+    eng.use_tc2 = True
+    eng.run_pipeline(0)
+    assert native.lib().hpg_last_launch_count() == 2
+    c = [t.cpu().numpy() for t in eng.fields16_device()] + [eng.coefs_device().cpu().numpy()]
+    assert np.abs(c[0].astype(int) - b[0]).max() <= 2 and np.abs(c[1].astype(int) - b[1]).max() <= 2
+    assert np.allclose(c[2], b[2], rtol=1e-5)
+    assert rel_l2_rows(c[3], b[3]) <= 2e-5
+    # the correction is not a no-op on these frames: without it the fields differ
+    off = _engine(dict(case, config=dict(case["config"], fillFactorCorrectionEnabled=0)), frames)
+    off.run_pipeline(0)
+    d = [t.cpu().numpy() for t in off.fields16_device()]
+    assert rel_l2_rows(dequant(d[0], d[1], d[2]), dequant(b[0], b[1], b[2])) > 1e-3
