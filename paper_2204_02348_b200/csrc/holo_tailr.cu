@@ -496,8 +496,9 @@ __global__ void __launch_bounds__(kThr, 5)
 }
 
 bool tailr_supported(const Geometry& g, const void* rcal) {
+  (void)rcal;   // applied with the removal phase (one wavelength: table q of the calibration)
   return g.wh == kN && g.ww == kN && g.gh == kN && g.gw == kN && g.G <= 48 && g.L == 1 && g.P <= kMaxPol &&
-         rcal == nullptr && tailr_layout(g.G).total <= 110 * 1024;
+         tailr_layout(g.G).total <= 110 * 1024;
 }
 
 cudaError_t launch_tailr(const RunParams& p, const FastTables& ft, cudaStream_t s, int i0, int i1, const float* win) {

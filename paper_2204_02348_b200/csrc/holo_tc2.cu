@@ -656,10 +656,11 @@ constexpr int kTc2Chunk = 2048;   // items per K1/K2 pair: the product planes (2
 bool tc2_supported(const Geometry& g, int A, int fmt, int transpose, int fill, const void* rcal, unsigned flags,
                    const void* windows) {
   (void)fill;   // the fill-factor envelope is folded into the DFT matrices (ensure_tc_tables)
+  (void)rcal;   // the reference calibration (one wavelength here) is applied by the tail with the removal phase
   const int es = fmt == 1 ? 2 : 4;
   const bool aligned = (g.W * es) % 16 == 0;   // TMA tensor map: 16-byte row stride
   return g.nx == 128 && g.ny == 128 && g.wh == 42 && g.ww == 42 && g.gh == 42 && g.gw == 42 && A == 1 &&
-         g.L == 1 && g.G <= FieldLayout<42, 42>::GMAX && !(fmt == 1 && transpose) && rcal == nullptr &&
+         g.L == 1 && g.G <= FieldLayout<42, 42>::GMAX && !(fmt == 1 && transpose) &&
          (flags & 1u) == 0 && windows == nullptr && aligned;
 }
 

@@ -238,10 +238,15 @@ def test_two_kernel_flag_on_every_case(name):
     """HPG_FLAG_TC2 on every golden case: where the two-kernel path applies (128 window, 42 x 42 field, one
     wavelength, no reference calibration / fill factor / averaging) it must match the reference, and where it
     does not hpg_run must fall back to the kernel that does."""
+    from paper_2204_02348_b200 import native
     case, g, frames = load(name)
     eng = _engine(case, frames)
     eng.use_tc2 = True
     _run(eng, case)
+    # the cases the two-kernel path must take (two launches): bases of 4 to 45 orders, LG / custom transforms,
+    # batch calibration, reference calibration of one wavelength
+    if name in {"custom", "dualpol", "dualpol_cal", "dualpol_g24", "largebasis", "lg", "pr1", "refcal_int"}:
+        assert native.lib().hpg_last_launch_count() == 2, name
     fr, fi, sc = (t.cpu().numpy() for t in eng.fields16_device())
     ef = rel_l2_rows(dequant(fr, fi, sc), dequant(g["fr"], g["fi"], g["scale"]))
     assert ef <= FIELD_TOL, f"{name}: field rel L2 {ef:.3e}"
