@@ -275,6 +275,38 @@ def test_two_kernel_tail_variants_agree(monkeypatch):
     assert rel_l2_rows(fb[3], g["coefs"]) <= COEF_TOL
 
 
+def test_frames_from_a_file_match_the_uint16_buffer(tmp_path):
+    """set_frame_buffer_from_file (holopipe/frames.py:61-75: raw little-endian uint16): same outputs as the same
+    integers handed over as a uint16 buffer, through the handle API."""
+    from paper_2204_02348_b200 import api
+    from paper_2204_02348_b200.errors import ErrorCode
+    case, g, frames = load("dualpol")
+    u16 = np.rint(frames).astype("<u2")
+    path = tmp_path / "frames.bin"
+    u16.tofile(path)
+
+    def run(setter):
+        h = api.create_handle()
+        eng = api.engine(h)
+        for k, v in case["config"].items():
+            setattr(eng.config, k, v)
+        assert setter(h) == ErrorCode.SUCCESS
+        coefs, b, m, p = api.process_batch(h)
+        fields = api.get_fields16(h)[:3]
+        api.destroy_handle(h)
+        return coefs, fields
+
+    ca, fa = run(lambda h: api.set_frame_buffer_from_file(h, str(path)))
+    cb, fb = run(lambda h: api.set_frame_buffer_uint16(h, u16))
+    assert np.array_equal(ca, cb)
+    for x, y in zip(fa, fb):
+        assert np.array_equal(x, y)
+    assert rel_l2_rows(ca, g["coefs"]) <= COEF_TOL
+    h = api.create_handle()
+    assert api.set_frame_buffer_from_file(h, str(tmp_path / "missing.bin")) == ErrorCode.FILENOTFOUND
+    api.destroy_handle(h)
+
+
 def _outputs(eng):
     out = [t.cpu().numpy().copy() for t in eng.fields16_device()]
     co = eng.coefs_device()
