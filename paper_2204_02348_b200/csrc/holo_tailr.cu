@@ -280,13 +280,22 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
   float lmax = 0.f;
   {
     const float2 eyq = sey[s];
+    if (!p.bcal && !rc) {   // the common case without its 8 predicated-off multiplies and a load per sample
 #pragma unroll
-    for (int x = 0; x < kN; ++x) {
-      float2 o = cmul(cmul(v[pos_of(x)], eyq), sex[x]);   // same operation order as ct_stage_final_rows
-      if (p.bcal) o = cmul(o, bc);
-      if (rc) o = cmul(o, __ldg(&rc[s * kN + x]));   // reference calibration (engine.py:250-255)
-      lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
-      v[pos_of(x)] = o;
+      for (int x = 0; x < kN; ++x) {
+        const float2 o = cmul(cmul(v[pos_of(x)], eyq), sex[x]);   // same operation order as ct_stage_final_rows
+        lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
+        v[pos_of(x)] = o;
+      }
+    } else {
+#pragma unroll
+      for (int x = 0; x < kN; ++x) {
+        float2 o = cmul(cmul(v[pos_of(x)], eyq), sex[x]);
+        if (p.bcal) o = cmul(o, bc);
+        if (rc) o = cmul(o, __ldg(&rc[s * kN + x]));   // reference calibration (engine.py:250-255)
+        lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
+        v[pos_of(x)] = o;
+      }
     }
   }
   {   // peak of each window: lanes of one warp belong to at most two windows
