@@ -102,10 +102,10 @@ namespace {
 // U[m][y = s] = sum_x F[y][x] hx[m][x] for an x-symmetric basis; v holds the folded row (v[pos(21 + d)] =
 // F(21 + d) + F(21 - d), v[pos(21 - d)] = the difference, d = 1..20; x = 21 and x = 0 plain); hxh: half table.
 // Two orders (one even, one odd) per pass: four accumulators and one 8-byte basis load live next to the row.
-HOLO_DEV void overlap_x_half(const float* __restrict__ hxh, const float2 (&v)[kN], float2* U, int s) {
+HOLO_DEV void overlap_x_half(const float* __restrict__ hxh, const float2 (&v)[kN], float2* U, int s, int G) {
   constexpr int CX = kN / 2;
 #pragma unroll 1
-  for (int mp = 0; mp < kPG / 2; ++mp) {
+  for (int mp = 0; 2 * mp < G; ++mp) {   // the zero-padded orders beyond G are never read back
     const float* hq = hxh + 2 * mp;
     const float2 h1 = *reinterpret_cast<const float2*>(hq), h0 = *reinterpret_cast<const float2*>(hq + kPG);
     float2 ae = make_float2(fmaf(v[pos_of(0)].x, h1.x, v[pos_of(CX)].x * h0.x),
@@ -359,7 +359,7 @@ HOLO_DEV void tail_body(const RunParams& p, const FastTables& ft, int i0, int i1
     }
     if constexpr (PB) {   // launched only for symmetric bases of at most kPG orders
       TAIL_MARK(10);
-      overlap_x_half(hxh, v, U, s);
+      overlap_x_half(hxh, v, U, s, G);
       TAIL_MARK(11);
     } else if (xsym) {
 #pragma unroll 1
