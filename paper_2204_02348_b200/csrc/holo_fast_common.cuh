@@ -69,6 +69,16 @@ HOLO_DEV float ct_stage_final_rows(const float2* __restrict__ src, float2* __res
     for (int j = 1; j < P; ++j) v[j] = cmul(v[j], twid<true>(tw[kWrap ? (j * k) % N : j * k]));
     dft_fixed<P, true>(v);
     const float2 eyq = cscale(ey[y], osc);
+    if (!use_bc && !rc) {   // the common case, without the predicated-off calibration multiplies
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const int x = k + L * t;
+        const float2 o = cmul(cmul(v[t], eyq), ex[x]);
+        lmax = fmaxf(lmax, fmaxf(fabsf(o.x), fabsf(o.y)));
+        dst[y * N + x] = o;
+      }
+      continue;
+    }
 #pragma unroll
     for (int t = 0; t < P; ++t) {
       const int x = k + L * t;
